@@ -1,0 +1,436 @@
+// wq_api.cu -- the C-ABI of include/wq.h: validation, plan sizing and
+// allocation, stream-ordered launches of the kernels, error reporting, and
+// the host-buffer end-to-end call.  Host logic only; every arithmetic step of
+// the WQ path runs in the CUDA kernels of this directory.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <atomic>
+#include <vector>
+#include "wq_internal.cuh"
+
+namespace {
+thread_local std::string g_err;
+
+inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int64_t host_knot_pos(int64_t e, int64_t E, int p, int64_t nq) {
+    if (e <= 0) return 0;
+    if (e >= E) return nq - 1;
+    return p + 2 * e;
+}
+int64_t host_nq(int64_t E, int p) { return E >= 2 ? 2 * E + 2 * p + 1 : p + 3; }
+int64_t host_qlo(int64_t i, int64_t E, int p) { return host_knot_pos(i - p, E, p, host_nq(E, p)) + 1; }
+int64_t host_qhi(int64_t i, int64_t E, int p) {
+    return host_knot_pos(i + 1 < E ? i + 1 : E, E, p, host_nq(E, p)) - 1;
+}
+int64_t host_pref(int64_t i, int p, int64_t n) {
+    int64_t s = 0;
+    for (int64_t k = 0; k < i; ++k) s += wq_ni(k, p, n);
+    return s;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+wq_status fail(wq_status st, const std::string &msg) {
+    g_err = msg;
+    return st;
+}
+}  // namespace
+
+static std::atomic<uint64_t> g_launches{0};
+void wq_count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+void wq_set_error(const std::string &msg) { g_err = msg; }
+
+wq_status wq_cuda_status(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return WQ_OK;
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return WQ_ECUDA;
+}
+
+extern "C" {
+
+const char *wq_status_string(wq_status s) {
+    switch (s) {
+    case WQ_OK: return "WQ_OK";
+    case WQ_EINVAL: return "WQ_EINVAL: invalid argument";
+    case WQ_EKNOTS: return "WQ_EKNOTS: invalid knot vector";
+    case WQ_ESINGULAR: return "WQ_ESINGULAR: WQ exactness system has no solution";
+    case WQ_EGEOMETRY: return "WQ_EGEOMETRY: det J vanishes or changes sign";
+    case WQ_ENOMEM: return "WQ_ENOMEM: device allocation failed";
+    case WQ_ECUDA: return "WQ_ECUDA: CUDA error";
+    case WQ_ERANGE: return "WQ_ERANGE: index out of range";
+    }
+    return "unknown status";
+}
+
+const char *wq_last_error(void) { return g_err.c_str(); }
+
+const char *wq_version(void) { return "libwq sm_100a " __DATE__ " " __TIME__; }
+
+uint64_t wq_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
+    if (!out) return fail(WQ_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!desc) return fail(WQ_EINVAL, "desc is NULL");
+    const int d = desc->d, p = desc->p;
+    if (d < 1 || d > 3) return fail(WQ_EINVAL, "d must be 1, 2 or 3");
+    if (p < 1 || p > WQ_MAX_DEGREE) return fail(p < 1 ? WQ_EKNOTS : WQ_EINVAL, "p must be in [1, WQ_MAX_DEGREE]");
+    if (!desc->n_knots || !desc->knots) return fail(WQ_EINVAL, "knots are NULL");
+    if (!desc->need_mass && !desc->need_stiffness) return fail(WQ_EINVAL, "need_mass or need_stiffness required");
+    wq_plan_s *P = new wq_plan_s();
+    memset(P, 0, sizeof(*P));
+    P->d = d;
+    P->p = p;
+    P->device = desc->device;
+    P->need_mass = desc->need_mass ? 1 : 0;
+    P->need_stiff = desc->need_stiffness ? 1 : 0;
+    // ---- validate knots
+    for (int l = 0; l < d; ++l) {
+        int64_t nk = desc->n_knots[l];
+        const double *xi = desc->knots[l];
+        if (!xi) { delete P; return fail(WQ_EINVAL, "knot vector is NULL"); }
+        int64_t E = nk - 2 * (int64_t)p - 1;
+        if (E < 1) { delete P; return fail(WQ_EKNOTS, "dir " + std::to_string(l) + ": too few knots"); }
+        for (int64_t k = 0; k < nk; ++k)
+            if (!std::isfinite(xi[k])) { delete P; return fail(WQ_EKNOTS, "dir " + std::to_string(l) + ": non-finite knot"); }
+        for (int k = 1; k <= p; ++k)
+            if (xi[k] != xi[0] || xi[nk - 1 - k] != xi[nk - 1]) {
+                delete P;
+                return fail(WQ_EKNOTS, "dir " + std::to_string(l) + ": knot vector is not open");
+            }
+        for (int64_t k = p; k < nk - p - 1; ++k)
+            if (!(xi[k] < xi[k + 1])) {
+                delete P;
+                return fail(WQ_EKNOTS, "dir " + std::to_string(l) + ": repeated or decreasing interior knot at " +
+                                           std::to_string(k));
+            }
+        DirView &v = P->dir[l];
+        v.nk = nk;
+        v.n = nk - p - 1;
+        v.E = E;
+        v.nq = host_nq(E, p);
+        int64_t mq = 0;
+        for (int64_t i = 0; i < v.n; ++i) {
+            int64_t q = host_qhi(i, E, p) - host_qlo(i, E, p) + 1;
+            if (q < wq_ni(i, p, v.n)) { delete P; return fail(WQ_ESINGULAR, "#Q < #I (Eq. numb_nodes)"); }
+            mq = q > mq ? q : mq;
+        }
+        v.maxq = (int32_t)mq;
+        P->L[l] = host_pref(v.n, p, v.n);
+    }
+    for (int l = d; l < 3; ++l) {
+        DirView &v = P->dir[l];
+        v.nk = 0; v.n = 1; v.E = 1; v.nq = 1; v.maxq = 1;
+        P->L[l] = 1;
+    }
+    int64_t N = 1, nnz = 1;
+    for (int l = 0; l < d; ++l) { N *= P->dir[l].n; nnz *= P->L[l]; }
+    if (N >= ((int64_t)1 << 31)) { delete P; return fail(WQ_ERANGE, "N_DOF >= 2^31 (int32 columns)"); }
+    P->n_dof_total = N;
+    P->nnz_total = nnz;
+    // ---- slab of the slowest direction
+    const int ld = d - 1;
+    const int64_t nd = P->dir[ld].n;
+    int64_t b = desc->slab_begin, e = desc->slab_end;
+    if (b == 0 && e == -1) e = nd;
+    if (b < 0 || e > nd || b >= e) { delete P; return fail(WQ_EINVAL, "bad slab range"); }
+    P->slab_b = b;
+    P->slab_e = e;
+    int64_t rows_per_plane = 1, L_per_plane = 1;
+    for (int l = 0; l < ld; ++l) { rows_per_plane *= P->dir[l].n; L_per_plane *= P->L[l]; }
+    P->row_begin = b * rows_per_plane;
+    P->n_rows_local = (e - b) * rows_per_plane;
+    P->nnz_local = (host_pref(e, p, nd) - host_pref(b, p, nd)) * L_per_plane;
+    // coefficient sub-grid along direction d
+    P->cq_b = host_qlo(b, P->dir[ld].E, p);
+    P->cq_e = host_qhi(e - 1, P->dir[ld].E, p) + 1;
+    int64_t cp = P->cq_e - P->cq_b;
+    for (int l = 0; l < ld; ++l) cp *= P->dir[l].nq;
+    P->coef_points = cp;
+    P->ncomp_s = P->need_stiff ? d * (d + 1) / 2 : 0;
+    P->ncomp = P->ncomp_s + P->need_mass;
+
+    // ---- device allocations
+    cudaError_t ce = cudaSetDevice(P->device);
+    if (ce != cudaSuccess) { delete P; return wq_cuda_status(ce, "cudaSetDevice"); }
+    size_t bytes = 0;
+    std::vector<size_t> offs;
+    auto take = [&](size_t n) { size_t o = bytes; bytes = align_up(bytes + n); offs.push_back(o); return o; };
+    struct Off { size_t knots, pts, span, qlo, qlen, jlo, jlen, pref, B, W; } O[3];
+    for (int l = 0; l < d; ++l) {
+        DirView &v = P->dir[l];
+        O[l].knots = take(sizeof(double) * v.nk);
+        O[l].pts = take(sizeof(double) * v.nq);
+        O[l].span = take(sizeof(int32_t) * v.nq);
+        O[l].qlo = take(sizeof(int32_t) * v.n);
+        O[l].qlen = take(sizeof(int32_t) * v.n);
+        O[l].jlo = take(sizeof(int32_t) * v.n);
+        O[l].jlen = take(sizeof(int32_t) * v.n);
+        O[l].pref = take(sizeof(int64_t) * (v.n + 1));
+        O[l].B = take(sizeof(double) * v.nq * WQ_BROWS * (p + 1));
+        O[l].W = take(sizeof(double) * v.n * 4 * v.maxq);
+    }
+    size_t o_gl = take(sizeof(double) * 4 * (p + 1));
+    size_t o_fl = take(sizeof(Flags));
+    void *arena = nullptr;
+    ce = cudaMalloc(&arena, bytes);
+    if (ce != cudaSuccess) { delete P; return fail(WQ_ENOMEM, "arena allocation failed"); }
+    cudaMemset(arena, 0, bytes);
+    P->arena = arena;
+    P->arena_bytes = bytes;
+    char *A = (char *)arena;
+    for (int l = 0; l < d; ++l) {
+        DirView &v = P->dir[l];
+        v.knots = (const double *)(A + O[l].knots);
+        v.pts = (double *)(A + O[l].pts);
+        v.span = (int32_t *)(A + O[l].span);
+        v.qlo = (int32_t *)(A + O[l].qlo);
+        v.qlen = (int32_t *)(A + O[l].qlen);
+        v.jlo = (int32_t *)(A + O[l].jlo);
+        v.jlen = (int32_t *)(A + O[l].jlen);
+        v.pref = (int64_t *)(A + O[l].pref);
+        v.B = (double *)(A + O[l].B);
+        v.W = (double *)(A + O[l].W);
+        ce = cudaMemcpy((void *)v.knots, desc->knots[l], sizeof(double) * v.nk, cudaMemcpyHostToDevice);
+        if (ce != cudaSuccess) { wq_plan_destroy(P); return wq_cuda_status(ce, "knot upload"); }
+    }
+    P->gl = (double *)(A + o_gl);
+    P->flags = (Flags *)(A + o_fl);
+    size_t cbytes = sizeof(double) * (size_t)P->ncomp * (size_t)P->coef_points;
+    ce = cudaMalloc((void **)&P->coef, cbytes);
+    if (ce != cudaSuccess) {
+        P->coef = nullptr;
+        wq_plan_destroy(P);
+        return fail(WQ_ENOMEM, "coefficient field allocation failed (" + std::to_string(cbytes) + " bytes)");
+    }
+    P->workspace_bytes = (int64_t)(bytes + cbytes);
+    *out = P;
+    return WQ_OK;
+}
+
+wq_status wq_plan_destroy(wq_plan P) {
+    if (!P) return WQ_OK;
+    cudaSetDevice(P->device);
+    if (P->arena) cudaFree(P->arena);
+    if (P->coef) cudaFree(P->coef);
+    if (P->ctrl_dev) cudaFree(P->ctrl_dev);
+    if (P->stage_val) cudaFree(P->stage_val);
+    delete P;
+    return WQ_OK;
+}
+
+wq_status wq_plan_info(wq_plan P, wq_plan_info_t *info) {
+    if (!P || !info) return fail(WQ_EINVAL, "NULL argument");
+    info->n_dof_total = P->n_dof_total;
+    info->nnz_total = P->nnz_total;
+    info->row_begin = P->row_begin;
+    info->n_rows_local = P->n_rows_local;
+    info->nnz_local = P->nnz_local;
+    for (int l = 0; l < 3; ++l) {
+        info->n_dof[l] = P->dir[l].n;
+        info->n_qp[l] = P->dir[l].nq;
+        info->max_q[l] = P->dir[l].maxq;
+    }
+    info->coef_points = P->coef_points;
+    info->workspace_bytes = P->workspace_bytes;
+    return WQ_OK;
+}
+
+wq_status wq_build_rules(wq_plan P, void *stream) {
+    if (!P) return fail(WQ_EINVAL, "NULL plan");
+    cudaSetDevice(P->device);
+    cudaError_t ce = cudaMemsetAsync(&P->flags->weights_bad, 0, sizeof(int), S(stream));
+    if (ce != cudaSuccess) return wq_cuda_status(ce, "flag reset");
+    return launch_rules(P, S(stream));
+}
+
+wq_status wq_build_coef(wq_plan P, const double *d_ctrl, void *stream) {
+    if (!P || !d_ctrl) return fail(WQ_EINVAL, "NULL argument");
+    cudaSetDevice(P->device);
+    cudaError_t ce = cudaMemsetAsync(&P->flags->det_pos, 0, 3 * sizeof(int), S(stream));
+    if (ce != cudaSuccess) return wq_cuda_status(ce, "flag reset");
+    return launch_coef(P, d_ctrl, S(stream));
+}
+
+wq_status wq_pattern(wq_plan P, int64_t nnz_base, int64_t *d_row_ptr, int32_t *d_col, void *stream) {
+    if (!P || !d_row_ptr) return fail(WQ_EINVAL, "NULL argument");
+    if (nnz_base < 0) return fail(WQ_EINVAL, "negative nnz_base");
+    cudaSetDevice(P->device);
+    return launch_pattern(P, nnz_base, d_row_ptr, d_col, 0, P->n_rows_local, S(stream));
+}
+
+static int64_t rows_per_plane(const wq_plan_s *P) {
+    int64_t r = 1;
+    for (int l = 0; l < P->d - 1; ++l) r *= P->dir[l].n;
+    return r;
+}
+
+static wq_status assemble_range(wq_plan_s *P, int matrix, wq_kernel kernel, double *val, int32_t *col,
+                                int64_t pl_lo, int64_t pl_hi, int64_t val_base, cudaStream_t s) {
+    if (matrix == WQ_MASS && !P->need_mass) return fail(WQ_EINVAL, "plan was created without need_mass");
+    if (matrix == WQ_STIFFNESS && !P->need_stiff) return fail(WQ_EINVAL, "plan was created without need_stiffness");
+    bool tile = tile_supported(P, matrix);
+    if (kernel == WQ_KERNEL_TILE && !tile) return fail(WQ_EINVAL, "tile kernel not available for this (d, p)");
+    if (kernel == WQ_KERNEL_DIRECT || !tile)
+        return launch_assemble_direct(P, matrix, val, col, pl_lo, pl_hi, val_base, s);
+    return launch_assemble_tile(P, matrix, val, col, pl_lo, pl_hi, val_base, s);
+}
+
+wq_status wq_assemble_ex(wq_plan P, wq_matrix matrix, wq_kernel kernel, double *d_val, int32_t *d_col, void *stream) {
+    if (!P || !d_val) return fail(WQ_EINVAL, "NULL argument");
+    if (matrix != WQ_MASS && matrix != WQ_STIFFNESS) return fail(WQ_EINVAL, "bad matrix");
+    cudaSetDevice(P->device);
+    return assemble_range(P, matrix, kernel, d_val, d_col, 0, P->slab_e - P->slab_b, 0, S(stream));
+}
+
+wq_status wq_assemble(wq_plan P, wq_matrix matrix, double *d_val, int32_t *d_col, void *stream) {
+    return wq_assemble_ex(P, matrix, WQ_KERNEL_AUTO, d_val, d_col, stream);
+}
+
+wq_status wq_check(wq_plan P, void *stream) {
+    if (!P) return fail(WQ_EINVAL, "NULL plan");
+    cudaSetDevice(P->device);
+    cudaError_t ce = cudaStreamSynchronize(S(stream));
+    if (ce != cudaSuccess) return wq_cuda_status(ce, "stream synchronize");
+    Flags f;
+    ce = cudaMemcpy(&f, P->flags, sizeof(Flags), cudaMemcpyDeviceToHost);
+    if (ce != cudaSuccess) return wq_cuda_status(ce, "flag readback");
+    if (f.weights_bad) {
+        int code = f.weights_bad - 1;
+        int row = code / 12, rem = code % 12, dir = rem / 4, fam = rem % 4;
+        char buf[160];
+        snprintf(buf, sizeof buf, "weight system failed: dir %d row %d family (%d,%d)", dir, row, fam & 1, fam >> 1);
+        return fail(WQ_ESINGULAR, buf);
+    }
+    if (f.det_zero || (f.det_pos && f.det_neg))
+        return fail(WQ_EGEOMETRY, f.det_zero ? "det J = 0 at a grid point" : "det J changes sign on the grid");
+    return WQ_OK;
+}
+
+wq_status wq_form_host(wq_plan P, wq_matrix matrix, const double *h_ctrl, int64_t nnz_base, int64_t *h_row_ptr,
+                       int32_t *h_col, double *h_val, void *stream) {
+    if (!P || !h_ctrl || !h_row_ptr || !h_col || !h_val) return fail(WQ_EINVAL, "NULL argument");
+    cudaSetDevice(P->device);
+    cudaStream_t s = S(stream);
+    const size_t cbytes = sizeof(double) * (size_t)P->n_dof_total * P->d;
+    cudaError_t ce;
+    if (P->ctrl_bytes < cbytes) {
+        if (P->ctrl_dev) cudaFree(P->ctrl_dev);
+        ce = cudaMalloc((void **)&P->ctrl_dev, cbytes);
+        if (ce != cudaSuccess) { P->ctrl_dev = nullptr; P->ctrl_bytes = 0; return fail(WQ_ENOMEM, "ctrl staging"); }
+        P->ctrl_bytes = cbytes;
+    }
+    // chunking by slab planes, double-buffered staging for values + columns + row_ptr
+    const int64_t nplanes = P->slab_e - P->slab_b;
+    const int64_t rpp = rows_per_plane(P);
+    const int64_t max_plane_nnz = [&] {
+        int64_t m = 1;
+        for (int l = 0; l < P->d - 1; ++l) m *= P->L[l];
+        return m * (2 * P->p + 1);
+    }();
+    int64_t target = (int64_t)1 << 26;  // ~64M nnz per chunk (768 MB of CSR)
+    int64_t ppc = target / max_plane_nnz;
+    if (ppc < 1) ppc = 1;
+    if (ppc > nplanes) ppc = nplanes;
+    const int64_t chunk_nnz = ppc * max_plane_nnz;
+    const int64_t chunk_rows = ppc * rpp + 1;
+    const size_t per = align_up(sizeof(double) * chunk_nnz) + align_up(sizeof(int32_t) * chunk_nnz) +
+                       align_up(sizeof(int64_t) * chunk_rows);
+    if (P->stage_bytes < 2 * per) {
+        if (P->stage_val) cudaFree(P->stage_val);
+        ce = cudaMalloc((void **)&P->stage_val, 2 * per);
+        if (ce != cudaSuccess) { P->stage_val = nullptr; P->stage_bytes = 0; return fail(WQ_ENOMEM, "staging"); }
+        P->stage_bytes = 2 * per;
+    }
+    char *base = (char *)P->stage_val;
+    double *sv[2];
+    int32_t *sc[2];
+    int64_t *sr[2];
+    for (int k = 0; k < 2; ++k) {
+        char *b = base + k * per;
+        sv[k] = (double *)b;
+        sc[k] = (int32_t *)(b + align_up(sizeof(double) * chunk_nnz));
+        sr[k] = (int64_t *)(b + align_up(sizeof(double) * chunk_nnz) + align_up(sizeof(int32_t) * chunk_nnz));
+    }
+    cudaStream_t cs;
+    ce = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    if (ce != cudaSuccess) return wq_cuda_status(ce, "copy stream");
+    cudaEvent_t done[2], freed[2];
+    for (int k = 0; k < 2; ++k) {
+        cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming);
+        cudaEventRecord(freed[k], cs);
+    }
+    wq_status st = WQ_OK;
+    ce = cudaMemcpyAsync(P->ctrl_dev, h_ctrl, cbytes, cudaMemcpyHostToDevice, s);
+    if (ce != cudaSuccess) st = wq_cuda_status(ce, "ctrl upload");
+    if (!st) st = wq_build_rules(P, s);
+    if (!st) st = wq_build_coef(P, P->ctrl_dev, s);
+    // host-side 1D prefix of the slowest direction for chunk offsets
+    const int64_t nd = P->dir[P->d - 1].n;
+    int64_t Lpp = 1;
+    for (int l = 0; l < P->d - 1; ++l) Lpp *= P->L[l];
+    const int64_t pref_b = host_pref(P->slab_b, P->p, nd);
+    int k = 0;
+    for (int64_t pl = 0; pl < nplanes && !st; pl += ppc, k ^= 1) {
+        int64_t ph = pl + ppc < nplanes ? pl + ppc : nplanes;
+        int64_t off_lo = (host_pref(P->slab_b + pl, P->p, nd) - pref_b) * Lpp;
+        int64_t off_hi = (host_pref(P->slab_b + ph, P->p, nd) - pref_b) * Lpp;
+        int64_t r_lo = pl * rpp, r_hi = ph * rpp;
+        cudaStreamWaitEvent(s, freed[k], 0);
+        st = assemble_range(P, matrix, WQ_KERNEL_AUTO, sv[k], sc[k], pl, ph, off_lo, s);
+        if (st) break;
+        st = launch_pattern(P, nnz_base, sr[k], nullptr, r_lo, r_hi - 1, s);
+        if (st) break;
+        cudaEventRecord(done[k], s);
+        cudaStreamWaitEvent(cs, done[k], 0);
+        size_t nz = (size_t)(off_hi - off_lo);
+        cudaMemcpyAsync(h_val + off_lo, sv[k], nz * sizeof(double), cudaMemcpyDeviceToHost, cs);
+        cudaMemcpyAsync(h_col + off_lo, sc[k], nz * sizeof(int32_t), cudaMemcpyDeviceToHost, cs);
+        cudaMemcpyAsync(h_row_ptr + r_lo, sr[k], (size_t)(r_hi - r_lo) * sizeof(int64_t), cudaMemcpyDeviceToHost, cs);
+        cudaEventRecord(freed[k], cs);
+    }
+    if (!st) {
+        // final row_ptr entry
+        h_row_ptr[P->n_rows_local] = nnz_base + P->nnz_local;
+    }
+    ce = cudaStreamSynchronize(cs);
+    if (!st && ce != cudaSuccess) st = wq_cuda_status(ce, "copy stream");
+    for (int kk = 0; kk < 2; ++kk) { cudaEventDestroy(done[kk]); cudaEventDestroy(freed[kk]); }
+    cudaStreamDestroy(cs);
+    if (!st) st = wq_check(P, stream);
+    return st;
+}
+
+wq_status wq_export_rules(wq_plan P, int dir, double *h_points, int32_t *h_qlo, int32_t *h_qlen, double *h_w,
+                          double *h_basis, int32_t *h_span) {
+    if (!P) return fail(WQ_EINVAL, "NULL plan");
+    if (dir < 0 || dir >= P->d) return fail(WQ_ERANGE, "dir out of range");
+    cudaSetDevice(P->device);
+    const DirView &v = P->dir[dir];
+    cudaError_t ce = cudaDeviceSynchronize();
+    if (!ce && h_points) ce = cudaMemcpy(h_points, v.pts, sizeof(double) * v.nq, cudaMemcpyDeviceToHost);
+    if (!ce && h_qlo) ce = cudaMemcpy(h_qlo, v.qlo, sizeof(int32_t) * v.n, cudaMemcpyDeviceToHost);
+    if (!ce && h_qlen) ce = cudaMemcpy(h_qlen, v.qlen, sizeof(int32_t) * v.n, cudaMemcpyDeviceToHost);
+    if (!ce && h_w) ce = cudaMemcpy(h_w, v.W, sizeof(double) * v.n * 4 * v.maxq, cudaMemcpyDeviceToHost);
+    if (!ce && h_basis) ce = cudaMemcpy(h_basis, v.B, sizeof(double) * v.nq * WQ_BROWS * (P->p + 1), cudaMemcpyDeviceToHost);
+    if (!ce && h_span) ce = cudaMemcpy(h_span, v.span, sizeof(int32_t) * v.nq, cudaMemcpyDeviceToHost);
+    return wq_cuda_status(ce, "export rules");
+}
+
+wq_status wq_export_coef(wq_plan P, double *h_out, int64_t *n_values, int32_t *ncomp, int64_t *q_d_begin) {
+    if (!P) return fail(WQ_EINVAL, "NULL plan");
+    if (n_values) *n_values = (int64_t)P->ncomp * P->coef_points;
+    if (ncomp) *ncomp = P->ncomp;
+    if (q_d_begin) *q_d_begin = P->cq_b;
+    if (!h_out) return WQ_OK;
+    cudaSetDevice(P->device);
+    cudaError_t ce = cudaDeviceSynchronize();
+    if (!ce) ce = cudaMemcpy(h_out, P->coef, sizeof(double) * P->ncomp * P->coef_points, cudaMemcpyDeviceToHost);
+    return wq_cuda_status(ce, "export coef");
+}
+
+}  // extern "C"

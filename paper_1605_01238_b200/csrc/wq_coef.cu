@@ -1,0 +1,273 @@
+// wq_coef.cu -- step 5 of the hot path: geometry coefficient field on the
+// tensor point grid (Alg. 1 lines 12/15; Eq. mass2 P:505-507,
+// Eq. coef_stiff, reading R7):
+//   c = |det J|,   C = |det J| J^{-1} J^{-T} = adj(J) adj(J)^T / |det J|.
+// J is evaluated from the DERIVATIVE CONTROL NETS
+//   dF/dzeta_m = sum_k Q^m_k N^{(p-1)}_{k_m} prod_{l != m} N^{(p)}_{k_l},
+//   Q^m_k = p (P_k - P_{k - e_m}) / (xi_{k_m + p} - xi_{k_m}),
+// i.e. with nonnegative degree-(p-1)/p bases and differences of the INPUT
+// control points, so no cancellation occurs (sum_k P_k dB_k/dzeta would lose
+// ~ (p/h) eps relative accuracy at fine meshes).
+// Sum-factorised over a CTA tile (q_1 tile x q_2 tile x one q_3):
+//   stage A contracts k_3, stage B contracts k_2, stage C contracts k_1 per
+//   point -- O(p) FMAs per component per point instead of the O(p^d) of the
+//   direct sum.
+#include "wq_internal.cuh"
+
+namespace {
+
+constexpr int TQ1 = 64;  // q_1 points per CTA (threads)
+constexpr int TQ2 = 8;   // q_2 points per CTA
+
+struct CoefArgs {
+    DirView v[3];
+    int d, p;
+    const double *ctrl;  // [N_DOF][d]
+    double *coef;        // [ncomp][points]
+    int64_t cq_b;        // first q_d of the sub-grid
+    int64_t nq_loc_d;    // q_d extent of the sub-grid
+    int ncomp_s, ncomp;
+    int need_s, need_m;
+    Flags *flags;
+};
+
+// table rows at grid point q: N = degree p (functions span..span+p),
+// M = degree p-1 (functions span+1..span+p)
+__device__ __forceinline__ const double *Ntab(const DirView &v, int p, int64_t q) { return v.B + q * WQ_BROWS * (p + 1); }
+__device__ __forceinline__ const double *Mtab(const DirView &v, int p, int64_t q) {
+    return v.B + q * WQ_BROWS * (p + 1) + 2 * (p + 1);
+}
+// p / (xi_{k+p} - xi_k): scale of derivative control point k (k >= 1)
+__device__ __forceinline__ double dscale(const DirView &v, int p, int64_t k) {
+    return (double)p / (v.knots[k + p] - v.knots[k]);
+}
+
+template <int D>
+__global__ void __launch_bounds__(TQ1) k_coef(CoefArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    const int p = a.p;
+    const DirView &v1 = a.v[0], &v2 = a.v[1], &v3 = a.v[2];
+    const int64_t q1a = (int64_t)blockIdx.x * TQ1;
+    const int64_t q2a = D >= 2 ? (int64_t)blockIdx.y * TQ2 : 0;
+    const int64_t q3l = D == 3 ? (int64_t)blockIdx.z : 0;  // local plane
+    const int64_t q3 = D == 3 ? a.cq_b + q3l : 0;
+    const int64_t q1off = D == 1 ? a.cq_b : 0;  // D == 1: direction 1 is the slab direction
+    const int64_t nq1 = D == 1 ? a.nq_loc_d : v1.nq;
+    const int64_t nq2 = D >= 2 ? (D == 2 ? a.nq_loc_d : v2.nq) : 1;
+    const int64_t q2off = D == 2 ? a.cq_b : 0;  // D == 2: direction 2 is the slab direction
+    const int64_t q1e = q1a + TQ1 < nq1 ? q1a + TQ1 : nq1;
+    const int64_t q2e = q2a + TQ2 < nq2 ? q2a + TQ2 : nq2;
+    const int nt1 = (int)(q1e - q1a), nt2 = (int)(q2e - q2a);
+    const int64_t k1a = v1.span[q1off + q1a], k1e = v1.span[q1off + q1e - 1] + p + 1;
+    const int K1 = (int)(k1e - k1a);
+    int64_t k2a = 0, k2e = 1;
+    if (D >= 2) { k2a = v2.span[q2off + q2a]; k2e = v2.span[q2off + q2e - 1] + p + 1; }
+    const int K2 = (int)(k2e - k2a);
+    const int64_t n1 = v1.n, n2 = D >= 2 ? v2.n : 1;
+    const int K1M = TQ1 + WQ_PMAX + 1, K2M = TQ2 + WQ_PMAX + 1;
+    // smem: A[3 variants][3 comps][K2M][K1M] (D == 3), X[TQ2][3 variants][3 comps][K1M]
+    double *Asm = sm;
+    double *Xsm = sm + (D == 3 ? 9 * K2M * K1M : 0);
+    const int tid = threadIdx.x;
+    const double *P = a.ctrl;
+
+    if (D == 3) {
+        // stage A: contract k_3.  A1 = N3 . Q^1, A2 = N3 . Q^2, A3 = M3 . Q^3
+        const double *n3 = Ntab(v3, p, q3), *m3 = Mtab(v3, p, q3);
+        const int64_t e3 = v3.span[q3];
+        for (int t = tid; t < K2 * K1; t += blockDim.x) {
+            const int c2 = t / K1, c1 = t % K1;
+            const int64_t k1 = k1a + c1, k2 = k2a + c2;
+            double A1[3] = {0, 0, 0}, A2[3] = {0, 0, 0}, A3[3] = {0, 0, 0};
+            const double s1 = k1 >= 1 ? dscale(v1, p, k1) : 0.0;
+            const double s2 = k2 >= 1 ? dscale(v2, p, k2) : 0.0;
+            double prev[3] = {0, 0, 0};
+            for (int r = 0; r <= p; ++r) {
+                const int64_t k3 = e3 + r;
+                const int64_t k = k1 + n1 * (k2 + n2 * k3);
+                const double nv = n3[r];
+                const double s3 = r >= 1 ? dscale(v3, p, k3) : 0.0;
+                #pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double cur = __ldg(P + k * 3 + c);
+                    const double d1 = k1 >= 1 ? (cur - __ldg(P + (k - 1) * 3 + c)) * s1 : 0.0;
+                    const double d2 = k2 >= 1 ? (cur - __ldg(P + (k - n1) * 3 + c)) * s2 : 0.0;
+                    A1[c] = fma(nv, d1, A1[c]);
+                    A2[c] = fma(nv, d2, A2[c]);
+                    if (r >= 1) A3[c] = fma(m3[r - 1], (cur - prev[c]) * s3, A3[c]);
+                    prev[c] = cur;
+                }
+            }
+            #pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                Asm[((0 * 3 + c) * K2M + c2) * K1M + c1] = A1[c];
+                Asm[((1 * 3 + c) * K2M + c2) * K1M + c1] = A2[c];
+                Asm[((2 * 3 + c) * K2M + c2) * K1M + c1] = A3[c];
+            }
+        }
+        __syncthreads();
+        // stage B: contract k_2.  X1 = N2 . A1, X2 = M2 . A2, X3 = N2 . A3
+        for (int t = tid; t < nt2 * K1; t += blockDim.x) {
+            const int t2 = t / K1, c1 = t % K1;
+            const int64_t q2 = q2a + t2;
+            const double *n2t = Ntab(v2, p, q2), *m2t = Mtab(v2, p, q2);
+            const int c2s = (int)(v2.span[q2] - k2a);
+            double X1[3] = {0, 0, 0}, X2[3] = {0, 0, 0}, X3[3] = {0, 0, 0};
+            for (int r = 0; r <= p; ++r) {
+                const double nv = n2t[r], mv = r < p ? m2t[r] : 0.0;
+                #pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    X1[c] = fma(nv, Asm[((0 * 3 + c) * K2M + c2s + r) * K1M + c1], X1[c]);
+                    X3[c] = fma(nv, Asm[((2 * 3 + c) * K2M + c2s + r) * K1M + c1], X3[c]);
+                    if (r < p) X2[c] = fma(mv, Asm[((1 * 3 + c) * K2M + c2s + 1 + r) * K1M + c1], X2[c]);
+                }
+            }
+            #pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                Xsm[((t2 * 3 + 0) * 3 + c) * K1M + c1] = X1[c];
+                Xsm[((t2 * 3 + 1) * 3 + c) * K1M + c1] = X2[c];
+                Xsm[((t2 * 3 + 2) * 3 + c) * K1M + c1] = X3[c];
+            }
+        }
+        __syncthreads();
+    } else if (D == 2) {
+        // stage B directly on the control net: X1 = N2 . Q^1, X2 = M2 . Q^2
+        for (int t = tid; t < nt2 * K1; t += blockDim.x) {
+            const int t2 = t / K1, c1 = t % K1;
+            const int64_t q2 = q2off + q2a + t2;
+            const double *n2t = Ntab(v2, p, q2), *m2t = Mtab(v2, p, q2);
+            const int64_t e2 = v2.span[q2];
+            const int64_t k1 = k1a + c1;
+            const double s1 = k1 >= 1 ? dscale(v1, p, k1) : 0.0;
+            double X1[2] = {0, 0}, X2[2] = {0, 0}, prev[2] = {0, 0};
+            for (int r = 0; r <= p; ++r) {
+                const int64_t k2 = e2 + r;
+                const int64_t k = k1 + n1 * k2;
+                const double s2 = r >= 1 ? dscale(v2, p, k2) : 0.0;
+                #pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const double cur = k1 < n1 ? __ldg(P + k * 2 + c) : 0.0;
+                    const double d1 = (k1 >= 1 && k1 < n1) ? (cur - __ldg(P + (k - 1) * 2 + c)) * s1 : 0.0;
+                    X1[c] = fma(n2t[r], d1, X1[c]);
+                    if (r >= 1) X2[c] = fma(m2t[r - 1], (cur - prev[c]) * s2, X2[c]);
+                    prev[c] = cur;
+                }
+            }
+            #pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                Xsm[((t2 * 3 + 0) * 3 + c) * K1M + c1] = X1[c];
+                Xsm[((t2 * 3 + 1) * 3 + c) * K1M + c1] = X2[c];
+            }
+        }
+        __syncthreads();
+    }
+    // stage C: one thread per q1, loop over the q2 of the tile
+    const int t1 = tid;
+    if (t1 >= nt1) return;
+    const int64_t q1 = q1a + t1;
+    const double *n1t = Ntab(v1, p, q1off + q1), *m1t = Mtab(v1, p, q1off + q1);
+    const int64_t e1 = v1.span[q1off + q1];
+    const int c1s = (int)(e1 - k1a);
+    const int64_t npts_plane = nq1 * (D >= 2 ? nq2 : 1);
+    const int64_t npts = npts_plane * (D == 3 ? a.nq_loc_d : 1);
+    for (int t2 = 0; t2 < (D >= 2 ? nt2 : 1); ++t2) {
+        double J[3][3];
+        #pragma unroll
+        for (int c = 0; c < 3; ++c)
+            #pragma unroll
+            for (int m = 0; m < 3; ++m) J[c][m] = 0.0;
+        if (D == 1) {
+            for (int r = 0; r < p; ++r) {
+                const int64_t k = e1 + 1 + r;
+                J[0][0] = fma(m1t[r], (__ldg(P + k) - __ldg(P + k - 1)) * dscale(v1, p, k), J[0][0]);
+            }
+        } else {
+            const double *X = Xsm + (t2 * 3) * 3 * K1M;
+            for (int r = 0; r <= p; ++r) {
+                const double nv = n1t[r], mv = r < p ? m1t[r] : 0.0;
+                #pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    if (r < p) J[c][0] = fma(mv, X[(0 * 3 + c) * K1M + c1s + 1 + r], J[c][0]);
+                    J[c][1] = fma(nv, X[(1 * 3 + c) * K1M + c1s + r], J[c][1]);
+                    if (D == 3) J[c][2] = fma(nv, X[(2 * 3 + c) * K1M + c1s + r], J[c][2]);
+                }
+            }
+        }
+        double det, adj[3][3];
+        if (D == 1) {
+            det = J[0][0];
+            adj[0][0] = 1.0;
+        } else if (D == 2) {
+            det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+            adj[0][0] = J[1][1]; adj[0][1] = -J[0][1];
+            adj[1][0] = -J[1][0]; adj[1][1] = J[0][0];
+        } else {
+            adj[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+            adj[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+            adj[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+            adj[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+            adj[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+            adj[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+            adj[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+            adj[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+            adj[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+            det = J[0][0] * adj[0][0] + J[0][1] * adj[1][0] + J[0][2] * adj[2][0];
+        }
+        if (!(det > 0.0) && !(det < 0.0)) atomicOr(&a.flags->det_zero, 1);
+        else if (det > 0.0) { if (!a.flags->det_pos) atomicOr(&a.flags->det_pos, 1); }
+        else { if (!a.flags->det_neg) atomicOr(&a.flags->det_neg, 1); }
+        const double ad = fabs(det);
+        const double inv = 1.0 / ad;
+        const int64_t pt = q1 + nq1 * (D >= 2 ? (q2a + t2) : 0) + (D == 3 ? npts_plane * q3l : 0);
+        int comp = 0;
+        if (a.need_s) {
+            #pragma unroll
+            for (int l = 0; l < D; ++l)
+                #pragma unroll
+                for (int m = l; m < D; ++m) {
+                    double s = 0.0;
+                    #pragma unroll
+                    for (int k = 0; k < D; ++k) s = fma(adj[l][k], adj[m][k], s);
+                    a.coef[(int64_t)comp * npts + pt] = s * inv;
+                    ++comp;
+                }
+        }
+        if (a.need_m) a.coef[(int64_t)comp * npts + pt] = ad;
+    }
+}
+
+}  // namespace
+
+wq_status launch_coef(wq_plan_s *P, const double *ctrl, cudaStream_t s) {
+    CoefArgs a;
+    for (int l = 0; l < 3; ++l) a.v[l] = P->dir[l];
+    a.d = P->d;
+    a.p = P->p;
+    a.ctrl = ctrl;
+    a.coef = P->coef;
+    a.cq_b = P->cq_b;
+    a.nq_loc_d = P->cq_e - P->cq_b;
+    a.ncomp_s = P->ncomp_s;
+    a.ncomp = P->ncomp;
+    a.need_s = P->need_stiff;
+    a.need_m = P->need_mass;
+    a.flags = P->flags;
+    const int K1M = TQ1 + WQ_PMAX + 1, K2M = TQ2 + WQ_PMAX + 1;
+    if (P->d == 3) {
+        size_t sm = (size_t)(9 * K2M * K1M + TQ2 * 9 * K1M) * sizeof(double);
+        static bool set = false;
+        if (!set) { cudaFuncSetAttribute(k_coef<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); set = true; }
+        dim3 g((unsigned)((P->dir[0].nq + TQ1 - 1) / TQ1), (unsigned)((P->dir[1].nq + TQ2 - 1) / TQ2),
+               (unsigned)a.nq_loc_d);
+        k_coef<3><<<g, TQ1, sm, s>>>(a);
+    } else if (P->d == 2) {
+        size_t sm = (size_t)(TQ2 * 9 * K1M) * sizeof(double);
+        dim3 g((unsigned)((P->dir[0].nq + TQ1 - 1) / TQ1), (unsigned)((a.nq_loc_d + TQ2 - 1) / TQ2), 1);
+        k_coef<2><<<g, TQ1, sm, s>>>(a);
+    } else {
+        dim3 g((unsigned)((a.nq_loc_d + TQ1 - 1) / TQ1), 1, 1);
+        k_coef<1><<<g, TQ1, 0, s>>>(a);
+    }
+    wq_count_launches(1);
+    return wq_cuda_status(cudaGetLastError(), "coefficient kernel");
+}

@@ -1,0 +1,84 @@
+// wq_internal.cuh -- plan layout and helpers shared by the libwq kernels.
+// Product code (sm_100a).  Shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include "../../include/wq.h"
+
+#define WQ_PMAX WQ_MAX_DEGREE          // compile-time bound on p
+#define WQ_KMAX (2 * WQ_PMAX + 1)      // max #I_i
+#define WQ_BROWS 3                     // rows of the per-point basis table
+
+// Device view of one parametric direction.  For l >= d the direction is a
+// dummy of extent 1 (n = nq = 1, one point, weight 1, B = 1, B' = 0).
+struct DirView {
+    int64_t n;        // DOFs
+    int64_t E;        // knot spans
+    int64_t nq;       // grid points (Remark 1)
+    int64_t nk;       // knots
+    int32_t maxq;     // max #Q_i
+    const double *knots;  // [nk]
+    double *pts;          // [nq]
+    int32_t *span;        // [nq] first nonzero function at the point (span index e)
+    int32_t *qlo, *qlen;  // [n] Q_i = [qlo, qlo+qlen)
+    int32_t *jlo, *jlen;  // [n] I_i = [jlo, jlo+jlen)
+    int64_t *pref;        // [n+1] prefix sums of jlen
+    double *B;            // [nq][WQ_BROWS][p+1]: values, first derivatives of functions
+                          // span..span+p, and degree p-1 values of span+1..span+p (last slot 0)
+    double *W;            // [n][4][maxq] weights, family f = a + 2b
+};
+
+struct Flags {   // device-side latched errors
+    int weights_bad;   // first failing (dir,row,family) + 1, packed
+    int det_pos;
+    int det_neg;
+    int det_zero;
+};
+
+struct wq_plan_s {
+    int d, p, device;
+    int need_mass, need_stiff;
+    int64_t slab_b, slab_e;        // planes of i_d
+    int64_t n_dof_total, nnz_total, row_begin, n_rows_local, nnz_local;
+    int64_t L[3];                  // sum_i #I_{l,i}
+    DirView dir[3];
+    // coefficient sub-grid: q_d in [cq_b, cq_e)
+    int64_t cq_b, cq_e, coef_points;
+    int ncomp_s, ncomp;            // stiffness components, total components
+    double *coef;                  // [ncomp][coef_points]
+    // Gauss-Legendre rule on [-1,1] in double-double: [p+1] (hi, lo) pairs
+    double *gl;                    // [2*(p+1)] t, [2*(p+1)] w
+    Flags *flags;                  // device
+    void *arena;                   // one allocation for all small tables
+    size_t arena_bytes;
+    double *ctrl_dev;              // device control-net staging (wq_form_host)
+    size_t ctrl_bytes;
+    // form_host staging
+    double *stage_val; int32_t *stage_col; int64_t *stage_rp; size_t stage_bytes;
+    int64_t workspace_bytes;
+};
+
+// host helpers
+void wq_count_launches(int n);  // adds n to the process-wide launch counter
+void wq_set_error(const std::string &msg);
+wq_status wq_cuda_status(cudaError_t e, const char *what);
+
+// 1D counts (host and device)
+__host__ __device__ inline int64_t wq_jlo(int64_t i, int p) { return i - p > 0 ? i - p : 0; }
+__host__ __device__ inline int64_t wq_jhi(int64_t i, int p, int64_t n) { return i + p < n - 1 ? i + p : n - 1; }
+__host__ __device__ inline int64_t wq_ni(int64_t i, int p, int64_t n) { return wq_jhi(i, p, n) - wq_jlo(i, p) + 1; }
+
+// kernel launchers (defined in the .cu files)
+wq_status launch_rules(wq_plan_s *P, cudaStream_t s);
+wq_status launch_coef(wq_plan_s *P, const double *ctrl, cudaStream_t s);
+wq_status launch_pattern(wq_plan_s *P, int64_t base, int64_t *rp, int32_t *col, int64_t row_lo,
+                         int64_t row_hi, cudaStream_t s);
+// value kernels over the slab planes [plane_lo, plane_hi) (relative to the
+// plan's first plane); entries are written at (row offset - val_base).
+wq_status launch_assemble_direct(wq_plan_s *P, int matrix, double *val, int32_t *col, int64_t plane_lo,
+                                 int64_t plane_hi, int64_t val_base, cudaStream_t s);
+wq_status launch_assemble_tile(wq_plan_s *P, int matrix, double *val, int32_t *col, int64_t plane_lo,
+                               int64_t plane_hi, int64_t val_base, cudaStream_t s);
+bool tile_supported(const wq_plan_s *P, int matrix);
+
