@@ -170,7 +170,7 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
         O[l].jlo = take(sizeof(int32_t) * v.n);
         O[l].jlen = take(sizeof(int32_t) * v.n);
         O[l].pref = take(sizeof(int64_t) * (v.n + 1));
-        O[l].B = take(sizeof(double) * v.nq * WQ_BROWS * (p + 1));
+        O[l].B = take(sizeof(double) * v.nq * wq_bstride(p));
         O[l].W = take(sizeof(double) * v.n * 4 * v.maxq);
     }
     size_t o_gl = take(sizeof(double) * 4 * (p + 1));
@@ -411,12 +411,29 @@ wq_status wq_export_rules(wq_plan P, int dir, double *h_points, int32_t *h_qlo, 
     if (dir < 0 || dir >= P->d) return fail(WQ_ERANGE, "dir out of range");
     cudaSetDevice(P->device);
     const DirView &v = P->dir[dir];
+    const int P1 = P->p + 1;
     cudaError_t ce = cudaDeviceSynchronize();
     if (!ce && h_points) ce = cudaMemcpy(h_points, v.pts, sizeof(double) * v.nq, cudaMemcpyDeviceToHost);
     if (!ce && h_qlo) ce = cudaMemcpy(h_qlo, v.qlo, sizeof(int32_t) * v.n, cudaMemcpyDeviceToHost);
     if (!ce && h_qlen) ce = cudaMemcpy(h_qlen, v.qlen, sizeof(int32_t) * v.n, cudaMemcpyDeviceToHost);
-    if (!ce && h_w) ce = cudaMemcpy(h_w, v.W, sizeof(double) * v.n * 4 * v.maxq, cudaMemcpyDeviceToHost);
-    if (!ce && h_basis) ce = cudaMemcpy(h_basis, v.B, sizeof(double) * v.nq * WQ_BROWS * (P->p + 1), cudaMemcpyDeviceToHost);
+    if (!ce && h_w) {  // device [n][maxq][4] -> documented [n][4][maxq]
+        std::vector<double> t((size_t)v.n * 4 * v.maxq);
+        ce = cudaMemcpy(t.data(), v.W, sizeof(double) * t.size(), cudaMemcpyDeviceToHost);
+        for (int64_t i = 0; i < v.n; ++i)
+            for (int c = 0; c < v.maxq; ++c)
+                for (int f = 0; f < 4; ++f) h_w[(i * 4 + f) * v.maxq + c] = t[(i * v.maxq + c) * 4 + f];
+    }
+    if (!ce && h_basis) {  // device [nq][pairs..., low...] -> documented [nq][3][p+1]
+        std::vector<double> t((size_t)v.nq * wq_bstride(P->p));
+        ce = cudaMemcpy(t.data(), v.B, sizeof(double) * t.size(), cudaMemcpyDeviceToHost);
+        for (int64_t q = 0; q < v.nq; ++q)
+            for (int r = 0; r < P1; ++r) {
+                const double *s = t.data() + q * wq_bstride(P->p);
+                h_basis[(q * 3 + 0) * P1 + r] = s[2 * r];
+                h_basis[(q * 3 + 1) * P1 + r] = s[2 * r + 1];
+                h_basis[(q * 3 + 2) * P1 + r] = s[2 * P1 + r];
+            }
+    }
     if (!ce && h_span) ce = cudaMemcpy(h_span, v.span, sizeof(int32_t) * v.nq, cudaMemcpyDeviceToHost);
     return wq_cuda_status(ce, "export rules");
 }

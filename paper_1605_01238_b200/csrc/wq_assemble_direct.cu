@@ -59,8 +59,8 @@ __global__ void __launch_bounds__(128) k_direct(DirectArgs a) {
                 int64_t q = ql[l] + c, j = jl[l] + t;
                 int loc = (int)(j - v.span[q]);
                 int b = f >> 1;
-                double B = (loc >= 0 && loc <= p) ? v.B[q * WQ_BROWS * P1 + b * P1 + loc] : 0.0;
-                val = v.W[(ii[l] * 4 + f) * v.maxq + c] * B;
+                double B = (loc >= 0 && loc <= p) ? v.B[q * wq_bstride(p) + 2 * loc + b] : 0.0;
+                val = v.W[(ii[l] * v.maxq + c) * 4 + f] * B;
             }
             A[((l * nf + f) * KM + t) * QM + c] = val;
         }

@@ -1,77 +1,104 @@
-// wq_assemble_tile.cu -- step 7, sum-factorised row-tile kernel (WQ_KERNEL_TILE)
-// for d = 3, compile-time degree P.  Eq. sumfactorization / Alg. 3
-// (P:859-870), re-organised so that the rows of a tile share every stage but
-// the last:
+// wq_assemble_tile.cu -- step 7, sum-factorised row-line kernel (WQ_KERNEL_TILE),
+// d = 3, compile-time degree P.  Eq. sumfactorization / Alg. 3
+// (P:859-870), re-organised so that rows share every stage but the last
+// (DESIGN.md §6 "Row-line kernel"):
 //
-//   CTA = one line (i2, i3) of the row grid, a batch of RB consecutive rows
-//         i1, and a chunk of T3C trial indices t3 (t3 is slowest in a CSR row).
-//   stage 3 (+ pointwise test weights of directions 2, 3), per q1 of the
-//         tile's q1-window and per c2:
-//     stiffness, chains (m, a1), m = trial-derivative direction, a1 = [l = 1]:
-//       Y_{m,a1}(q1,c2,t3) = sum_{c3} B3^{[m=3]}_{t3}(c3) *
-//                            sum_{l: [l=1]=a1} w2^{([l=2],[m=2])}(c2) w3^{([l=3],[m=3])}(c3) C_lm(q1,c2,c3)
-//     mass: Y(q1,c2,t3) = sum_{c3} B3_{t3}(c3) w2^(0,0)(c2) w3^(0,0)(c3) c(q1,c2,c3)
-//   stage 2: G[b1][a1](q1,t2,t3) = sum_{c2} (B2^{[m=2]}_{t2} Y_{m,a1}) summed over the m
-//         with [m=1] = b1   (mass: G = sum_{c2} B2_{t2} Y)
-//   stage 1 (per row i1):  out(t1,t2,t3) = sum_{c1} B1^0_{t1}(c1) U^0(c1) + B1^1_{t1}(c1) U^1(c1)
-//         U^0 = w1^(0,0) G[0][0] + w1^(1,0) G[0][1],  U^1 = w1^(0,1) G[1][0] + w1^(1,1) G[1][1]
-//         (mass: out = sum_{c1} B1_{t1}(c1) w1^(0,0)(c1) G).
+// CTA = one line (i2, i3) of the row grid (all i1, processed in batches of RB
+// rows) x one chunk of T3C trial indices t3.  Per point q1 of the line:
+//   stage 3 (+ test weights of directions 2, 3 applied pointwise), fibre (q1, c2):
+//     stiffness chains (m, a1); m = trial-derivative direction, a1 = [l == 0]:
+//       Y_{m,a1}(c2,t3) = sum_{c3} B3^{[m==2]}_{t3}(c3) *
+//                         sum_{l: [l==0]=a1} w2^{([l==1],[m==1])}(c2) w3^{([l==2],[m==2])}(c3) C_lm(q1,c2,c3)
+//     mass: Y(c2,t3) = sum_{c3} B3_{t3}(c3) w2^(0,0)(c2) w3^(0,0)(c3) c(q1,c2,c3)
+//   stage 2, fibre (q1, t3): G[b1][a1](t2,t3) = sum_{c2} sum_{m: [m==0]=b1} B2^{[m==1]}_{t2}(c2) Y_{m,a1}(c2,t3)
+// G lives in a shared-memory ring indexed by q1, so each point is done once per line.
+//   stage 1, per row i1 (threads = columns (t2,t3), NR rows per thread in registers):
+//     out(t1) = sum_{c1} B1_{t1}(c1) U0(c1) + B1'_{t1}(c1) U1(c1),
+//     U0 = w1^(0,0) G[0][0] + w1^(1,0) G[0][1],  U1 = w1^(0,1) G[1][0] + w1^(1,1) G[1][1]
+//     (mass: out = sum_{c1} B1_{t1}(c1) w1^(0,0)(c1) G).
+// The B-spline factors are taken from the compact per-point tables: at point
+// q the nonzero functions are span(q)..span(q)+P, so in a row with first
+// column jlo the point contributes to t = span(q) - jlo + r, r = 0..P (a
+// monotone staircase).  The staircase offset is dispatched to compile-time
+// register indices (uniform across the CTA for stages 3/2, compile-time for
+// rows whose support touches no boundary span).
 // (a, b) = (test, trial) derivative order (reading R3); directions 1..3 are
-// indices 0..2 in the code.  Tables are dense (zero outside the B-spline
-// support) so all inner loops have compile-time trip counts.
+// indices 0..2 in the code.
+#include <type_traits>
 #include "wq_rows.cuh"
 
 namespace {
+
+template <int P, bool STIFF>
+struct Cfg {
+    static constexpr int K = 2 * P + 1;   // max #I
+    static constexpr int QB = 3 * P + 1;  // max #Q (supports with one boundary span)
+    static constexpr int NP = P + 1;
+    static constexpr int T3C = P <= 5 ? K : (P <= 7 ? 7 : (P <= 9 ? 5 : 3));  // t3 chunk
+    static constexpr int NCH = (K + T3C - 1) / T3C;
+    static constexpr int COLS = K * T3C;  // columns (t2 + K*t3l) of a chunk
+    static constexpr int NT = 256;
+    static constexpr int NR = P <= 2 ? 4 : (P <= 4 ? 3 : 2);  // rows per final-stage thread
+    static constexpr int NY = STIFF ? 6 : 1;
+    static constexpr int NG = STIFF ? 4 : 1;
+    __host__ __device__ static constexpr int ev(int x) { return (x + 1) & ~1; }  // keep regions 16-B aligned
+    static constexpr int STV = ev(K * COLS + 2);            // staging doubles per group buffer
+    static constexpr int STC = (K * COLS + 4 + 3) / 4 * 2;  // staging int32 per group buffer, in doubles
+    static constexpr size_t LIMIT = 224 * 1024;
+    __host__ __device__ static constexpr size_t smem_for(int ng, int nqs) {
+        const int rb = NR * ng, ring = QB + 2 * rb + P;
+        const size_t tab = 2 * (2 * QB * NP) + 2 * (4 * QB) + 2 * ring * NP + rb * QB * 4;
+        return sizeof(double) * ((size_t)ev(NY * nqs * QB * T3C) + (size_t)ev(NG * ring * COLS) +
+                                 2 * (size_t)ng * (STV + STC) + tab + 4);
+    }
+    // row groups per batch: as many as threads allow and shared memory holds
+    __host__ __device__ static constexpr int pick_ng() {
+        for (int ng = NT / COLS; ng > 1; --ng)
+            if (smem_for(ng, NR * ng) <= LIMIT) return ng;
+        return 1;
+    }
+    static constexpr int NGRP = pick_ng();
+    static constexpr int RB = NR * NGRP;          // rows per batch
+    static constexpr int RING = QB + 2 * RB + P;  // >= q1 window of a batch
+    // stage-3 sub-batch: all new points of a batch (2 RB) if it fits
+    static constexpr int NQS = smem_for(NGRP, 2 * RB) <= LIMIT ? 2 * RB
+                             : (smem_for(NGRP, RB) <= LIMIT ? RB : (RB / 2 > 2 ? RB / 2 : 2));
+    static constexpr int Y_D = ev(NY * NQS * QB * T3C);
+    static constexpr int G_D = ev(NG * RING * COLS);
+    static constexpr size_t SMEM = smem_for(NGRP, NQS);
+    static_assert(NT / COLS >= 1, "columns per chunk exceed the CTA");
+    static_assert(SMEM <= 227 * 1024, "tile kernel shared memory");
+};
+
+// compile-time dispatch of a runtime offset o in [O, HI]: f(integral_constant<o>)
+template <int O, int HI, class F>
+__device__ __forceinline__ void dispatch(int o, F &&f) {
+    if constexpr (O <= HI) {
+        if (o == O) f(std::integral_constant<int, O>{});
+        else dispatch<O + 1, HI>(o, f);
+    }
+}
+
+template <int N, class F>
+__device__ __forceinline__ void unroll(F &&f) {
+    if constexpr (N > 0) {
+        unroll<N - 1>(f);
+        f(std::integral_constant<int, N - 1>{});
+    }
+}
 
 struct TileArgs {
     RowGeo g;
     DirView v[3];
     const double *coef;
-    int64_t nq1, nq2;     // coefficient strides
+    int64_t nq1, nq2;  // coefficient strides
     int64_t cq_b;
     int64_t npts;
     int comp_mass;
     double *val;
     int32_t *col;
     int64_t val_base;
-    int64_t plane_lo;     // first slab plane (relative) of this launch
-    int n_batch;          // row batches per line
-    int n_chunk;          // t3 chunks
-};
-
-template <int P, bool STIFF>
-struct Cfg {
-    static constexpr int K = 2 * P + 1;      // max #I
-    static constexpr int QB = 3 * P + 1;     // max #Q (n_EL >= P + 2)
-    static constexpr int NY = STIFF ? 6 : 1; // chains through stage 3
-    static constexpr int NG = STIFF ? 4 : 1; // merged chains after stage 2
-    static constexpr int NQS = 8;            // q1 sub-batch of stage 3
-    static constexpr int NW1 = STIFF ? 4 : 1;
-    __host__ __device__ static constexpr size_t ev(size_t x) { return (x + 1) & ~(size_t)1; }  // 16-B aligned regions
-    __host__ __device__ static constexpr size_t bytes_for(int RB, int T3C) {
-        size_t W = QB + 2 * RB + P;
-        size_t d = ev((size_t)NY * NQS * QB * T3C)          // Y
-                   + ev((size_t)NG * W * K * T3C)           // G
-                   + (size_t)RB * K * QB * 2                // B1 pairs per row
-                   + (size_t)RB * QB * 4                    // w1 per row
-                   + 2 * ((size_t)K * QB * 2 + 4 * QB);     // B2, w2, B3, w3
-        return d * sizeof(double);
-    }
-    static constexpr size_t LIMIT = 200 * 1024;
-    // largest T3C (fewest t3 chunks), then largest RB in {8, 4, 2}, that fits
-    __host__ __device__ static constexpr int pick(bool want_rb) {
-        for (int nch = 1; nch <= K; ++nch) {
-            int t3c = (K + nch - 1) / nch;
-            for (int rb = 8; rb >= 2; rb /= 2)
-                if (bytes_for(rb, t3c) <= LIMIT) return want_rb ? rb : t3c;
-        }
-        return want_rb ? 2 : 1;
-    }
-    static constexpr int RB = pick(true);
-    static constexpr int T3C = pick(false);
-    static constexpr int W = QB + 2 * RB + P;
-    static constexpr size_t SMEM = bytes_for(RB, T3C);
-    static_assert(SMEM <= 227 * 1024, "tile kernel shared memory");
+    int64_t plane_lo;  // first slab plane (relative) of this launch
 };
 
 __device__ __forceinline__ int comp_ix(int l, int m) {  // upper-triangle index, d = 3
@@ -79,229 +106,360 @@ __device__ __forceinline__ int comp_ix(int l, int m) {  // upper-triangle index,
     return l * 3 - l * (l - 1) / 2 + (m - l);
 }
 
-// dense (value, derivative) pair of B_{j}(x_q) from the compact table
-__device__ __forceinline__ double2 bpair(const DirView &v, int P, int64_t j, int64_t q) {
-    int loc = (int)(j - v.span[q]);
-    if (loc < 0 || loc > P) return make_double2(0.0, 0.0);
-    const double *b = v.B + q * WQ_BROWS * (P + 1);
-    return make_double2(b[loc], b[P + 1 + loc]);
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+// shared -> global bulk copy (TMA, async proxy); addresses 16-B aligned, bytes % 16 == 0
+__device__ __forceinline__ void bulk_s2g(void *g, const void *s, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(smem_u32(s)), "r"(bytes)
+                 : "memory");
 }
 
 template <int P, bool STIFF>
-__global__ void __launch_bounds__(256) k_tile(TileArgs a) {
+__global__ void __launch_bounds__(256, 1) k_tile(TileArgs a) {
     using CF = Cfg<P, STIFF>;
-    constexpr int K = CF::K, QB = CF::QB, NY = CF::NY, NG = CF::NG, NQS = CF::NQS;
-    constexpr int RB = CF::RB, T3C = CF::T3C, W = CF::W;
+    constexpr int K = CF::K, NP = CF::NP, T3C = CF::T3C, COLS = CF::COLS, NR = CF::NR, NGRP = CF::NGRP;
+    constexpr int RB = CF::RB, RING = CF::RING, NQS = CF::NQS, QB = CF::QB, NT = CF::NT;
+    constexpr int BS = wq_bstride(P);  // basis-table stride per point (even)
+    constexpr int STV = CF::STV, STC = CF::STC;
     extern __shared__ __align__(16) double sm[];
-    double *Ys = sm;                                        // [NY][NQS][QB][T3C]
-    double *Gs = Ys + CF::ev(NY * NQS * QB * T3C);          // [NG][W][K][T3C]
-    double2 *B1s = (double2 *)(Gs + CF::ev(NG * W * K * T3C)); // [RB][K][QB]
-    double *w1s = (double *)(B1s + RB * K * QB);       // [RB][QB][4]
-    double2 *B2s = (double2 *)(w1s + RB * QB * 4);     // [K][QB]
-    double *w2s = (double *)(B2s + K * QB);            // [4][QB]
-    double2 *B3s = (double2 *)(w2s + 4 * QB);          // [K][QB]
-    double *w3s = (double *)(B3s + K * QB);            // [4][QB]
+    double *Ys = sm;                                    // [NY][NQS][QB][T3C]
+    double *Gs = Ys + CF::Y_D;                          // [NG][RING][COLS]
+    double *Sv = Gs + CF::G_D;                          // [2][NGRP][STV]
+    int32_t *Sc = (int32_t *)(Sv + 2 * NGRP * STV);     // [2][NGRP][2*STC]
+    double2 *B2s = (double2 *)(Sv + 2 * NGRP * (STV + STC));  // [QB][NP] (value, derivative)
+    double2 *B3s = B2s + QB * NP;                       // [QB][NP]
+    double2 *W2s = B3s + QB * NP;                       // [QB][2] (f0,f1),(f2,f3)
+    double2 *W3s = W2s + QB * 2;                        // [QB][2]
+    double2 *B1w = W3s + QB * 2;                        // [RING][NP] per q1 slot
+    double2 *W1b = B1w + RING * NP;                     // [RB][QB][2] rows of the batch
 
     const int tid = threadIdx.x;
-    // ---- tile coordinates
-    int64_t bid = blockIdx.x;
-    const int chunk = (int)(bid % a.n_chunk);
-    bid /= a.n_chunk;
-    const int batch = (int)(bid % a.n_batch);
-    const int64_t line = bid / a.n_batch;
-    const int64_t n1 = a.g.n[0], n2 = a.g.n[1];
-    const int64_t i2 = line % n2, i3 = a.g.slab_b + a.plane_lo + line / n2;
-    const int64_t r0 = (int64_t)batch * RB;
-    if (r0 >= n1) return;
-    const int nrows = (int)(n1 - r0 < RB ? n1 - r0 : RB);
+    const int chunk = (int)(blockIdx.x % CF::NCH);
+    const int line = (int)(blockIdx.x / CF::NCH);
+    const int n1 = (int)a.g.n[0], n2 = (int)a.g.n[1];
+    const int i2 = line % n2, i3 = (int)(a.g.slab_b + a.plane_lo) + line / n2;
     const DirView &v1 = a.v[0], &v2 = a.v[1], &v3 = a.v[2];
     const int ni2 = v2.jlen[i2], nq2 = v2.qlen[i2];
     const int ni3 = v3.jlen[i3], nq3 = v3.qlen[i3];
-    const int64_t jl2 = v2.jlo[i2], ql2 = v2.qlo[i2], jl3 = v3.jlo[i3], ql3 = v3.qlo[i3];
+    const int jl2 = v2.jlo[i2], ql2 = v2.qlo[i2], jl3 = v3.jlo[i3], ql3 = v3.qlo[i3];
     const int t3a = chunk * T3C;
     if (t3a >= ni3) return;
     const int nt3 = ni3 - t3a < T3C ? ni3 - t3a : T3C;
-    const int64_t qw0 = v1.qlo[r0];
-    const int nw = (int)(v1.qlo[r0 + nrows - 1] + v1.qlen[r0 + nrows - 1] - qw0);
-
-    // ---- tables
-    for (int x = tid; x < K * QB; x += blockDim.x) {
-        int t = x / QB, c = x % QB;
-        B2s[x] = (t < ni2 && c < nq2) ? bpair(v2, P, jl2 + t, ql2 + c) : make_double2(0.0, 0.0);
-        int t3 = t3a + t;
-        B3s[x] = (t < nt3 && c < nq3) ? bpair(v3, P, jl3 + t3, ql3 + c) : make_double2(0.0, 0.0);
-    }
-    for (int x = tid; x < 4 * QB; x += blockDim.x) {
-        int f = x / QB, c = x % QB;
-        w2s[x] = c < nq2 ? v2.W[(i2 * 4 + f) * v2.maxq + c] : 0.0;
-        w3s[x] = c < nq3 ? v3.W[(i3 * 4 + f) * v3.maxq + c] : 0.0;
-    }
-    for (int x = tid; x < RB * K * QB; x += blockDim.x) {
-        int b = x / (K * QB), t = (x / QB) % K, c = x % QB;
-        double2 val = make_double2(0.0, 0.0);
-        if (b < nrows) {
-            int64_t i1 = r0 + b;
-            if (t < v1.jlen[i1] && c < v1.qlen[i1]) val = bpair(v1, P, v1.jlo[i1] + t, v1.qlo[i1] + c);
-        }
-        B1s[x] = val;
-    }
-    for (int x = tid; x < RB * QB * 4; x += blockDim.x) {
-        int b = x / (QB * 4), c = (x / 4) % QB, f = x % 4;
-        double val = 0.0;
-        if (b < nrows) {
-            int64_t i1 = r0 + b;
-            if (c < v1.qlen[i1]) val = v1.W[(i1 * 4 + f) * v1.maxq + c];
-        }
-        w1s[x] = val;
-    }
-    __syncthreads();
-
-    const double *__restrict__ C = a.coef;
     const int64_t plane_stride = a.nq1 * a.nq2;
-    // ---- stages 3 and 2 over the q1 window, in sub-batches of NQS
-    for (int qs0 = 0; qs0 < nw; qs0 += NQS) {
-        const int nqs = nw - qs0 < NQS ? nw - qs0 : NQS;
-        // stage 3: fibers (q1s, c2, m)
-        const int nfib = nqs * nq2 * (STIFF ? 3 : 1);
-        for (int f = tid; f < nfib; f += blockDim.x) {
-            const int q1s = f % nqs;
-            const int c2 = (f / nqs) % nq2;
-            const int m = STIFF ? f / (nqs * nq2) : 0;
-            const int64_t q1 = qw0 + qs0 + q1s;
-            const int64_t pbase = q1 + a.nq1 * (ql2 + c2) + plane_stride * (ql3 - a.cq_b);
-            double y0[T3C], y1[T3C];
-            #pragma unroll
-            for (int t = 0; t < T3C; ++t) { y0[t] = 0.0; y1[t] = 0.0; }
-            if (STIFF) {
-                const int b2 = (m == 1) ? 2 : 0, b3 = (m == 2) ? 2 : 0;  // 2*[trial derivative]
-                const double wa2 = w2s[(0 + b2) * QB + c2];  // l = 0: w2^(0, [m==1])
-                const double wb2 = w2s[(1 + b2) * QB + c2];  // l = 1: w2^(1, [m==1])
-                const double wc2 = w2s[(0 + b2) * QB + c2];  // l = 2: w2^(0, [m==1])
-                const double *Ca = C + (int64_t)comp_ix(0, m) * a.npts + pbase;
-                const double *Cb = C + (int64_t)comp_ix(1, m) * a.npts + pbase;
-                const double *Cc = C + (int64_t)comp_ix(2, m) * a.npts + pbase;
-                for (int c3 = 0; c3 < nq3; ++c3) {
-                    const int64_t o = plane_stride * c3;
-                    const double ca = __ldg(Ca + o), cb = __ldg(Cb + o), cc = __ldg(Cc + o);
-                    const double h1 = wa2 * w3s[(0 + b3) * QB + c3] * ca;
-                    const double h0 = wb2 * w3s[(0 + b3) * QB + c3] * cb + wc2 * w3s[(1 + b3) * QB + c3] * cc;
-                    #pragma unroll
-                    for (int t = 0; t < T3C; ++t) {
-                        const double2 bb = B3s[t * QB + c3];
-                        const double B = m == 2 ? bb.y : bb.x;
-                        y1[t] = fma(B, h1, y1[t]);
-                        y0[t] = fma(B, h0, y0[t]);
+    const int *__restrict__ qlo1 = v1.qlo, *__restrict__ qlen1 = v1.qlen, *__restrict__ jlo1 = v1.jlo;
+    const int *__restrict__ jlen1 = v1.jlen, *__restrict__ span1 = v1.span;
+    const int mq1 = v1.maxq;
+    // directions 2 and 3 are fixed for the CTA: stage their tables in shared memory
+    for (int x = tid; x < QB * NP; x += NT) {
+        const int c = x / NP, r = x % NP;
+        B2s[x] = c < nq2 ? __ldg((const double2 *)(v2.B + (int64_t)(ql2 + c) * BS) + r) : make_double2(0.0, 0.0);
+        B3s[x] = c < nq3 ? __ldg((const double2 *)(v3.B + (int64_t)(ql3 + c) * BS) + r) : make_double2(0.0, 0.0);
+    }
+    for (int x = tid; x < QB * 2; x += NT) {
+        const int c = x / 2;
+        W2s[x] = c < nq2 ? __ldg((const double2 *)(v2.W + ((int64_t)i2 * v2.maxq + c) * 4) + (x & 1)) : make_double2(0.0, 0.0);
+        W3s[x] = c < nq3 ? __ldg((const double2 *)(v3.W + ((int64_t)i3 * v3.maxq + c) * 4) + (x & 1)) : make_double2(0.0, 0.0);
+    }
+    const int off2_0 = v2.span[ql2] - jl2;  // staircase start (dir 2)
+    const int off3_0 = v3.span[ql3] - jl3;
+    const bool int2 = nq2 == 2 * P + 1 && i2 >= P + 1 && i2 <= n2 - P - 2;  // interior pattern in dir 2
+    const bool int3 = nq3 == 2 * P + 1 && i3 >= P + 1 && i3 <= (int)a.g.n[2] - P - 2 && CF::NCH == 1;
+    // coefficient field restricted to this line
+    const double *__restrict__ Cl = a.coef + (int64_t)ql2 * a.nq1 + (int64_t)(ql3 - a.cq_b) * plane_stride;
+
+    // final-stage thread role: group grp, column colx = t2 + K*t3l
+    const int grp = tid / COLS, colx = tid % COLS;
+    const int t2c = colx % K, t3c = colx / K;
+    const bool fin = grp < NGRP && t2c < ni2 && t3c < nt3;
+    int sbuf = 0;  // staging buffer parity
+
+    int q_done = qlo1[0] - 1;  // last q1 whose G is in the ring
+    for (int r0 = 0; r0 < n1; r0 += RB) {
+        const int rl = (r0 + RB < n1 ? r0 + RB : n1) - 1;
+        const int q_hi = qlo1[rl] + qlen1[rl] - 1;
+        // direction-1 tables of the batch: basis pairs of the new points, weights of the rows
+        for (int x = tid; x < (q_hi - q_done) * NP; x += NT) {
+            const int q = q_done + 1 + x / NP, r = x % NP;
+            B1w[(q % RING) * NP + r] = __ldg((const double2 *)(v1.B + (int64_t)q * BS) + r);
+        }
+        for (int x = tid; x < RB * QB * 2; x += NT) {
+            const int b = x / (QB * 2), c = (x / 2) % QB, i1 = r0 + b;
+            W1b[x] = (i1 < n1 && c < qlen1[i1]) ? __ldg((const double2 *)(v1.W + ((int64_t)i1 * mq1 + c) * 4) + (x & 1))
+                                              : make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+        // ---------------- stages 3 and 2 for the new points (q_done, q_hi]
+        for (int qs = q_done + 1; qs <= q_hi; qs += NQS) {
+            const int nqs = q_hi - qs + 1 < NQS ? q_hi - qs + 1 : NQS;
+            // stage 3: fibres (q1s, c2, m); coefficient loads hoisted into registers
+            const int nfib = nqs * nq2 * (STIFF ? 3 : 1);
+            for (int f = tid; f < nfib; f += NT) {
+                const int q1s = f % nqs;
+                const int c2 = (f / nqs) % nq2;
+                const int m = STIFF ? f / (nqs * nq2) : 0;
+                const double *cp = Cl + (int64_t)c2 * a.nq1 + (qs + q1s);
+                double y0[T3C], y1[T3C];
+                #pragma unroll
+                for (int t = 0; t < T3C; ++t) { y0[t] = 0.0; y1[t] = 0.0; }
+                const int b3 = STIFF && m == 2 ? 1 : 0;
+                const double2 w2v = W2s[c2 * 2 + (STIFF && m == 1 ? 1 : 0)];  // (w2^(0,b2), w2^(1,b2))
+                const double *Ca = cp + (int64_t)(STIFF ? comp_ix(0, m) : a.comp_mass) * a.npts;
+                const double *Cb = cp + (int64_t)comp_ix(1, m) * a.npts;
+                const double *Cc = cp + (int64_t)comp_ix(2, m) * a.npts;
+                double ca[QB], cb[QB], cc[QB];
+                #pragma unroll
+                for (int c3 = 0; c3 < QB; ++c3)
+                    if (c3 < nq3) {
+                        const int64_t o = plane_stride * c3;
+                        ca[c3] = __ldg(Ca + o);
+                        if (STIFF) { cb[c3] = __ldg(Cb + o); cc[c3] = __ldg(Cc + o); }
                     }
+                // contribution of point c3 at staircase offset O (compile time)
+                auto point3 = [&](int c3, auto O) {
+                    constexpr int o0 = decltype(O)::value;
+                    const double2 w3v = W3s[c3 * 2 + b3];  // (w3^(0,b3), w3^(1,b3))
+                    const double2 *bp = B3s + c3 * NP;
+                    if (STIFF) {
+                        const double h1 = w2v.x * w3v.x * ca[c3];                             // l = 0
+                        const double h0 = fma(w2v.y * w3v.x, cb[c3], w2v.x * w3v.y * cc[c3]);  // l = 1, 2
+                        #pragma unroll
+                        for (int r = 0; r <= P; ++r) {
+                            const int t = o0 + r;
+                            if (t >= 0 && t < T3C) {
+                                const double2 bb = bp[r];
+                                const double bv = b3 ? bb.y : bb.x;
+                                y1[t] = fma(bv, h1, y1[t]);
+                                y0[t] = fma(bv, h0, y0[t]);
+                            }
+                        }
+                    } else {
+                        const double h = w2v.x * w3v.x * ca[c3];
+                        #pragma unroll
+                        for (int r = 0; r <= P; ++r) {
+                            const int t = o0 + r;
+                            if (t >= 0 && t < T3C) y0[t] = fma(bp[r].x, h, y0[t]);
+                        }
+                    }
+                };
+                if (int3) {
+                    unroll<2 * P + 1>([&](auto C3) {
+                        constexpr int c3 = decltype(C3)::value;
+                        point3(c3, std::integral_constant<int, (c3 + 1) / 2>{});
+                    });
+                } else {
+                    #pragma unroll
+                    for (int c3 = 0; c3 < QB; ++c3)
+                        if (c3 < nq3) {
+                            const int off = v3.span[ql3 + c3] - jl3 - t3a;
+                            if (CF::NCH == 1) dispatch<0, K - NP>(off, [&](auto O) { point3(c3, O); });
+                            else dispatch<-P, T3C - 1>(off, [&](auto O) { point3(c3, O); });
+                        }
                 }
+                double *Y1 = Ys + (((m * 2 + 1) * NQS + q1s) * QB + c2) * T3C;
+                double *Y0 = Ys + (((m * 2 + 0) * NQS + q1s) * QB + c2) * T3C;
                 #pragma unroll
                 for (int t = 0; t < T3C; ++t) {
-                    Ys[(((m * 2 + 1) * NQS + q1s) * QB + c2) * T3C + t] = y1[t];
-                    Ys[(((m * 2 + 0) * NQS + q1s) * QB + c2) * T3C + t] = y0[t];
+                    Y0[t] = y0[t];
+                    if (STIFF) Y1[t] = y1[t];
                 }
-            } else {
-                const double w2v = w2s[c2];
-                const double *Cm = C + (int64_t)a.comp_mass * a.npts + pbase;
-                for (int c3 = 0; c3 < nq3; ++c3) {
-                    const double h = w2v * w3s[c3] * __ldg(Cm + plane_stride * c3);
-                    #pragma unroll
-                    for (int t = 0; t < T3C; ++t) y0[t] = fma(B3s[t * QB + c3].x, h, y0[t]);
-                }
-                #pragma unroll
-                for (int t = 0; t < T3C; ++t) Ys[(q1s * QB + c2) * T3C + t] = y0[t];
             }
-        }
-        __syncthreads();
-        // stage 2: fibers (q1s, t3, a1) -> G[b1][a1]
-        const int nfib2 = nqs * T3C * (STIFF ? 2 : 1);
-        for (int f = tid; f < nfib2; f += blockDim.x) {
-            const int q1s = f % nqs;
-            const int t3 = (f / nqs) % T3C;
-            const int a1 = STIFF ? f / (nqs * T3C) : 0;
-            const int qw = qs0 + q1s;
-            double g0[K], g1[K];
-            #pragma unroll
-            for (int t = 0; t < K; ++t) { g0[t] = 0.0; g1[t] = 0.0; }
-            if (STIFF) {
-                const double *Y0 = Ys + ((0 * 2 + a1) * NQS + q1s) * QB * T3C + t3;  // m = 1 (dir index 0)
-                const double *Y1 = Ys + ((1 * 2 + a1) * NQS + q1s) * QB * T3C + t3;  // m = 2
-                const double *Y2 = Ys + ((2 * 2 + a1) * NQS + q1s) * QB * T3C + t3;  // m = 3
-                for (int c2 = 0; c2 < nq2; ++c2) {
-                    const double y0 = Y0[c2 * T3C], y1 = Y1[c2 * T3C], y2 = Y2[c2 * T3C];
-                    #pragma unroll
-                    for (int t = 0; t < K; ++t) {
-                        const double2 bb = B2s[t * QB + c2];
-                        g1[t] = fma(bb.x, y0, g1[t]);                 // b1 = 1: m = 1, trial value in dir 2
-                        g0[t] = fma(bb.y, y1, fma(bb.x, y2, g0[t]));  // b1 = 0: m = 2 (B2'), m = 3 (B2)
+            __syncthreads();
+            // stage 2: fibres (t3l, q1s, a1) -> G ring
+            const int nfib2 = nqs * T3C * (STIFF ? 2 : 1);
+            for (int f = tid; f < nfib2; f += NT) {
+                const int t3l = f % T3C;
+                const int q1s = (f / T3C) % nqs;
+                const int a1 = STIFF ? f / (T3C * nqs) : 0;
+                const int slot = (qs + q1s) % RING;
+                double g0[K], g1[K];
+                #pragma unroll
+                for (int t = 0; t < K; ++t) { g0[t] = 0.0; g1[t] = 0.0; }
+                const double *Yb0 = Ys + ((0 * 2 + a1) * NQS + q1s) * QB * T3C + t3l;  // m = 0 (or mass)
+                const double *Yb1 = Ys + ((1 * 2 + a1) * NQS + q1s) * QB * T3C + t3l;  // m = 1
+                const double *Yb2 = Ys + ((2 * 2 + a1) * NQS + q1s) * QB * T3C + t3l;  // m = 2
+                auto point2 = [&](int c2, auto O) {
+                    constexpr int o0 = decltype(O)::value;
+                    const double2 *bp = B2s + c2 * NP;
+                    if (STIFF) {
+                        const double y0 = Yb0[c2 * T3C], y1 = Yb1[c2 * T3C], y2 = Yb2[c2 * T3C];
+                        #pragma unroll
+                        for (int r = 0; r <= P; ++r) {
+                            const double2 b = bp[r];
+                            g1[o0 + r] = fma(b.x, y0, g1[o0 + r]);                // b1 = 1: m = 0
+                            g0[o0 + r] = fma(b.y, y1, fma(b.x, y2, g0[o0 + r]));  // b1 = 0: m = 1, 2
+                        }
+                    } else {
+                        const double y = Yb0[c2 * T3C];
+                        #pragma unroll
+                        for (int r = 0; r <= P; ++r) g0[o0 + r] = fma(bp[r].x, y, g0[o0 + r]);
+                    }
+                };
+                if (t3l < nt3) {
+                    if (int2) {
+                        unroll<2 * P + 1>([&](auto C2) {
+                            constexpr int c2 = decltype(C2)::value;
+                            point2(c2, std::integral_constant<int, (c2 + 1) / 2>{});
+                        });
+                    } else {
+                        for (int c2 = 0; c2 < nq2; ++c2) {
+                            const int off = v2.span[ql2 + c2] - jl2;
+                            dispatch<0, K - NP>(off, [&](auto O) { point2(c2, O); });
+                        }
                     }
                 }
+                double *G0 = Gs + ((0 * 2 + a1) * RING + slot) * COLS + K * t3l;
+                double *G1 = Gs + ((1 * 2 + a1) * RING + slot) * COLS + K * t3l;
                 #pragma unroll
                 for (int t = 0; t < K; ++t) {
-                    Gs[(((0 * 2 + a1) * W + qw) * K + t) * T3C + t3] = g0[t];
-                    Gs[(((1 * 2 + a1) * W + qw) * K + t) * T3C + t3] = g1[t];
+                    G0[t] = g0[t];
+                    if (STIFF) G1[t] = g1[t];
                 }
-            } else {
-                const double *Y0 = Ys + q1s * QB * T3C + t3;
-                for (int c2 = 0; c2 < nq2; ++c2) {
-                    const double y = Y0[c2 * T3C];
-                    #pragma unroll
-                    for (int t = 0; t < K; ++t) g0[t] = fma(B2s[t * QB + c2].x, y, g0[t]);
-                }
-                #pragma unroll
-                for (int t = 0; t < K; ++t) Gs[(qw * K + t) * T3C + t3] = g0[t];
             }
+            __syncthreads();
         }
-        __syncthreads();
-    }
-    // ---- stage 1 per row: items (row b, t2, t3)
-    const int nitems = nrows * ni2 * nt3;
-    for (int it = tid; it < nitems; it += blockDim.x) {
-        const int t3 = it % nt3;
-        const int t2 = (it / nt3) % ni2;
-        const int b = it / (nt3 * ni2);
-        const int64_t i1 = r0 + b;
-        const int ni1 = v1.jlen[i1], nq1 = v1.qlen[i1];
-        const int qoff = (int)(v1.qlo[i1] - qw0);
-        double out[K];
+        q_done = q_hi;
+        // ---------------- stage 1: row group grp, batch rows bl = grp*NR + k
+        const int rg = r0 + grp * NR;
+        double acc[NR][K];
         #pragma unroll
-        for (int t = 0; t < K; ++t) out[t] = 0.0;
-        const double2 *B1r = B1s + b * K * QB;
-        const double *w1r = w1s + b * QB * 4;
-        for (int c1 = 0; c1 < nq1; ++c1) {
-            const int qw = qoff + c1;
+        for (int k = 0; k < NR; ++k)
+            #pragma unroll
+            for (int t = 0; t < K; ++t) acc[k][t] = 0.0;
+        const bool interior = rg >= P + 1 && rg + NR - 1 <= n1 - P - 2;
+        auto gload = [&](int slot, double &g00, double &g01, double &g10, double &g11) {
+            g00 = Gs[((0 * 2 + 0) * RING + slot) * COLS + colx];
             if (STIFF) {
-                const double g00 = Gs[(((0 * 2 + 0) * W + qw) * K + t2) * T3C + t3];
-                const double g01 = Gs[(((0 * 2 + 1) * W + qw) * K + t2) * T3C + t3];
-                const double g10 = Gs[(((1 * 2 + 0) * W + qw) * K + t2) * T3C + t3];
-                const double g11 = Gs[(((1 * 2 + 1) * W + qw) * K + t2) * T3C + t3];
-                const double2 wA = *(const double2 *)(w1r + c1 * 4);      // w^(0,0), w^(1,0)
-                const double2 wB = *(const double2 *)(w1r + c1 * 4 + 2);  // w^(0,1), w^(1,1)
-                const double u0 = fma(wA.x, g00, wA.y * g01);
-                const double u1 = fma(wB.x, g10, wB.y * g11);
+                g01 = Gs[((0 * 2 + 1) * RING + slot) * COLS + colx];
+                g10 = Gs[((1 * 2 + 0) * RING + slot) * COLS + colx];
+                g11 = Gs[((1 * 2 + 1) * RING + slot) * COLS + colx];
+            }
+        };
+        if (fin && interior) {
+            // rows of the group have the interior pattern: 2P+1 points, consecutive rows
+            // shifted by 2 points, staircase offset (c+1)/2
+            const int qb = qlo1[rg];
+            const int slot0 = qb % RING;
+            constexpr int UW = 2 * (NR - 1) + 2 * P + 1;
+            #pragma unroll
+            for (int u = 0; u < UW; ++u) {
+                int slot = slot0 + u;
+                if (slot >= RING) slot -= RING;
+                double g00, g01 = 0.0, g10 = 0.0, g11 = 0.0;
+                gload(slot, g00, g01, g10, g11);
+                double2 bb[NP];
                 #pragma unroll
-                for (int t = 0; t < K; ++t) {
-                    const double2 bb = B1r[t * QB + c1];
-                    out[t] = fma(bb.x, u0, fma(bb.y, u1, out[t]));
+                for (int r = 0; r <= P; ++r) bb[r] = B1w[slot * NP + r];
+                #pragma unroll
+                for (int k = 0; k < NR; ++k) {
+                    if (u >= 2 * k && u <= 2 * k + 2 * P) {
+                        const int c = u - 2 * k;
+                        const int o0 = (c + 1) / 2;
+                        const double2 *wr = W1b + ((grp * NR + k) * QB + c) * 2;
+                        if (STIFF) {
+                            const double2 wA = wr[0], wB = wr[1];
+                            const double u0 = fma(wA.x, g00, wA.y * g01);
+                            const double u1 = fma(wB.x, g10, wB.y * g11);
+                            #pragma unroll
+                            for (int r = 0; r <= P; ++r)
+                                acc[k][o0 + r] = fma(bb[r].x, u0, fma(bb[r].y, u1, acc[k][o0 + r]));
+                        } else {
+                            const double u0 = wr[0].x * g00;
+                            #pragma unroll
+                            for (int r = 0; r <= P; ++r) acc[k][o0 + r] = fma(bb[r].x, u0, acc[k][o0 + r]);
+                        }
+                    }
                 }
-            } else {
-                const double g = Gs[(qw * K + t2) * T3C + t3];
-                const double u = w1r[c1 * 4] * g;
-                #pragma unroll
-                for (int t = 0; t < K; ++t) out[t] = fma(B1r[t * QB + c1].x, u, out[t]);
             }
         }
-        const int64_t off = a.g.offset(i1, i2, i3) - a.val_base;
-        const int tt3 = t3a + t3;
-        const int64_t base = off + (int64_t)ni1 * (t2 + (int64_t)ni2 * tt3);
-        const int64_t jl1 = v1.jlo[i1];
-        const int64_t colbase = n1 * ((jl2 + t2) + n2 * (jl3 + tt3));
+        // write the group's rows (rows touching a boundary span are computed here one at a time)
         #pragma unroll
-        for (int t = 0; t < K; ++t) {
-            if (t < ni1) {
-                a.val[base + t] = out[t];
-                if (a.col) a.col[base + t] = (int32_t)(jl1 + t + colbase);
+        for (int k = 0; k < NR; ++k) {
+            const int i1 = rg + k;
+            const bool live = grp < NGRP && i1 < n1;
+            int64_t goff = 0;
+            int ni1 = 0;
+            if (live) {
+                ni1 = jlen1[i1];
+                goff = a.g.offset(i1, i2, i3) - a.val_base + (int64_t)ni1 * ni2 * t3a;
             }
+            if (fin && live) {
+                if (!interior) {
+                    double out[K];
+                    #pragma unroll
+                    for (int t = 0; t < K; ++t) out[t] = 0.0;
+                    const int q0 = qlo1[i1], nq1 = qlen1[i1], jl1 = jlo1[i1];
+                    for (int c = 0; c < nq1; ++c) {
+                        const int q = q0 + c;
+                        const int slot = q % RING;
+                        const double2 *bp = B1w + slot * NP;
+                        const double2 *wr = W1b + ((grp * NR + k) * QB + c) * 2;
+                        double g00, g01 = 0.0, g10 = 0.0, g11 = 0.0;
+                        gload(slot, g00, g01, g10, g11);
+                        double u0, u1 = 0.0;
+                        if (STIFF) {
+                            const double2 wA = wr[0], wB = wr[1];
+                            u0 = fma(wA.x, g00, wA.y * g01);
+                            u1 = fma(wB.x, g10, wB.y * g11);
+                        } else {
+                            u0 = wr[0].x * g00;
+                        }
+                        const int off = span1[q] - jl1;
+                        dispatch<0, K - NP>(off, [&](auto O) {
+                            #pragma unroll
+                            for (int r = 0; r <= P; ++r) {
+                                constexpr int o0 = decltype(O)::value;
+                                const double2 b = bp[r];
+                                out[o0 + r] = STIFF ? fma(b.x, u0, fma(b.y, u1, out[o0 + r])) : fma(b.x, u0, out[o0 + r]);
+                            }
+                        });
+                    }
+                    #pragma unroll
+                    for (int t = 0; t < K; ++t) acc[k][t] = out[t];
+                }
+                // stage in CSR order of the row's chunk: t1 + ni1 * (t2 + ni2 * t3l), shifted so
+                // that the 16-B aligned part of the global segment starts on a 16-B boundary
+                const int colbase = jlo1[i1] + n1 * ((jl2 + t2c) + n2 * (jl3 + t3a + t3c));
+                const int e0 = ni1 * (t2c + ni2 * t3c);
+                double *sv = Sv + (sbuf * NGRP + grp) * STV + (int)(goff & 1);
+                int32_t *sc = Sc + (sbuf * NGRP + grp) * 2 * STC + (int)(goff & 3);
+                #pragma unroll
+                for (int t = 0; t < K; ++t)
+                    if (t < ni1) {
+                        sv[e0 + t] = acc[k][t];
+                        sc[e0 + t] = colbase + t;
+                    }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            // one thread per group issues the TMA bulk copies of its row segment
+            if (live && colx == 0) {
+                const int len = ni1 * ni2 * nt3;
+                const double *sv = Sv + (sbuf * NGRP + grp) * STV + (int)(goff & 1);
+                const int32_t *sc = Sc + (sbuf * NGRP + grp) * 2 * STC + (int)(goff & 3);
+                double *dv = a.val + goff;
+                const int hv = (int)(goff & 1);              // unaligned head (values)
+                const int nbv = (len - hv) & ~1;             // bulk elements
+                if (hv && len > 0) dv[0] = sv[0];
+                if (nbv > 0) bulk_s2g(dv + hv, sv + hv, (unsigned)nbv * 8u);
+                for (int e = hv + nbv; e < len; ++e) dv[e] = sv[e];
+                if (a.col) {
+                    int32_t *dc = a.col + goff;
+                    const int hc = (4 - (int)(goff & 3)) & 3;
+                    const int hcn = hc < len ? hc : len;
+                    const int nbc = (len - hcn) & ~3;
+                    for (int e = 0; e < hcn; ++e) dc[e] = sc[e];
+                    if (nbc > 0) bulk_s2g(dc + hcn, sc + hcn, (unsigned)nbc * 4u);
+                    for (int e = hcn + nbc; e < len; ++e) dc[e] = sc[e];
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                // the other buffer is reused next: its copies (one group back) must have read smem
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            }
+            sbuf ^= 1;
+            __syncthreads();
         }
     }
+    if (colx == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 template <int P, bool STIFF>
@@ -321,25 +479,22 @@ wq_status launch_tile_p(wq_plan_s *Pl, double *val, int32_t *col, int64_t pl_lo,
     a.col = col;
     a.val_base = val_base;
     a.plane_lo = pl_lo;
-    const int64_t n1 = Pl->dir[0].n;
-    a.n_batch = (int)((n1 + CF::RB - 1) / CF::RB);
-    a.n_chunk = (CF::K + CF::T3C - 1) / CF::T3C;
     const int64_t lines = Pl->dir[1].n * (pl_hi - pl_lo);
-    const int64_t blocks = lines * a.n_batch * a.n_chunk;
+    const int64_t blocks = lines * CF::NCH;
     static bool set = false;
     if (!set) {
         cudaFuncSetAttribute(k_tile<P, STIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
         set = true;
     }
     if (blocks > 0) {
-        k_tile<P, STIFF><<<(unsigned)blocks, 256, CF::SMEM, s>>>(a);
+        k_tile<P, STIFF><<<(unsigned)blocks, CF::NT, CF::SMEM, s>>>(a);
         wq_count_launches(1);
     }
     return wq_cuda_status(cudaGetLastError(), "tile assembly kernel");
 }
 
 template <bool STIFF>
-wq_status dispatch(wq_plan_s *Pl, double *val, int32_t *col, int64_t lo, int64_t hi, int64_t vb, cudaStream_t s) {
+wq_status dispatch_p(wq_plan_s *Pl, double *val, int32_t *col, int64_t lo, int64_t hi, int64_t vb, cudaStream_t s) {
     switch (Pl->p) {
     case 1: return launch_tile_p<1, STIFF>(Pl, val, col, lo, hi, vb, s);
     case 2: return launch_tile_p<2, STIFF>(Pl, val, col, lo, hi, vb, s);
@@ -372,6 +527,6 @@ wq_status launch_assemble_tile(wq_plan_s *P, int matrix, double *val, int32_t *c
         wq_set_error("tile kernel not available for this plan");
         return WQ_EINVAL;
     }
-    return matrix == WQ_MASS ? dispatch<false>(P, val, col, plane_lo, plane_hi, val_base, s)
-                             : dispatch<true>(P, val, col, plane_lo, plane_hi, val_base, s);
+    return matrix == WQ_MASS ? dispatch_p<false>(P, val, col, plane_lo, plane_hi, val_base, s)
+                             : dispatch_p<true>(P, val, col, plane_lo, plane_hi, val_base, s);
 }

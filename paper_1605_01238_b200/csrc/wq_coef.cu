@@ -31,11 +31,11 @@ struct CoefArgs {
     Flags *flags;
 };
 
-// table rows at grid point q: N = degree p (functions span..span+p),
-// M = degree p-1 (functions span+1..span+p)
-__device__ __forceinline__ const double *Ntab(const DirView &v, int p, int64_t q) { return v.B + q * WQ_BROWS * (p + 1); }
+// table rows at grid point q: N = degree p (functions span..span+p, stride 2:
+// values interleaved with derivatives), M = degree p-1 (functions span+1..span+p)
+__device__ __forceinline__ const double *Ntab(const DirView &v, int p, int64_t q) { return v.B + q * wq_bstride(p); }
 __device__ __forceinline__ const double *Mtab(const DirView &v, int p, int64_t q) {
-    return v.B + q * WQ_BROWS * (p + 1) + 2 * (p + 1);
+    return v.B + q * wq_bstride(p) + 2 * (p + 1);
 }
 // p / (xi_{k+p} - xi_k): scale of derivative control point k (k >= 1)
 __device__ __forceinline__ double dscale(const DirView &v, int p, int64_t k) {
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(TQ1) k_coef(CoefArgs a) {
             for (int r = 0; r <= p; ++r) {
                 const int64_t k3 = e3 + r;
                 const int64_t k = k1 + n1 * (k2 + n2 * k3);
-                const double nv = n3[r];
+                const double nv = n3[2 * r];
                 const double s3 = r >= 1 ? dscale(v3, p, k3) : 0.0;
                 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(TQ1) k_coef(CoefArgs a) {
             const int c2s = (int)(v2.span[q2] - k2a);
             double X1[3] = {0, 0, 0}, X2[3] = {0, 0, 0}, X3[3] = {0, 0, 0};
             for (int r = 0; r <= p; ++r) {
-                const double nv = n2t[r], mv = r < p ? m2t[r] : 0.0;
+                const double nv = n2t[2 * r], mv = r < p ? m2t[r] : 0.0;
                 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     X1[c] = fma(nv, Asm[((0 * 3 + c) * K2M + c2s + r) * K1M + c1], X1[c]);
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(TQ1) k_coef(CoefArgs a) {
                 for (int c = 0; c < 2; ++c) {
                     const double cur = k1 < n1 ? __ldg(P + k * 2 + c) : 0.0;
                     const double d1 = (k1 >= 1 && k1 < n1) ? (cur - __ldg(P + (k - 1) * 2 + c)) * s1 : 0.0;
-                    X1[c] = fma(n2t[r], d1, X1[c]);
+                    X1[c] = fma(n2t[2 * r], d1, X1[c]);
                     if (r >= 1) X2[c] = fma(m2t[r - 1], (cur - prev[c]) * s2, X2[c]);
                     prev[c] = cur;
                 }
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(TQ1) k_coef(CoefArgs a) {
         } else {
             const double *X = Xsm + (t2 * 3) * 3 * K1M;
             for (int r = 0; r <= p; ++r) {
-                const double nv = n1t[r], mv = r < p ? m1t[r] : 0.0;
+                const double nv = n1t[2 * r], mv = r < p ? m1t[r] : 0.0;
                 #pragma unroll
                 for (int c = 0; c < D; ++c) {
                     if (r < p) J[c][0] = fma(mv, X[(0 * 3 + c) * K1M + c1s + 1 + r], J[c][0]);

@@ -9,6 +9,8 @@
 #define WQ_PMAX WQ_MAX_DEGREE          // compile-time bound on p
 #define WQ_KMAX (2 * WQ_PMAX + 1)      // max #I_i
 #define WQ_BROWS 3                     // rows of the per-point basis table
+// doubles per point of the basis table, even so (value, derivative) pairs are 16-B aligned
+__host__ __device__ constexpr int wq_bstride(int p) { return (WQ_BROWS * (p + 1) + 1) & ~1; }
 
 // Device view of one parametric direction.  For l >= d the direction is a
 // dummy of extent 1 (n = nq = 1, one point, weight 1, B = 1, B' = 0).
@@ -24,9 +26,9 @@ struct DirView {
     int32_t *qlo, *qlen;  // [n] Q_i = [qlo, qlo+qlen)
     int32_t *jlo, *jlen;  // [n] I_i = [jlo, jlo+jlen)
     int64_t *pref;        // [n+1] prefix sums of jlen
-    double *B;            // [nq][WQ_BROWS][p+1]: values, first derivatives of functions
-                          // span..span+p, and degree p-1 values of span+1..span+p (last slot 0)
-    double *W;            // [n][4][maxq] weights, family f = a + 2b
+    double *B;            // [nq][wq_bstride(p)]: (value, first derivative) pairs of functions
+                          // span..span+p, then degree p-1 values of span+1..span+p (last slot 0)
+    double *W;            // [n][maxq][4] weights, family f = a + 2b fastest
 };
 
 struct Flags {   // device-side latched errors

@@ -136,10 +136,10 @@ __global__ void k_basis(DirArgs a) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < v.nq; g += (int64_t)gridDim.x * blockDim.x) {
         dd N[WQ_PMAX + 1], dN[WQ_PMAX + 1], Nl[WQ_PMAX + 1];
         bspl_dd(v.knots, p, v.span[g], dd_make(v.pts[g]), N, dN, Nl);
-        double *o = v.B + g * WQ_BROWS * (p + 1);
+        double *o = v.B + g * wq_bstride(p);  // [(value, derivative) pairs][degree p-1 values]
         for (int r = 0; r <= p; ++r) {
-            o[r] = dd_to_d(N[r]);
-            o[p + 1 + r] = dd_to_d(dN[r]);
+            o[2 * r] = dd_to_d(N[r]);
+            o[2 * r + 1] = dd_to_d(dN[r]);
             o[2 * (p + 1) + r] = r < p ? dd_to_d(Nl[r]) : 0.0;
         }
     }
@@ -371,9 +371,9 @@ __global__ void __launch_bounds__(64) k_weights(DirArgs a, const double *__restr
     }
     __syncthreads();
     // Phase 5: round, store, residual check on all #I equations (Eq. exact)
-    double *W = v.W + (size_t)i * 4 * v.maxq;
+    double *W = v.W + (size_t)i * 4 * v.maxq;  // [c][family]
     for (int t = tid; t < 4 * v.maxq; t += blockDim.x) {
-        int f = t / v.maxq, q = t % v.maxq;
+        int q = t >> 2, f = t & 3;
         int bb = f >> 1, aa = f & 1;
         W[t] = q < nqi ? dd_to_d(Z[(bb * 2 + aa) * QM + q]) : 0.0;
     }
