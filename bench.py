@@ -104,23 +104,13 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------- ours
-def slab_cuts(cfg, world):
-    """Contiguous planes of the slowest index, balanced by nnz (closed form)."""
-    n, p = cfg.n_el + cfg.p, cfg.p
-    ni = np.array([min(n - 1, i + p) - max(0, i - p) + 1 for i in range(n)], dtype=np.int64)
-    c = np.concatenate([[0], np.cumsum(ni)])
-    targets = [c[-1] * r / world for r in range(world + 1)]
-    cuts = [int(np.searchsorted(c, t)) for t in targets]
-    cuts[0], cuts[-1] = 0, n
-    return cuts
-
-
 def run_ours(cfg, steps, warmup, rank, world, device, dist, want_e2e=True, want_roofline=True):
     import torch
     import paper_1605_01238_b200 as wq
 
     torch.cuda.set_device(device)
-    cuts = slab_cuts(cfg, world)
+    from paper_1605_01238_b200.dist import slab_cuts
+    cuts = slab_cuts(cfg.n_el + cfg.p, cfg.p, world)
     knots = cfg.knots()
     ctrl = cfg.ctrl()
     plan = wq.Plan(cfg.p, knots, slab=(cuts[rank], cuts[rank + 1]), need_mass=False, need_stiffness=True,
@@ -138,7 +128,7 @@ def run_ours(cfg, steps, warmup, rank, world, device, dist, want_e2e=True, want_
         with torch.cuda.stream(stream):
             wq.wq_build_rules(plan.h, stream)
             wq.wq_build_coef(plan.h, d_ctrl, stream)
-            if world > 1:
+            if world > 1:  # the one exchange: all-gather of per-rank nnz -> row_ptr base
                 dist.all_gather_into_tensor(nnz_all, my_nnz)
                 base = int(nnz_all[:rank].sum().item()) if rank else 0
             else:
