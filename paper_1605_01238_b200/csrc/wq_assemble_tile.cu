@@ -70,14 +70,22 @@ struct Cfg {
     static_assert(SMEM <= 227 * 1024, "tile kernel shared memory");
 };
 
-// compile-time dispatch of a runtime offset o in [O, HI]: f(integral_constant<o>)
-template <int O, int HI, class F>
+// compile-time dispatch of a runtime offset o in [LO, HI] (|o| <= 31): f(integral_constant<o>);
+// a dense switch, compiled to a jump table (one indirect branch, uniform across the CTA)
+#define WQ_CASE(O) \
+    case O:        \
+        if constexpr ((O) >= LO && (O) <= HI) f(std::integral_constant<int, (O)>{}); \
+        break;
+#define WQ_CASE8(B) WQ_CASE(B) WQ_CASE(B + 1) WQ_CASE(B + 2) WQ_CASE(B + 3) WQ_CASE(B + 4) WQ_CASE(B + 5) WQ_CASE(B + 6) WQ_CASE(B + 7)
+template <int LO, int HI, class F>
 __device__ __forceinline__ void dispatch(int o, F &&f) {
-    if constexpr (O <= HI) {
-        if (o == O) f(std::integral_constant<int, O>{});
-        else dispatch<O + 1, HI>(o, f);
+    static_assert(LO >= -16 && HI < 32, "dispatch range");
+    switch (o) {
+        WQ_CASE8(-16) WQ_CASE8(-8) WQ_CASE8(0) WQ_CASE8(8) WQ_CASE8(16) WQ_CASE8(24)
+    default: break;
     }
 }
+#undef WQ_CASE8
 
 template <int N, class F>
 __device__ __forceinline__ void unroll(F &&f) {
@@ -167,6 +175,9 @@ __global__ void __launch_bounds__(256, 1) k_tile(TileArgs a) {
     // coefficient field restricted to this line
     const double *__restrict__ Cl = a.coef + (int64_t)ql2 * a.nq1 + (int64_t)(ql3 - a.cq_b) * plane_stride;
 
+    // CSR offset of row (0, i2, i3) relative to the first owned row; row i1 adds ni2*ni3*P1(i1)
+    const int64_t line_off = a.g.offset(0, i2, i3) - a.val_base;
+    const int64_t *__restrict__ pref1 = a.g.pref[0];
     // final-stage thread role: group grp, column colx = t2 + K*t3l
     const int grp = tid / COLS, colx = tid % COLS;
     const int t2c = colx % K, t3c = colx / K;
@@ -191,69 +202,88 @@ __global__ void __launch_bounds__(256, 1) k_tile(TileArgs a) {
         // ---------------- stages 3 and 2 for the new points (q_done, q_hi]
         for (int qs = q_done + 1; qs <= q_hi; qs += NQS) {
             const int nqs = q_hi - qs + 1 < NQS ? q_hi - qs + 1 : NQS;
-            // stage 3: fibres (q1s, c2, m); coefficient loads hoisted into registers
-            const int nfib = nqs * nq2 * (STIFF ? 3 : 1);
+            // stage 3: fibres (q1s, m, c2), q1s fastest; compile-time divisors only
+            const int nfib = NQS * (STIFF ? 3 : 1) * nq2;
             for (int f = tid; f < nfib; f += NT) {
-                const int q1s = f % nqs;
-                const int c2 = (f / nqs) % nq2;
-                const int m = STIFF ? f / (nqs * nq2) : 0;
-                const double *cp = Cl + (int64_t)c2 * a.nq1 + (qs + q1s);
+                const int q1s = f % NQS;
+                const int rest = f / NQS;
+                const int m = STIFF ? rest % 3 : 0;
+                const int c2 = STIFF ? rest / 3 : rest;
+                if (q1s >= nqs) continue;
                 double y0[T3C], y1[T3C];
                 #pragma unroll
                 for (int t = 0; t < T3C; ++t) { y0[t] = 0.0; y1[t] = 0.0; }
                 const int b3 = STIFF && m == 2 ? 1 : 0;
                 const double2 w2v = W2s[c2 * 2 + (STIFF && m == 1 ? 1 : 0)];  // (w2^(0,b2), w2^(1,b2))
-                const double *Ca = cp + (int64_t)(STIFF ? comp_ix(0, m) : a.comp_mass) * a.npts;
-                const double *Cb = cp + (int64_t)comp_ix(1, m) * a.npts;
-                const double *Cc = cp + (int64_t)comp_ix(2, m) * a.npts;
-                double ca[QB], cb[QB], cc[QB];
-                #pragma unroll
-                for (int c3 = 0; c3 < QB; ++c3)
-                    if (c3 < nq3) {
-                        const int64_t o = plane_stride * c3;
-                        ca[c3] = __ldg(Ca + o);
-                        if (STIFF) { cb[c3] = __ldg(Cb + o); cc[c3] = __ldg(Cc + o); }
-                    }
-                // contribution of point c3 at staircase offset O (compile time)
-                auto point3 = [&](int c3, auto O) {
+                // components C_{0m}, C_{1m}, C_{2m} (upper-triangle storage) or c
+                const int ka = STIFF ? m : a.comp_mass;
+                const int kb = m == 0 ? 1 : (m == 1 ? 3 : 4);
+                const int kc = m == 0 ? 2 : (m == 1 ? 4 : 5);
+                const int64_t fo = (int64_t)c2 * a.nq1 + (qs + q1s);
+                const double *pa = Cl + (int64_t)ka * a.npts + fo;
+                const double *pb = Cl + (int64_t)kb * a.npts + fo;
+                const double *pc = Cl + (int64_t)kc * a.npts + fo;
+                const double *B3b = (const double *)B3s + b3;  // value (b3 = 0) or derivative column
+                // contribution of point c3 (coefficients ca, cb, cc) at staircase offset O (compile time)
+                auto point3 = [&](int c3, double ca, double cb, double cc, auto O) {
                     constexpr int o0 = decltype(O)::value;
                     const double2 w3v = W3s[c3 * 2 + b3];  // (w3^(0,b3), w3^(1,b3))
-                    const double2 *bp = B3s + c3 * NP;
+                    const double *bp = B3b + c3 * 2 * NP;
                     if (STIFF) {
-                        const double h1 = w2v.x * w3v.x * ca[c3];                             // l = 0
-                        const double h0 = fma(w2v.y * w3v.x, cb[c3], w2v.x * w3v.y * cc[c3]);  // l = 1, 2
+                        const double h1 = w2v.x * w3v.x * ca;                        // l = 0
+                        const double h0 = fma(w2v.y * w3v.x, cb, w2v.x * w3v.y * cc);  // l = 1, 2
                         #pragma unroll
                         for (int r = 0; r <= P; ++r) {
                             const int t = o0 + r;
                             if (t >= 0 && t < T3C) {
-                                const double2 bb = bp[r];
-                                const double bv = b3 ? bb.y : bb.x;
+                                const double bv = bp[2 * r];
                                 y1[t] = fma(bv, h1, y1[t]);
                                 y0[t] = fma(bv, h0, y0[t]);
                             }
                         }
                     } else {
-                        const double h = w2v.x * w3v.x * ca[c3];
+                        const double h = w2v.x * w3v.x * ca;
                         #pragma unroll
                         for (int r = 0; r <= P; ++r) {
                             const int t = o0 + r;
-                            if (t >= 0 && t < T3C) y0[t] = fma(bp[r].x, h, y0[t]);
+                            if (t >= 0 && t < T3C) y0[t] = fma(bp[2 * r], h, y0[t]);
                         }
                     }
                 };
                 if (int3) {
-                    unroll<2 * P + 1>([&](auto C3) {
+                    // interior, unchunked: all loads hoisted, compile-time staircase (c3+1)/2
+                    constexpr int NQ = 2 * P + 1;
+                    double ca[NQ], cb[NQ], cc[NQ];
+                    #pragma unroll
+                    for (int c3 = 0; c3 < NQ; ++c3) {
+                        ca[c3] = __ldg(pa);
+                        if (STIFF) { cb[c3] = __ldg(pb); cc[c3] = __ldg(pc); }
+                        pa += plane_stride;
+                        pb += plane_stride;
+                        pc += plane_stride;
+                    }
+                    unroll<NQ>([&](auto C3) {
                         constexpr int c3 = decltype(C3)::value;
-                        point3(c3, std::integral_constant<int, (c3 + 1) / 2>{});
+                        point3(c3, ca[c3], STIFF ? cb[c3] : 0.0, STIFF ? cc[c3] : 0.0,
+                               std::integral_constant<int, (c3 + 1) / 2>{});
                     });
                 } else {
-                    #pragma unroll
-                    for (int c3 = 0; c3 < QB; ++c3)
-                        if (c3 < nq3) {
-                            const int off = v3.span[ql3 + c3] - jl3 - t3a;
-                            if (CF::NCH == 1) dispatch<0, K - NP>(off, [&](auto O) { point3(c3, O); });
-                            else dispatch<-P, T3C - 1>(off, [&](auto O) { point3(c3, O); });
+                    // boundary or chunked: rolled loop, next point's coefficients prefetched
+                    double na = __ldg(pa), nb = STIFF ? __ldg(pb) : 0.0, nc = STIFF ? __ldg(pc) : 0.0;
+                    #pragma unroll 1
+                    for (int c3 = 0; c3 < nq3; ++c3) {
+                        const double ca = na, cb = nb, cc = nc;
+                        if (c3 + 1 < nq3) {
+                            pa += plane_stride;
+                            pb += plane_stride;
+                            pc += plane_stride;
+                            na = __ldg(pa);
+                            if (STIFF) { nb = __ldg(pb); nc = __ldg(pc); }
                         }
+                        const int off = v3.span[ql3 + c3] - jl3 - t3a;
+                        if (CF::NCH == 1) dispatch<0, K - NP>(off, [&](auto O) { point3(c3, ca, cb, cc, O); });
+                        else dispatch<-P, T3C - 1>(off, [&](auto O) { point3(c3, ca, cb, cc, O); });
+                    }
                 }
                 double *Y1 = Ys + (((m * 2 + 1) * NQS + q1s) * QB + c2) * T3C;
                 double *Y0 = Ys + (((m * 2 + 0) * NQS + q1s) * QB + c2) * T3C;
@@ -264,12 +294,13 @@ __global__ void __launch_bounds__(256, 1) k_tile(TileArgs a) {
                 }
             }
             __syncthreads();
-            // stage 2: fibres (t3l, q1s, a1) -> G ring
-            const int nfib2 = nqs * T3C * (STIFF ? 2 : 1);
+            // stage 2: fibres (t3l, a1, q1s), compile-time divisors only
+            const int nfib2 = T3C * (STIFF ? 2 : 1) * nqs;
             for (int f = tid; f < nfib2; f += NT) {
                 const int t3l = f % T3C;
-                const int q1s = (f / T3C) % nqs;
-                const int a1 = STIFF ? f / (T3C * nqs) : 0;
+                const int rest = f / T3C;
+                const int a1 = STIFF ? rest & 1 : 0;
+                const int q1s = STIFF ? rest >> 1 : rest;
                 const int slot = (qs + q1s) % RING;
                 double g0[K], g1[K];
                 #pragma unroll
@@ -380,7 +411,7 @@ __global__ void __launch_bounds__(256, 1) k_tile(TileArgs a) {
             int ni1 = 0;
             if (live) {
                 ni1 = jlen1[i1];
-                goff = a.g.offset(i1, i2, i3) - a.val_base + (int64_t)ni1 * ni2 * t3a;
+                goff = line_off + (int64_t)(ni2 * ni3) * pref1[i1] + ni1 * ni2 * t3a;
             }
             if (fin && live) {
                 if (!interior) {

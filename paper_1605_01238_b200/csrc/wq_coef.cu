@@ -16,8 +16,9 @@
 
 namespace {
 
-constexpr int TQ1 = 64;  // q_1 points per CTA (threads)
-constexpr int TQ2 = 8;   // q_2 points per CTA
+constexpr int TQ1 = 32;  // q_1 points per CTA
+constexpr int TQ2 = 8;   // q_2 points per CTA (D >= 2); threads = TQ1 * TQ2, one per point in stage C
+constexpr int NTC = TQ1 * TQ2;
 
 struct CoefArgs {
     DirView v[3];
@@ -43,7 +44,7 @@ __device__ __forceinline__ double dscale(const DirView &v, int p, int64_t k) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(TQ1) k_coef(CoefArgs a) {
+__global__ void __launch_bounds__(NTC) k_coef(CoefArgs a) {
     extern __shared__ __align__(16) double sm[];
     const int p = a.p;
     const DirView &v1 = a.v[0], &v2 = a.v[1], &v3 = a.v[2];
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(TQ1) k_coef(CoefArgs a) {
     if (D >= 2) { k2a = v2.span[q2off + q2a]; k2e = v2.span[q2off + q2e - 1] + p + 1; }
     const int K2 = (int)(k2e - k2a);
     const int64_t n1 = v1.n, n2 = D >= 2 ? v2.n : 1;
-    const int K1M = TQ1 + WQ_PMAX + 1, K2M = TQ2 + WQ_PMAX + 1;
+    const int K1M = TQ1 + p + 1, K2M = TQ2 + p + 1;  // bounds of K1, K2 (smem sized by the actual p)
     // smem: A[3 variants][3 comps][K2M][K1M] (D == 3), X[TQ2][3 variants][3 comps][K1M]
     double *Asm = sm;
     double *Xsm = sm + (D == 3 ? 9 * K2M * K1M : 0);
@@ -161,16 +162,16 @@ __global__ void __launch_bounds__(TQ1) k_coef(CoefArgs a) {
         }
         __syncthreads();
     }
-    // stage C: one thread per q1, loop over the q2 of the tile
-    const int t1 = tid;
-    if (t1 >= nt1) return;
+    // stage C: one thread per point (q1, q2) of the tile
+    const int t1 = tid % TQ1, t2 = D >= 2 ? tid / TQ1 : 0;
+    if (t1 >= nt1 || (D >= 2 && t2 >= nt2) || (D == 1 && tid >= TQ1)) return;
     const int64_t q1 = q1a + t1;
     const double *n1t = Ntab(v1, p, q1off + q1), *m1t = Mtab(v1, p, q1off + q1);
     const int64_t e1 = v1.span[q1off + q1];
     const int c1s = (int)(e1 - k1a);
     const int64_t npts_plane = nq1 * (D >= 2 ? nq2 : 1);
     const int64_t npts = npts_plane * (D == 3 ? a.nq_loc_d : 1);
-    for (int t2 = 0; t2 < (D >= 2 ? nt2 : 1); ++t2) {
+    {
         double J[3][3];
         #pragma unroll
         for (int c = 0; c < 3; ++c)
@@ -252,21 +253,21 @@ wq_status launch_coef(wq_plan_s *P, const double *ctrl, cudaStream_t s) {
     a.need_s = P->need_stiff;
     a.need_m = P->need_mass;
     a.flags = P->flags;
-    const int K1M = TQ1 + WQ_PMAX + 1, K2M = TQ2 + WQ_PMAX + 1;
+    const int K1M = TQ1 + P->p + 1, K2M = TQ2 + P->p + 1;
     if (P->d == 3) {
         size_t sm = (size_t)(9 * K2M * K1M + TQ2 * 9 * K1M) * sizeof(double);
         static bool set = false;
-        if (!set) { cudaFuncSetAttribute(k_coef<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); set = true; }
+        if (!set) { cudaFuncSetAttribute(k_coef<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024); set = true; }
         dim3 g((unsigned)((P->dir[0].nq + TQ1 - 1) / TQ1), (unsigned)((P->dir[1].nq + TQ2 - 1) / TQ2),
                (unsigned)a.nq_loc_d);
-        k_coef<3><<<g, TQ1, sm, s>>>(a);
+        k_coef<3><<<g, NTC, sm, s>>>(a);
     } else if (P->d == 2) {
         size_t sm = (size_t)(TQ2 * 9 * K1M) * sizeof(double);
         dim3 g((unsigned)((P->dir[0].nq + TQ1 - 1) / TQ1), (unsigned)((a.nq_loc_d + TQ2 - 1) / TQ2), 1);
-        k_coef<2><<<g, TQ1, sm, s>>>(a);
+        k_coef<2><<<g, NTC, sm, s>>>(a);
     } else {
         dim3 g((unsigned)((a.nq_loc_d + TQ1 - 1) / TQ1), 1, 1);
-        k_coef<1><<<g, TQ1, 0, s>>>(a);
+        k_coef<1><<<g, NTC, 0, s>>>(a);
     }
     wq_count_launches(1);
     return wq_cuda_status(cudaGetLastError(), "coefficient kernel");
