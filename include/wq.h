@@ -63,8 +63,14 @@ typedef enum { WQ_MASS = 0, WQ_STIFFNESS = 1 } wq_matrix;
 typedef enum {
     WQ_KERNEL_AUTO = 0,   /* fastest available for (d, p)                     */
     WQ_KERNEL_DIRECT = 1, /* per-entry direct nested sum (Eq. massquadrature) */
-    WQ_KERNEL_TILE = 2    /* sum-factorised row-tile kernel (Eq. sumfactorization
+    WQ_KERNEL_TILE = 2,   /* sum-factorised row-tile kernel (Eq. sumfactorization
                              P:837, rows of a tile share the d..2 stages)      */
+    WQ_KERNEL_WS = 3,     /* same arithmetic as TILE, warp-specialised
+                             persistent pipeline (TMA coefficient stream,
+                             stage-3/2 producer warps, stage-1 consumer warps) */
+    WQ_KERNEL_LINE = 4    /* lines interior in directions 2, 3 by the
+                             warp-specialised line kernel (independent producer
+                             warps, 2-point TMA tasks), the others by TILE    */
 } wq_kernel;
 
 typedef struct wq_plan_s *wq_plan;

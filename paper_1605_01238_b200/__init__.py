@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libwq.so")
 
 WQ_OK, WQ_EINVAL, WQ_EKNOTS, WQ_ESINGULAR, WQ_EGEOMETRY, WQ_ENOMEM, WQ_ECUDA, WQ_ERANGE = range(8)
 WQ_MASS, WQ_STIFFNESS = 0, 1
-WQ_KERNEL_AUTO, WQ_KERNEL_DIRECT, WQ_KERNEL_TILE = 0, 1, 2
+WQ_KERNEL_AUTO, WQ_KERNEL_DIRECT, WQ_KERNEL_TILE, WQ_KERNEL_WS, WQ_KERNEL_LINE = 0, 1, 2, 3, 4
 WQ_MAX_DEGREE = 10
 
 EXPORTED = ("wq_plan_create", "wq_plan_destroy", "wq_plan_info", "wq_build_rules", "wq_build_coef",

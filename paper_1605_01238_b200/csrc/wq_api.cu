@@ -8,6 +8,7 @@
 #include <string>
 #include <atomic>
 #include <vector>
+#include <algorithm>
 #include "wq_internal.cuh"
 
 namespace {
@@ -150,6 +151,9 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     int64_t cp = P->cq_e - P->cq_b;
     for (int l = 0; l < ld; ++l) cp *= P->dir[l].nq;
     P->coef_points = cp;
+    P->c0off = d == 3 ? 1 : 0;
+    P->cld1 = d == 3 ? (P->dir[0].nq + 2) / 2 * 2 : P->dir[0].nq;
+    P->cstride = d == 3 ? cp / P->dir[0].nq * P->cld1 : cp;
     P->ncomp_s = P->need_stiff ? d * (d + 1) / 2 : 0;
     P->ncomp = P->ncomp_s + P->need_mass;
 
@@ -199,14 +203,37 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     }
     P->gl = (double *)(A + o_gl);
     P->flags = (Flags *)(A + o_fl);
-    size_t cbytes = sizeof(double) * (size_t)P->ncomp * (size_t)P->coef_points;
+    size_t cbytes = sizeof(double) * (size_t)P->ncomp * (size_t)P->cstride;
     ce = cudaMalloc((void **)&P->coef, cbytes);
     if (ce != cudaSuccess) {
         P->coef = nullptr;
         wq_plan_destroy(P);
         return fail(WQ_ENOMEM, "coefficient field allocation failed (" + std::to_string(cbytes) + " bytes)");
     }
-    P->workspace_bytes = (int64_t)(bytes + cbytes);
+    // row lines of the slab, split for the line kernel (interior in directions 2 and 3) vs the rest
+    P->lines_dev = nullptr;
+    size_t lbytes = 0;
+    if (d == 3) {
+        const int64_t n2 = P->dir[1].n;
+        auto inter = [&](int l, int64_t i) {
+            const int64_t E = P->dir[l].E, n = P->dir[l].n;
+            return i >= p + 1 && i <= n - p - 2 && host_qhi(i, E, p) - host_qlo(i, E, p) + 1 == 2 * p + 1;
+        };
+        for (int64_t i3 = P->slab_b; i3 < P->slab_e; ++i3)
+            for (int64_t i2 = 0; i2 < n2; ++i2) {
+                const int32_t line = (int32_t)(i2 + n2 * (i3 - P->slab_b));
+                (inter(1, i2) && inter(2, i3) ? P->lines_int : P->lines_bnd).push_back(line);
+            }
+        lbytes = sizeof(int32_t) * (P->lines_int.size() + P->lines_bnd.size());
+        ce = cudaMalloc((void **)&P->lines_dev, lbytes > 0 ? lbytes : 4);
+        if (ce != cudaSuccess) { P->lines_dev = nullptr; wq_plan_destroy(P); return fail(WQ_ENOMEM, "line lists"); }
+        if (!P->lines_int.empty())
+            cudaMemcpy(P->lines_dev, P->lines_int.data(), sizeof(int32_t) * P->lines_int.size(), cudaMemcpyHostToDevice);
+        if (!P->lines_bnd.empty())
+            cudaMemcpy(P->lines_dev + P->lines_int.size(), P->lines_bnd.data(), sizeof(int32_t) * P->lines_bnd.size(),
+                       cudaMemcpyHostToDevice);
+    }
+    P->workspace_bytes = (int64_t)(bytes + cbytes + lbytes);
     *out = P;
     return WQ_OK;
 }
@@ -216,6 +243,7 @@ wq_status wq_plan_destroy(wq_plan P) {
     cudaSetDevice(P->device);
     if (P->arena) cudaFree(P->arena);
     if (P->coef) cudaFree(P->coef);
+    if (P->lines_dev) cudaFree(P->lines_dev);
     if (P->ctrl_dev) cudaFree(P->ctrl_dev);
     if (P->stage_val) cudaFree(P->stage_val);
     delete P;
@@ -272,10 +300,31 @@ static wq_status assemble_range(wq_plan_s *P, int matrix, wq_kernel kernel, doub
                                 int64_t pl_lo, int64_t pl_hi, int64_t val_base, cudaStream_t s) {
     if (matrix == WQ_MASS && !P->need_mass) return fail(WQ_EINVAL, "plan was created without need_mass");
     if (matrix == WQ_STIFFNESS && !P->need_stiff) return fail(WQ_EINVAL, "plan was created without need_stiffness");
-    bool tile = tile_supported(P, matrix);
+    const bool tile = tile_supported(P, matrix);
+    const bool ws = ws_supported(P, matrix);
+    const bool line = line_supported(P, matrix) && tile;
+    if (kernel == WQ_KERNEL_LINE && !line) return fail(WQ_EINVAL, "line kernel not available for this (d, p, matrix)");
+    if (kernel == WQ_KERNEL_LINE || (kernel == WQ_KERNEL_AUTO && line)) {
+        // interior lines of the plane range by the line kernel, the others by the tile kernel
+        const int64_t n2 = P->dir[1].n, lo = pl_lo * n2, hi = pl_hi * n2;
+        auto sub = [&](const std::vector<int32_t> &v, int64_t &first, int64_t &count) {
+            first = std::lower_bound(v.begin(), v.end(), (int32_t)lo) - v.begin();
+            count = (std::lower_bound(v.begin(), v.end(), (int32_t)hi) - v.begin()) - first;
+        };
+        int64_t fi, ni, fb, nb;
+        sub(P->lines_int, fi, ni);
+        sub(P->lines_bnd, fb, nb);
+        wq_status st = launch_assemble_line(P, matrix, P->lines_dev + fi, ni, val, col, val_base, s);
+        if (!st && nb > 0 && !getenv("WQ_LINE_ONLY"))
+            st = launch_assemble_tile_list(P, matrix, P->lines_dev + P->lines_int.size() + fb, nb, val, col, val_base, s);
+        return st;
+    }
     if (kernel == WQ_KERNEL_TILE && !tile) return fail(WQ_EINVAL, "tile kernel not available for this (d, p)");
-    if (kernel == WQ_KERNEL_DIRECT || !tile)
+    if (kernel == WQ_KERNEL_WS && !ws) return fail(WQ_EINVAL, "warp-specialised kernel not available for this (d, p)");
+    if (kernel == WQ_KERNEL_DIRECT || (kernel == WQ_KERNEL_AUTO && !tile))
         return launch_assemble_direct(P, matrix, val, col, pl_lo, pl_hi, val_base, s);
+    if (kernel == WQ_KERNEL_WS)
+        return launch_assemble_ws(P, matrix, val, col, pl_lo, pl_hi, val_base, s);
     return launch_assemble_tile(P, matrix, val, col, pl_lo, pl_hi, val_base, s);
 }
 
@@ -446,7 +495,12 @@ wq_status wq_export_coef(wq_plan P, double *h_out, int64_t *n_values, int32_t *n
     if (!h_out) return WQ_OK;
     cudaSetDevice(P->device);
     cudaError_t ce = cudaDeviceSynchronize();
-    if (!ce) ce = cudaMemcpy(h_out, P->coef, sizeof(double) * P->ncomp * P->coef_points, cudaMemcpyDeviceToHost);
+    // d = 3: un-pad the q_1 leading dimension (rows of nq_1 values at column offset c0off)
+    const int64_t nq1 = P->dir[0].nq, rows = P->coef_points / nq1;
+    if (P->d < 3) {
+        if (!ce) ce = cudaMemcpy(h_out, P->coef, sizeof(double) * P->ncomp * P->coef_points, cudaMemcpyDeviceToHost);
+    } else if (!ce) ce = cudaMemcpy2D(h_out, sizeof(double) * nq1, P->coef + P->c0off, sizeof(double) * P->cld1, sizeof(double) * nq1,
+                               (size_t)(rows * P->ncomp), cudaMemcpyDeviceToHost);
     return wq_cuda_status(ce, "export coef");
 }
 

@@ -15,6 +15,7 @@ struct DirectArgs {
     int d, p, matrix;
     const double *coef;
     int64_t npts, nq1, nq2;  // coefficient sub-grid strides
+    int64_t c0off;
     int64_t cq_b;
     int comp_mass, ncomp_s;
     double *val;
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(128) k_direct(DirectArgs a) {
                 for (int c2 = 0; c2 < nq[1]; ++c2) {
                     double s1 = 0.0;
                     int64_t base;
-                    if (D == 3) base = (ql[0]) + a.nq1 * ((ql[1] + c2) + a.nq2 * (ql[2] + c3 - a.cq_b));
+                    if (D == 3) base = a.c0off + (ql[0]) + a.nq1 * ((ql[1] + c2) + a.nq2 * (ql[2] + c3 - a.cq_b));
                     else if (D == 2) base = (ql[0]) + a.nq1 * (ql[1] + c2 - a.cq_b);
                     else base = ql[0] - a.cq_b;
                     for (int c1 = 0; c1 < nq[0]; ++c1) s1 = fma(A1[c1], __ldg(Cc + base + c1), s1);
@@ -117,8 +118,9 @@ wq_status launch_assemble_direct(wq_plan_s *P, int matrix, double *val, int32_t 
     a.p = P->p;
     a.matrix = matrix;
     a.coef = P->coef;
-    a.npts = P->coef_points;
-    a.nq1 = P->dir[0].nq;
+    a.npts = P->cstride;
+    a.c0off = P->c0off;
+    a.nq1 = P->cld1;
     a.nq2 = P->dir[1].nq;
     a.cq_b = P->cq_b;
     a.ncomp_s = P->ncomp_s;

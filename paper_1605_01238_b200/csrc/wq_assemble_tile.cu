@@ -107,6 +107,7 @@ struct TileArgs {
     int32_t *col;
     int64_t val_base;
     int64_t plane_lo;  // first slab plane (relative) of this launch
+    const int32_t *lines;  // optional list of lines (i2 + n2 * (i3 - slab_b)); plane_lo = 0 then
 };
 
 __device__ __forceinline__ int comp_ix(int l, int m) {  // upper-triangle index, d = 3
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(256, 1) k_tile(TileArgs a) {
 
     const int tid = threadIdx.x;
     const int chunk = (int)(blockIdx.x % CF::NCH);
-    const int line = (int)(blockIdx.x / CF::NCH);
+    const int line = a.lines ? a.lines[blockIdx.x / CF::NCH] : (int)(blockIdx.x / CF::NCH);
     const int n1 = (int)a.g.n[0], n2 = (int)a.g.n[1];
     const int i2 = line % n2, i3 = (int)(a.g.slab_b + a.plane_lo) + line / n2;
     const DirView &v1 = a.v[0], &v2 = a.v[1], &v3 = a.v[2];
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(256, 1) k_tile(TileArgs a) {
     const bool int2 = nq2 == 2 * P + 1 && i2 >= P + 1 && i2 <= n2 - P - 2;  // interior pattern in dir 2
     const bool int3 = nq3 == 2 * P + 1 && i3 >= P + 1 && i3 <= (int)a.g.n[2] - P - 2 && CF::NCH == 1;
     // coefficient field restricted to this line
-    const double *__restrict__ Cl = a.coef + (int64_t)ql2 * a.nq1 + (int64_t)(ql3 - a.cq_b) * plane_stride;
+    const double *__restrict__ Cl = a.coef + 1 + (int64_t)ql2 * a.nq1 + (int64_t)(ql3 - a.cq_b) * plane_stride;
 
     // CSR offset of row (0, i2, i3) relative to the first owned row; row i1 adds ni2*ni3*P1(i1)
     const int64_t line_off = a.g.offset(0, i2, i3) - a.val_base;
@@ -495,22 +496,23 @@ __global__ void __launch_bounds__(256, 1) k_tile(TileArgs a) {
 
 template <int P, bool STIFF>
 wq_status launch_tile_p(wq_plan_s *Pl, double *val, int32_t *col, int64_t pl_lo, int64_t pl_hi, int64_t val_base,
-                        cudaStream_t s) {
+                        cudaStream_t s, const int32_t *list = nullptr, int64_t n_list = 0) {
     using CF = Cfg<P, STIFF>;
     TileArgs a;
     a.g.init(Pl);
     for (int l = 0; l < 3; ++l) a.v[l] = Pl->dir[l];
     a.coef = Pl->coef;
-    a.nq1 = Pl->dir[0].nq;
+    a.nq1 = Pl->cld1;
     a.nq2 = Pl->dir[1].nq;
     a.cq_b = Pl->cq_b;
-    a.npts = Pl->coef_points;
+    a.npts = Pl->cstride;
     a.comp_mass = Pl->need_stiff ? Pl->ncomp_s : 0;
     a.val = val;
     a.col = col;
     a.val_base = val_base;
-    a.plane_lo = pl_lo;
-    const int64_t lines = Pl->dir[1].n * (pl_hi - pl_lo);
+    a.plane_lo = list ? 0 : pl_lo;
+    a.lines = list;
+    const int64_t lines = list ? n_list : Pl->dir[1].n * (pl_hi - pl_lo);
     const int64_t blocks = lines * CF::NCH;
     static bool set = false;
     if (!set) {
@@ -525,18 +527,19 @@ wq_status launch_tile_p(wq_plan_s *Pl, double *val, int32_t *col, int64_t pl_lo,
 }
 
 template <bool STIFF>
-wq_status dispatch_p(wq_plan_s *Pl, double *val, int32_t *col, int64_t lo, int64_t hi, int64_t vb, cudaStream_t s) {
+wq_status dispatch_p(wq_plan_s *Pl, double *val, int32_t *col, int64_t lo, int64_t hi, int64_t vb, cudaStream_t s,
+                     const int32_t *list = nullptr, int64_t n_list = 0) {
     switch (Pl->p) {
-    case 1: return launch_tile_p<1, STIFF>(Pl, val, col, lo, hi, vb, s);
-    case 2: return launch_tile_p<2, STIFF>(Pl, val, col, lo, hi, vb, s);
-    case 3: return launch_tile_p<3, STIFF>(Pl, val, col, lo, hi, vb, s);
-    case 4: return launch_tile_p<4, STIFF>(Pl, val, col, lo, hi, vb, s);
-    case 5: return launch_tile_p<5, STIFF>(Pl, val, col, lo, hi, vb, s);
-    case 6: return launch_tile_p<6, STIFF>(Pl, val, col, lo, hi, vb, s);
-    case 7: return launch_tile_p<7, STIFF>(Pl, val, col, lo, hi, vb, s);
-    case 8: return launch_tile_p<8, STIFF>(Pl, val, col, lo, hi, vb, s);
-    case 9: return launch_tile_p<9, STIFF>(Pl, val, col, lo, hi, vb, s);
-    case 10: return launch_tile_p<10, STIFF>(Pl, val, col, lo, hi, vb, s);
+    case 1: return launch_tile_p<1, STIFF>(Pl, val, col, lo, hi, vb, s, list, n_list);
+    case 2: return launch_tile_p<2, STIFF>(Pl, val, col, lo, hi, vb, s, list, n_list);
+    case 3: return launch_tile_p<3, STIFF>(Pl, val, col, lo, hi, vb, s, list, n_list);
+    case 4: return launch_tile_p<4, STIFF>(Pl, val, col, lo, hi, vb, s, list, n_list);
+    case 5: return launch_tile_p<5, STIFF>(Pl, val, col, lo, hi, vb, s, list, n_list);
+    case 6: return launch_tile_p<6, STIFF>(Pl, val, col, lo, hi, vb, s, list, n_list);
+    case 7: return launch_tile_p<7, STIFF>(Pl, val, col, lo, hi, vb, s, list, n_list);
+    case 8: return launch_tile_p<8, STIFF>(Pl, val, col, lo, hi, vb, s, list, n_list);
+    case 9: return launch_tile_p<9, STIFF>(Pl, val, col, lo, hi, vb, s, list, n_list);
+    case 10: return launch_tile_p<10, STIFF>(Pl, val, col, lo, hi, vb, s, list, n_list);
     }
     wq_set_error("tile kernel: unsupported degree");
     return WQ_EINVAL;
@@ -560,4 +563,15 @@ wq_status launch_assemble_tile(wq_plan_s *P, int matrix, double *val, int32_t *c
     }
     return matrix == WQ_MASS ? dispatch_p<false>(P, val, col, plane_lo, plane_hi, val_base, s)
                              : dispatch_p<true>(P, val, col, plane_lo, plane_hi, val_base, s);
+}
+
+wq_status launch_assemble_tile_list(wq_plan_s *P, int matrix, const int32_t *lines, int64_t n_lines, double *val,
+                                    int32_t *col, int64_t val_base, cudaStream_t s) {
+    if (!tile_supported(P, matrix)) {
+        wq_set_error("tile kernel not available for this plan");
+        return WQ_EINVAL;
+    }
+    if (n_lines <= 0) return WQ_OK;
+    return matrix == WQ_MASS ? dispatch_p<false>(P, val, col, 0, 0, val_base, s, lines, n_lines)
+                             : dispatch_p<true>(P, val, col, 0, 0, val_base, s, lines, n_lines);
 }

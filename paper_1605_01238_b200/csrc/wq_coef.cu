@@ -27,6 +27,7 @@ struct CoefArgs {
     double *coef;        // [ncomp][points]
     int64_t cq_b;        // first q_d of the sub-grid
     int64_t nq_loc_d;    // q_d extent of the sub-grid
+    int64_t cld1, cstride, c0off;  // coefficient layout (wq_internal.cuh)
     int ncomp_s, ncomp;
     int need_s, need_m;
     Flags *flags;
@@ -169,8 +170,9 @@ __global__ void __launch_bounds__(NTC) k_coef(CoefArgs a) {
     const double *n1t = Ntab(v1, p, q1off + q1), *m1t = Mtab(v1, p, q1off + q1);
     const int64_t e1 = v1.span[q1off + q1];
     const int c1s = (int)(e1 - k1a);
-    const int64_t npts_plane = nq1 * (D >= 2 ? nq2 : 1);
-    const int64_t npts = npts_plane * (D == 3 ? a.nq_loc_d : 1);
+    const int64_t ld1 = D == 3 ? a.cld1 : nq1;
+    const int64_t npts_plane = ld1 * (D >= 2 ? nq2 : 1);
+    const int64_t npts = a.cstride;
     {
         double J[3][3];
         #pragma unroll
@@ -219,7 +221,7 @@ __global__ void __launch_bounds__(NTC) k_coef(CoefArgs a) {
         else { if (!a.flags->det_neg) atomicOr(&a.flags->det_neg, 1); }
         const double ad = fabs(det);
         const double inv = 1.0 / ad;
-        const int64_t pt = q1 + nq1 * (D >= 2 ? (q2a + t2) : 0) + (D == 3 ? npts_plane * q3l : 0);
+        const int64_t pt = (D == 3 ? a.c0off : 0) + q1 + ld1 * (D >= 2 ? (q2a + t2) : 0) + (D == 3 ? npts_plane * q3l : 0);
         int comp = 0;
         if (a.need_s) {
             #pragma unroll
@@ -248,6 +250,9 @@ wq_status launch_coef(wq_plan_s *P, const double *ctrl, cudaStream_t s) {
     a.coef = P->coef;
     a.cq_b = P->cq_b;
     a.nq_loc_d = P->cq_e - P->cq_b;
+    a.cld1 = P->cld1;
+    a.c0off = P->c0off;
+    a.cstride = P->cstride;
     a.ncomp_s = P->ncomp_s;
     a.ncomp = P->ncomp;
     a.need_s = P->need_stiff;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
+#include <vector>
 #include "../../include/wq.h"
 
 #define WQ_PMAX WQ_MAX_DEGREE          // compile-time bound on p
@@ -47,8 +48,13 @@ struct wq_plan_s {
     DirView dir[3];
     // coefficient sub-grid: q_d in [cq_b, cq_e)
     int64_t cq_b, cq_e, coef_points;
+    int64_t c0off;                 // d = 3: point q_1 is stored at column q_1 + 1 (c0off = 1), so that
+                                   // the 2-point boxes [1 + 2k, 2 + 2k] of the row kernels start 16-B
+                                   // aligned for TMA; else 0
+    int64_t cld1;                  // leading dimension along q_1 (d = 3: nq_1 + 1 rounded up to even)
+    int64_t cstride;               // doubles per component = cld1 * (points / nq_1)
     int ncomp_s, ncomp;            // stiffness components, total components
-    double *coef;                  // [ncomp][coef_points]
+    double *coef;                  // [ncomp][cstride], point (q1, q2, q3) at q1 + c0off + cld1 * (q2 + nq2 * (q3 - cq_b))
     // Gauss-Legendre rule on [-1,1] in double-double: [p+1] (hi, lo) pairs
     double *gl;                    // [2*(p+1)] t, [2*(p+1)] w
     Flags *flags;                  // device
@@ -59,6 +65,11 @@ struct wq_plan_s {
     // form_host staging
     double *stage_val; int32_t *stage_col; int64_t *stage_rp; size_t stage_bytes;
     int64_t workspace_bytes;
+    // d = 3 row lines (i2 + n2 * (i3 - slab_b)) split by the line kernel's applicability:
+    // interior in directions 2 and 3 (#Q = 2p+1, no boundary span) first, then the rest.
+    // Both sorted; device copy in lines_dev (interior at 0, boundary at n_lines_int).
+    std::vector<int32_t> lines_int, lines_bnd;
+    int32_t *lines_dev;
 };
 
 // host helpers
@@ -83,4 +94,13 @@ wq_status launch_assemble_direct(wq_plan_s *P, int matrix, double *val, int32_t 
 wq_status launch_assemble_tile(wq_plan_s *P, int matrix, double *val, int32_t *col, int64_t plane_lo,
                                int64_t plane_hi, int64_t val_base, cudaStream_t s);
 bool tile_supported(const wq_plan_s *P, int matrix);
+wq_status launch_assemble_ws(wq_plan_s *P, int matrix, double *val, int32_t *col, int64_t plane_lo,
+                             int64_t plane_hi, int64_t val_base, cudaStream_t s);
+bool ws_supported(const wq_plan_s *P, int matrix);
+wq_status launch_assemble_line(wq_plan_s *P, int matrix, const int32_t *lines, int64_t n_lines, double *val,
+                               int32_t *col, int64_t val_base, cudaStream_t s);
+bool line_supported(const wq_plan_s *P, int matrix);
+// tile kernel over an explicit list of lines of the plan's slab
+wq_status launch_assemble_tile_list(wq_plan_s *P, int matrix, const int32_t *lines, int64_t n_lines, double *val,
+                                    int32_t *col, int64_t val_base, cudaStream_t s);
 

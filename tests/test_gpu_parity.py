@@ -11,7 +11,7 @@ from wqinputs import baseline_config, control_net, graded_open_knots, uniform_op
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [wq.WQ_KERNEL_DIRECT, wq.WQ_KERNEL_TILE]
+KERNELS = [wq.WQ_KERNEL_DIRECT, wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_WS, wq.WQ_KERNEL_LINE]
 
 
 def _torch():
@@ -29,9 +29,9 @@ def make_case(d, p, E, geometry="grid", amp=0.1, knots="uniform", seed=0):
 def run_full(ks, ctrl, p, matrix, kernel=wq.WQ_KERNEL_AUTO, slab=(0, -1), fused_col=True):
     torch = _torch()
     plan = wq.Plan(p, ks, slab=slab, need_mass=True, need_stiffness=True)
-    if kernel == wq.WQ_KERNEL_TILE and not _tile_ok(plan, matrix):
+    if kernel in (wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_WS, wq.WQ_KERNEL_LINE) and not _kernel_ok(plan, matrix, kernel):
         plan.close()
-        pytest.skip("tile kernel not available for this (d, p)")
+        pytest.skip(f"kernel {kernel} not available for this (d, p)")
     d_ctrl = torch.from_numpy(ctrl).cuda()
     rp, col, val = plan.alloc_csr()
     plan.setup(d_ctrl)
@@ -44,12 +44,12 @@ def run_full(ks, ctrl, p, matrix, kernel=wq.WQ_KERNEL_AUTO, slab=(0, -1), fused_
     return rp, col, val, info
 
 
-def _tile_ok(plan, matrix):
+def _kernel_ok(plan, matrix, kernel):
     torch = _torch()
     try:
         v = torch.empty(plan.info["nnz_local"], dtype=torch.float64, device="cuda")
         plan.setup(torch.zeros(plan.info["n_dof_total"] * plan.d, dtype=torch.float64, device="cuda") + 1)
-        wq.wq_assemble(plan.h, matrix, v, None, kernel=wq.WQ_KERNEL_TILE)
+        wq.wq_assemble(plan.h, matrix, v, None, kernel=kernel)
         torch.cuda.synchronize()
         return True
     except wq.WQError:
@@ -252,11 +252,43 @@ def test_form_host_equals_device():
         assert np.array_equal(hval.numpy(), val0.cpu().numpy())
 
 
-def test_kernels_agree():
-    """Direct and tile kernels agree to roundoff on a mid-size 3D case."""
-    ks, ctrl = make_case(3, 4, 9, "annulus", 0.05)
+@pytest.mark.parametrize("p,E", [(2, 11), (3, 10), (4, 9)])
+def test_kernels_agree(p, E):
+    """Direct, tile and warp-specialised kernels agree to roundoff on mid-size
+    3D cases; columns bit-exact."""
+    ks, ctrl = make_case(3, p, E, "annulus", 0.05)
     for mat in (MASS, STIFFNESS):
-        _, _, v1, _ = run_full(ks, ctrl, 4, mat, wq.WQ_KERNEL_DIRECT)
-        _, _, v2, _ = run_full(ks, ctrl, 4, mat, wq.WQ_KERNEL_TILE)
-        a, b = v1.cpu().numpy(), v2.cpu().numpy()
-        assert np.abs(a - b).max() <= 1e-12 * np.abs(a).max()
+        _, c1, v1, _ = run_full(ks, ctrl, p, mat, wq.WQ_KERNEL_DIRECT)
+        a = v1.cpu().numpy()
+        for k in (wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_WS, wq.WQ_KERNEL_LINE):
+            if k == wq.WQ_KERNEL_LINE and mat == MASS:
+                continue
+            _, c2, v2, _ = run_full(ks, ctrl, p, mat, k)
+            assert np.array_equal(c1.cpu().numpy(), c2.cpu().numpy())
+            b = v2.cpu().numpy()
+            assert np.abs(a - b).max() <= 1e-12 * np.abs(a).max()
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_ws_sub_slab_launch(p):
+    """Warp-specialised kernel on slab sub-ranges (plane_lo > 0, few items per
+    CTA, grid smaller than the SM count) equals the whole-slab launch."""
+    torch = _torch()
+    ks, ctrl = make_case(3, p, 7, "grid", 0.1)
+    rp0, col0, val0, info = run_full(ks, ctrl, p, STIFFNESS, wq.WQ_KERNEL_WS)
+    n_d = 7 + p
+    plan = wq.Plan(p, ks, slab=(2, n_d - 1), need_mass=False, need_stiffness=True)
+    d_ctrl = torch.from_numpy(ctrl).cuda()
+    rp, col, val = plan.alloc_csr()
+    plan.setup(d_ctrl)
+    base = int(rp0[plan.info["row_begin"]])
+    wq.wq_pattern(plan.h, base, rp, None)
+    wq.wq_assemble(plan.h, STIFFNESS, val, col, kernel=wq.WQ_KERNEL_WS)
+    torch.cuda.synchronize()
+    r0 = plan.info["row_begin"]
+    n = plan.info["n_rows_local"]
+    plan.close()
+    lo, hi = int(rp0[r0]), int(rp0[r0 + n])
+    assert np.array_equal(rp.cpu().numpy(), rp0[r0:r0 + n + 1].cpu().numpy())
+    assert np.array_equal(col.cpu().numpy(), col0[lo:hi].cpu().numpy())
+    assert np.array_equal(val.cpu().numpy(), val0[lo:hi].cpu().numpy())
