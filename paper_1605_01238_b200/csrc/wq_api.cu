@@ -302,7 +302,7 @@ static wq_status assemble_range(wq_plan_s *P, int matrix, wq_kernel kernel, doub
     if (matrix == WQ_STIFFNESS && !P->need_stiff) return fail(WQ_EINVAL, "plan was created without need_stiffness");
     const bool tile = tile_supported(P, matrix);
     const bool ws = ws_supported(P, matrix);
-    const bool line = line_supported(P, matrix) && tile;
+    const bool line = line_supported(P, matrix, false) && (line_supported(P, matrix, true) || tile);
     if (kernel == WQ_KERNEL_LINE && !line) return fail(WQ_EINVAL, "line kernel not available for this (d, p, matrix)");
     if (kernel == WQ_KERNEL_LINE || (kernel == WQ_KERNEL_AUTO && line)) {
         // interior lines of the plane range by the line kernel, the others by the tile kernel
@@ -314,9 +314,11 @@ static wq_status assemble_range(wq_plan_s *P, int matrix, wq_kernel kernel, doub
         int64_t fi, ni, fb, nb;
         sub(P->lines_int, fi, ni);
         sub(P->lines_bnd, fb, nb);
-        wq_status st = launch_assemble_line(P, matrix, P->lines_dev + fi, ni, val, col, val_base, s);
+        wq_status st = launch_assemble_line(P, matrix, false, P->lines_dev + fi, ni, val, col, val_base, s);
+        const int32_t *lb = P->lines_dev + P->lines_int.size() + fb;
         if (!st && nb > 0 && !getenv("WQ_LINE_ONLY"))
-            st = launch_assemble_tile_list(P, matrix, P->lines_dev + P->lines_int.size() + fb, nb, val, col, val_base, s);
+            st = line_supported(P, matrix, true) ? launch_assemble_line(P, matrix, true, lb, nb, val, col, val_base, s)
+                                                 : launch_assemble_tile_list(P, matrix, lb, nb, val, col, val_base, s);
         return st;
     }
     if (kernel == WQ_KERNEL_TILE && !tile) return fail(WQ_EINVAL, "tile kernel not available for this (d, p)");

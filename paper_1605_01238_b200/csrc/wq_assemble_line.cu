@@ -39,7 +39,16 @@ namespace {
 struct LnPar {
     int nr, nteam, nwp, nts, nb;  // nb: coefficient box buffers per producer warp
 };
-__host__ __device__ constexpr LnPar ln_par(int p) {
+// BND: lines touching a boundary span in direction 2 or 3 (#Q up to 3p+1, runtime staircase)
+__host__ __device__ constexpr LnPar ln_par(int p, bool bnd) {
+    if (bnd) {
+        switch (p) {
+        case 2: return {4, 8, 6, 20, 1};
+        case 3: return {4, 4, 6, 16, 1};
+        case 4: return {3, 2, 4, 12, 1};
+        default: return {0, 0, 0, 0, 0};
+        }
+    }
     switch (p) {
     case 2: return {4, 8, 8, 24, 2};
     case 3: return {4, 4, 8, 18, 2};
@@ -48,9 +57,9 @@ __host__ __device__ constexpr LnPar ln_par(int p) {
     }
 }
 
-template <int P>
+template <int P, bool BND>
 struct LnCfg {
-    static constexpr LnPar W = ln_par(P);
+    static constexpr LnPar W = ln_par(P, BND);
     static constexpr bool ENABLED = W.nr > 0;
     static constexpr int K = 2 * P + 1;   // #I of an interior row = #Q of an interior row
     static constexpr int QI = 2 * P + 1;
@@ -69,16 +78,20 @@ struct LnCfg {
     static constexpr int NTS = ENABLED ? W.nts : 2;  // task slots (2 points each) in the G ring
     static constexpr int NB = ENABLED ? W.nb : 1;
     static constexpr int RING = 2 * NTS;
-    static constexpr int NF = 3 * QI;                // stage-3 / stage-2 fibres per warp
-    // doubles per coefficient box buffer (= Y per task), padded so that every buffer starts 128-B aligned (TMA)
-    static constexpr int BOXD = (6 * QI * QI * 2 + 15) / 16 * 16;
-    static constexpr int TABD = 4 * QI * NP + 4 * QI + 4 * QI;  // per-warp line tables (doubles)
+    static constexpr int QX = BND ? QB : QI;         // box / table extent in directions 2, 3
+    static constexpr int NF = 3 * QX;                // stage-3 fibres (m, c2) per task
+    static constexpr int NPASS = (NF + 31) / 32;     // stage-3 passes over the fibres
+    // doubles per coefficient box buffer, padded so that every buffer starts 128-B aligned (TMA); the
+    // interior kernel writes Y over the consumed box, BND (several stage-3 passes) into its own buffer
+    static constexpr int BOXD = (6 * QX * QX * 2 + 15) / 16 * 16;
+    static constexpr int YD = BND ? (3 * 2 * QX * K * 2 + 15) / 16 * 16 : 0;
+    static constexpr int TABD = 4 * QX * NP + 4 * QX + 4 * QX + QX;  // per-warp line tables (doubles; + offsets)
     static constexpr int SSTV = 32 * K + 2;
     static constexpr int SSTC = 32 * K + 4;
     __host__ __device__ static constexpr size_t al(size_t x) { return (x + 127) & ~(size_t)127; }
     static constexpr size_t O_BAR = 0;
     static constexpr size_t O_BOX = al(8 * (2 * NWP + 2 * NTS + 2 * NWC));
-    static constexpr size_t O_TAB = al(O_BOX + (size_t)NWP * NB * BOXD * 8);
+    static constexpr size_t O_TAB = al(O_BOX + (size_t)NWP * (NB * BOXD + YD) * 8);
     static constexpr size_t O_G = al(O_TAB + (size_t)NWP * TABD * 8);
     static constexpr size_t O_B1 = al(O_G + (size_t)4 * RING * COLS * 8);
     static constexpr size_t O_W1 = al(O_B1 + (size_t)RING * NP * 16);
@@ -91,7 +104,7 @@ struct LnCfg {
     __host__ __device__ static constexpr size_t d1_bytes(int64_t n1, int64_t nq1) {
         return al(16 * (size_t)n1 + 8 * (size_t)(n1 + 1) + 4 * (size_t)nq1);
     }
-    static constexpr bool FITS = ENABLED && NF <= 32 && NWC % 2 == 0 && NWP <= 2 * RW && SMEM + d1_bytes(128, 2 * 128 + 2 * P + 1) <= 227 * 1024 &&
+    static constexpr bool FITS = ENABLED && (BND || NF <= 32) && 3 * K <= 32 && NWC % 2 == 0 && NWP <= 2 * RW && SMEM + d1_bytes(128, 2 * 128 + 2 * P + 1) <= 227 * 1024 &&
                                  NT <= 1024;
 };
 
@@ -109,7 +122,7 @@ struct LnArgs {
 };
 
 struct LItem {
-    int i2, i3, ql2, ql3, jl2, jl3;
+    int i2, i3, ql2, ql3, jl2, jl3, nq2, nq3, ni2, ni3;
 };
 
 __device__ __forceinline__ LItem ln_item(const LnArgs &a, int64_t it) {
@@ -122,6 +135,10 @@ __device__ __forceinline__ LItem ln_item(const LnArgs &a, int64_t it) {
     I.jl2 = a.v[1].jlo[I.i2];
     I.ql3 = a.v[2].qlo[I.i3];
     I.jl3 = a.v[2].jlo[I.i3];
+    I.nq2 = a.v[1].qlen[I.i2];
+    I.nq3 = a.v[2].qlen[I.i3];
+    I.ni2 = a.v[1].jlen[I.i2];
+    I.ni3 = a.v[2].jlen[I.i3];
     return I;
 }
 
@@ -135,10 +152,11 @@ __device__ __forceinline__ void twait(uint64_t *b, unsigned par, unsigned long l
     }
 }
 
-template <int P>
-__global__ void __launch_bounds__(LnCfg<P>::NT, 1)
+template <int P, bool BND>
+__global__ void __launch_bounds__(LnCfg<P, BND>::NT, 1)
     k_line(const __grid_constant__ CUtensorMap tm, LnArgs a) {
-    using CF = LnCfg<P>;
+    using CF = LnCfg<P, BND>;
+    constexpr int QX = CF::QX;
     constexpr int K = CF::K, QI = CF::QI, QB = CF::QB, NP = CF::NP, COLS = CF::COLS, TW = CF::TW;
     constexpr int NR = CF::NR, NTEAM = CF::NTEAM, NWP = CF::NWP, NTS = CF::NTS, RING = CF::RING;
     constexpr int NF = CF::NF, BOXD = CF::BOXD;
@@ -198,11 +216,14 @@ __global__ void __launch_bounds__(LnCfg<P>::NT, 1)
         // ============================================================ producer warp
         const int wp = wrow * 2 + smsp;
         if (wp >= NWP) return;
-        double *box[2] = {Boxes + (wp * CF::NB + 0) * BOXD, Boxes + (wp * CF::NB + (CF::NB - 1)) * BOXD};
+        double *wbase = Boxes + wp * (CF::NB * BOXD + CF::YD);
+        double *box[2] = {wbase, wbase + (CF::NB - 1) * BOXD};
+        double *Ybuf = wbase + CF::NB * BOXD;  // BND only
         double *tab = Tabs + wp * CF::TABD;
-        double *B2v = tab, *B2d = B2v + QI * NP, *B3v = B2d + QI * NP, *B3d = B3v + QI * NP;
-        double *W2t = B3d + QI * NP, *W3t = W2t + 4 * QI;  // [c][f], f = a + 2b
-        constexpr unsigned BOX_BYTES = 6 * QI * QI * 2 * 8;
+        double *B2v = tab, *B2d = B2v + QX * NP, *B3v = B2d + QX * NP, *B3d = B3v + QX * NP;
+        double *W2t = B3d + QX * NP, *W3t = W2t + 4 * QX;  // [c][f], f = a + 2b
+        int *off2 = (int *)(W3t + 4 * QX), *off3 = off2 + QX;  // BND: staircase offsets span - jlo
+        constexpr unsigned BOX_BYTES = 6 * QX * QX * 2 * 8;
         int64_t ik = -1;
         int iq2 = 0, iq3 = 0;
         auto issue = [&](int64_t T, int b) {  // lane 0: TMA of task T into buffer b
@@ -221,9 +242,10 @@ __global__ void __launch_bounds__(LnCfg<P>::NT, 1)
             if (CF::NB == 2) issue(wp + NWP, 1);
         }
         int64_t cur_item = -1;
-        // lane roles: stage 3 fibre (m, c2), stage 2 fibre (m, t3); lanes >= NF idle in the contractions
-        const int fm = lane / QI, fc = lane % QI;
-        const bool fl = lane < NF;
+        // lane roles: stage 3 fibre (m, c2) (pass-strided for BND), stage 2 fibre (m, t3)
+        const int fm = lane / K, fc = lane % K;  // stage 2 (and interior stage 3, QI == K)
+        const bool fl = lane < 3 * K;
+        int cq2 = QI, cq3 = QI;  // #Q of the current item in directions 2, 3
         int use = 0;
         for (int64_t T = wp; T < n_tasks; T += NWP, ++use) {
             const int b = CF::NB == 2 ? (use & 1) : 0;
@@ -235,16 +257,22 @@ __global__ void __launch_bounds__(LnCfg<P>::NT, 1)
                 const LItem I = ln_item(a, first + k * step);
                 const DirView &v2 = a.v[1], &v3 = a.v[2];
                 __syncwarp();
-                for (int x = lane; x < QI * NP; x += 32) {
+                if (BND) { cq2 = I.nq2; cq3 = I.nq3; }
+                for (int x = lane; x < QX * NP; x += 32) {
                     const int c = x / NP, r = x % NP;
-                    const double2 b2 = __ldg((const double2 *)(v2.B + (int64_t)(I.ql2 + c) * BS) + r);
-                    const double2 b3 = __ldg((const double2 *)(v3.B + (int64_t)(I.ql3 + c) * BS) + r);
+                    const double2 b2 = c < cq2 ? __ldg((const double2 *)(v2.B + (int64_t)(I.ql2 + c) * BS) + r) : make_double2(0.0, 0.0);
+                    const double2 b3 = c < cq3 ? __ldg((const double2 *)(v3.B + (int64_t)(I.ql3 + c) * BS) + r) : make_double2(0.0, 0.0);
                     B2v[x] = b2.x; B2d[x] = b2.y; B3v[x] = b3.x; B3d[x] = b3.y;
                 }
-                for (int x = lane; x < 4 * QI; x += 32) {
-                    W2t[x] = __ldg(v2.W + (int64_t)I.i2 * v2.maxq * 4 + x);
-                    W3t[x] = __ldg(v3.W + (int64_t)I.i3 * v3.maxq * 4 + x);
+                for (int x = lane; x < 4 * QX; x += 32) {
+                    W2t[x] = x / 4 < cq2 ? __ldg(v2.W + (int64_t)I.i2 * v2.maxq * 4 + x) : 0.0;
+                    W3t[x] = x / 4 < cq3 ? __ldg(v3.W + (int64_t)I.i3 * v3.maxq * 4 + x) : 0.0;
                 }
+                if (BND)
+                    for (int x = lane; x < QX; x += 32) {
+                        off2[x] = x < cq2 ? v2.span[I.ql2 + x] - I.jl2 : 0;
+                        off3[x] = x < cq3 ? v3.span[I.ql3 + x] - I.jl3 : 0;
+                    }
                 __syncwarp();
             }
             // direction-1 basis pairs of the task's points (consumed at the end of the task)
@@ -254,49 +282,63 @@ __global__ void __launch_bounds__(LnCfg<P>::NT, 1)
             if (lane < 2 * NP && b1q < q_end) b1v = __ldg((const double2 *)(v1.B + (int64_t)b1q * BS) + b1r);
             if (!(a.dbg & 1)) twait(&pfull[wp * 2 + b], (CF::NB == 2 ? use >> 1 : use) & 1, pA);
             const double *bx = box[b];  // [comp][c3][c2][pt]
-            // ---------------- stage 3: lane (m, c2), both points, chains a1 = 0 (y0), 1 (y1)
-            double y0[2][K], y1[2][K];
+            // ---------------- stage 3: fibre (m, c2), both points, chains a1 = 0 (y0), 1 (y1)
+            // Y layout: [m][a1][c2][t3][pt]; interior: over the consumed box, BND: own buffer
+            double *Y = BND ? Ybuf : box[b];
             #pragma unroll
-            for (int pt = 0; pt < 2; ++pt)
+            for (int pass = 0; pass < CF::NPASS; ++pass) {
+                const int f = lane + 32 * pass;
+                const int m = f / QX, c2 = f % QX;
+                const bool fv = f < CF::NF && (!BND || c2 < cq2);
+                double y0[2][K], y1[2][K];
                 #pragma unroll
-                for (int t = 0; t < K; ++t) { y0[pt][t] = 0.0; y1[pt][t] = 0.0; }
-            if (fl && !(a.dbg & 4)) {
-                const int m = fm, c2 = fc;
-                const int ka = m, kb = m == 0 ? 1 : (m == 1 ? 3 : 4), kc = m == 0 ? 2 : (m == 1 ? 4 : 5);
-                const double w2a = W2t[c2 * 4 + (m == 1 ? 2 : 0)];  // w2^(0,b2)
-                const double w2b = W2t[c2 * 4 + (m == 1 ? 3 : 1)];  // w2^(1,b2)
-                const double *B3c = m == 2 ? B3d : B3v;
-                const int b3o = m == 2 ? 2 : 0;
-                unroll<QI>([&](auto C3) {
-                    constexpr int c3 = decltype(C3)::value;
-                    constexpr int o0 = (c3 + 1) / 2;
-                    const double w3a = W3t[c3 * 4 + b3o], w3b = W3t[c3 * 4 + b3o + 1];  // w3^(0,b3), w3^(1,b3)
-                    const double s1 = w2a * w3a, s2 = w2b * w3a, s3 = w2a * w3b;
-                    const double2 ca = *(const double2 *)(bx + ((ka * QI + c3) * QI + c2) * 2);
-                    const double2 cb = *(const double2 *)(bx + ((kb * QI + c3) * QI + c2) * 2);
-                    const double2 cc = *(const double2 *)(bx + ((kc * QI + c3) * QI + c2) * 2);
-                    const double h1a = s1 * ca.x, h1b = s1 * ca.y;                       // l = 0
-                    const double h0a = fma(s2, cb.x, s3 * cc.x), h0b = fma(s2, cb.y, s3 * cc.y);  // l = 1, 2
+                for (int pt = 0; pt < 2; ++pt)
                     #pragma unroll
-                    for (int r = 0; r <= P; ++r) {
-                        const double bv = B3c[c3 * NP + r];
-                        y1[0][o0 + r] = fma(bv, h1a, y1[0][o0 + r]);
-                        y1[1][o0 + r] = fma(bv, h1b, y1[1][o0 + r]);
-                        y0[0][o0 + r] = fma(bv, h0a, y0[0][o0 + r]);
-                        y0[1][o0 + r] = fma(bv, h0b, y0[1][o0 + r]);
+                    for (int t = 0; t < K; ++t) { y0[pt][t] = 0.0; y1[pt][t] = 0.0; }
+                if (fv && !(a.dbg & 4)) {
+                    const int ka = m, kb = m == 0 ? 1 : (m == 1 ? 3 : 4), kc = m == 0 ? 2 : (m == 1 ? 4 : 5);
+                    const double w2a = W2t[c2 * 4 + (m == 1 ? 2 : 0)];  // w2^(0,b2)
+                    const double w2b = W2t[c2 * 4 + (m == 1 ? 3 : 1)];  // w2^(1,b2)
+                    const double *B3c = m == 2 ? B3d : B3v;
+                    const int b3o = m == 2 ? 2 : 0;
+                    auto plane = [&](int c3, auto O) {
+                        constexpr int o0 = decltype(O)::value;
+                        const double w3a = W3t[c3 * 4 + b3o], w3b = W3t[c3 * 4 + b3o + 1];  // w3^(0,b3), w3^(1,b3)
+                        const double s1 = w2a * w3a, s2 = w2b * w3a, s3 = w2a * w3b;
+                        const double2 ca = *(const double2 *)(bx + ((ka * QX + c3) * QX + c2) * 2);
+                        const double2 cb = *(const double2 *)(bx + ((kb * QX + c3) * QX + c2) * 2);
+                        const double2 cc = *(const double2 *)(bx + ((kc * QX + c3) * QX + c2) * 2);
+                        const double h1a = s1 * ca.x, h1b = s1 * ca.y;                                // l = 0
+                        const double h0a = fma(s2, cb.x, s3 * cc.x), h0b = fma(s2, cb.y, s3 * cc.y);  // l = 1, 2
+                        #pragma unroll
+                        for (int r = 0; r <= P; ++r) {
+                            const double bv = B3c[c3 * NP + r];
+                            y1[0][o0 + r] = fma(bv, h1a, y1[0][o0 + r]);
+                            y1[1][o0 + r] = fma(bv, h1b, y1[1][o0 + r]);
+                            y0[0][o0 + r] = fma(bv, h0a, y0[0][o0 + r]);
+                            y0[1][o0 + r] = fma(bv, h0b, y0[1][o0 + r]);
+                        }
+                    };
+                    if constexpr (BND) {
+                        #pragma unroll 1
+                        for (int c3 = 0; c3 < cq3; ++c3)
+                            dispatch<0, K - NP>(off3[c3], [&](auto O) { plane(c3, O); });
+                    } else {
+                        unroll<QI>([&](auto C3) {
+                            constexpr int c3 = decltype(C3)::value;
+                            plane(c3, std::integral_constant<int, (c3 + 1) / 2>{});
+                        });
                     }
-                });
-            }
-            __syncwarp();  // every lane has read the box: Y may overwrite it
-            // Y over the box: [m][a1][c2][t3][pt]
-            double *Y = box[b];
-            if (fl) {
-                double *Y0 = Y + ((fm * 2 + 0) * QI + fc) * K * 2;
-                double *Y1 = Y + ((fm * 2 + 1) * QI + fc) * K * 2;
-                #pragma unroll
-                for (int t = 0; t < K; ++t) {
-                    *(double2 *)(Y0 + t * 2) = make_double2(y0[0][t], y0[1][t]);
-                    *(double2 *)(Y1 + t * 2) = make_double2(y1[0][t], y1[1][t]);
+                }
+                if (!BND) __syncwarp();  // every lane has read the box: Y may overwrite it
+                if (fv) {
+                    double *Y0 = Y + ((m * 2 + 0) * QX + c2) * K * 2;
+                    double *Y1 = Y + ((m * 2 + 1) * QX + c2) * K * 2;
+                    #pragma unroll
+                    for (int t = 0; t < K; ++t) {
+                        *(double2 *)(Y0 + t * 2) = make_double2(y0[0][t], y0[1][t]);
+                        *(double2 *)(Y1 + t * 2) = make_double2(y1[0][t], y1[1][t]);
+                    }
                 }
             }
             __syncwarp();
@@ -311,11 +353,10 @@ __global__ void __launch_bounds__(LnCfg<P>::NT, 1)
             if (fl && !(a.dbg & 8)) {
                 const int m = fm, t3 = fc;
                 const double *B2c = m == 1 ? B2d : B2v;
-                const double *Ya0 = Y + ((m * 2 + 0) * QI) * K * 2 + t3 * 2;
-                const double *Ya1 = Y + ((m * 2 + 1) * QI) * K * 2 + t3 * 2;
-                unroll<QI>([&](auto C2) {
-                    constexpr int c2 = decltype(C2)::value;
-                    constexpr int o0 = (c2 + 1) / 2;
+                const double *Ya0 = Y + ((m * 2 + 0) * QX) * K * 2 + t3 * 2;
+                const double *Ya1 = Y + ((m * 2 + 1) * QX) * K * 2 + t3 * 2;
+                auto point2 = [&](int c2, auto O) {
+                    constexpr int o0 = decltype(O)::value;
                     const double2 ya0 = *(const double2 *)(Ya0 + c2 * K * 2);
                     const double2 ya1 = *(const double2 *)(Ya1 + c2 * K * 2);
                     #pragma unroll
@@ -326,7 +367,16 @@ __global__ void __launch_bounds__(LnCfg<P>::NT, 1)
                         g[1][0][o0 + r] = fma(bv, ya1.x, g[1][0][o0 + r]);
                         g[1][1][o0 + r] = fma(bv, ya1.y, g[1][1][o0 + r]);
                     }
-                });
+                };
+                if constexpr (BND) {
+                    #pragma unroll 1
+                    for (int c2 = 0; c2 < cq2; ++c2) dispatch<0, K - NP>(off2[c2], [&](auto O) { point2(c2, O); });
+                } else {
+                    unroll<QI>([&](auto C2) {
+                        constexpr int c2 = decltype(C2)::value;
+                        point2(c2, std::integral_constant<int, (c2 + 1) / 2>{});
+                    });
+                }
             }
             // b1 = 0 collects m = 1 and m = 2: lane (1, t3) += lane (2, t3)
             #pragma unroll
@@ -335,7 +385,7 @@ __global__ void __launch_bounds__(LnCfg<P>::NT, 1)
                 for (int pt = 0; pt < 2; ++pt)
                     #pragma unroll
                     for (int t = 0; t < K; ++t) {
-                        const double o = __shfl_down_sync(0xffffffffu, g[a1][pt][t], QI);
+                        const double o = __shfl_down_sync(0xffffffffu, g[a1][pt][t], K);
                         if (fm == 1) g[a1][pt][t] += o;
                     }
             const uint32_t Tl = (uint32_t)T;  // slot accounting in task units
@@ -368,7 +418,7 @@ __global__ void __launch_bounds__(LnCfg<P>::NT, 1)
     const int team = cw / TW, wt = cw % TW;
     const int colx = wt * 32 + lane;
     const int t2c = colx % K, t3c = colx / K;
-    const bool live = colx < COLS;
+    bool live = colx < COLS;
     double *W1b = (double *)W1all + cw * 2 * CF::W1D;  // [2][NR][maxq][4]
     double *Sv = Svall + cw * CF::SSTV;
     int32_t *Sc = Scall + cw * CF::SSTC;
@@ -388,12 +438,23 @@ __global__ void __launch_bounds__(LnCfg<P>::NT, 1)
     int wbuf = 0;
     unsigned wuse[2] = {0, 0};
     if (lane == 0 && my_first < n1 && first < a.n_items) w1_issue(my_first, 0);
-    const unsigned lm = __ballot_sync(0xffffffffu, live);
-    const int e_lo = __shfl_sync(0xffffffffu, colx, __ffs(lm) - 1);        // interior: entry (t2 + K t3) in units of ni1
-    const int e_hi = __shfl_sync(0xffffffffu, colx, 31 - __clz(lm)) + 1;
+    // entry of column (t2, t3) in a row, in units of ni1: t2 + ni2 * t3 (interior: colx)
+    int el = colx, e_lo = 0, e_hi = 0, nc23 = K * K;
+    auto seg = [&]() {
+        const unsigned lm = __ballot_sync(0xffffffffu, live);
+        e_lo = lm ? __shfl_sync(0xffffffffu, el, __ffs(lm) - 1) : 0;
+        e_hi = lm ? __shfl_sync(0xffffffffu, el, 31 - __clz(lm)) + 1 : 0;
+    };
+    if (!BND) seg();
     uint32_t got = 0, rel = 0, Tbase = 0;  // tasks waited for / released, first task of the item
     for (int64_t it = first; it < a.n_items; it += step) {
         const LItem I = ln_item(a, it);
+        if (BND) {
+            live = colx < COLS && t2c < I.ni2 && t3c < I.ni3;
+            el = t2c + I.ni2 * t3c;
+            nc23 = I.ni2 * I.ni3;
+            seg();
+        }
         const int64_t line_off = a.g.offset(0, I.i2, I.i3) - a.val_base;
         const int colbase = n1 * ((I.jl2 + t2c) + (int)a.g.n[1] * (I.jl3 + t3c));
         for (int r0 = team * NR; r0 < n1; r0 += NTEAM * NR) {
@@ -402,7 +463,7 @@ __global__ void __launch_bounds__(LnCfg<P>::NT, 1)
             const uint32_t t_hi = Tbase + (uint32_t)((qlo1[rl] + qlen1[rl] - 1 - q0) / 2);
             const uint32_t t_lo = Tbase + (uint32_t)((qlo1[r0] - q0) / 2);
             // this batch's weights: wait for the prefetch, then prefetch the next batch of the team
-            mbar_wait(&wfull[cw * 2 + wbuf], wuse[wbuf] & 1);
+            twait(&wfull[cw * 2 + wbuf], wuse[wbuf] & 1, pC);
             ++wuse[wbuf];
             const double2 *W1w = (const double2 *)(W1b + wbuf * CF::W1D);  // [row][c][2] double2, row stride mq1
             if (lane == 0) {
@@ -507,47 +568,53 @@ __global__ void __launch_bounds__(LnCfg<P>::NT, 1)
                     ++rel;
                 }
             }
-            #pragma unroll
-            for (int k = 0; k < NR; ++k) {
-                if (k >= nr || (a.dbg & 256)) break;
-                const int i1 = r0 + k;
-                const int ni1 = jlen1[i1];
-                const int64_t goff = line_off + (int64_t)(K * K) * pref1[i1];
-                const int64_t dst0 = goff + (int64_t)ni1 * e_lo;
-                const int len = ni1 * (e_hi - e_lo);
-                const int hv = (int)(dst0 & 1), hc = (int)(dst0 & 3);
-                double *sv = Sv + hv;
-                int32_t *sc = Sc + hc;
-                if (lane == 0) bulk_wait_read<0>();  // the previous row's copy has read the staging buffer
-                __syncwarp();
-                if (live && !(a.dbg & 128)) {
-                    const int e0 = ni1 * (colx - e_lo);
-                    const int cb = jlo1[i1] + colbase;
-                    #pragma unroll
-                    for (int t = 0; t < K; ++t)
-                        if (t < ni1) {
-                            sv[e0 + t] = acc[k][t];
-                            sc[e0 + t] = cb + t;
+            // write the batch's rows: stage the warp's slice of each row in CSR order, TMA bulk copy
+            // of its 16-B aligned middle, <= 1 + 1 values and <= 3 + 3 columns at the ends by single lanes
+            if (e_hi > e_lo) {
+                const int nseg = e_hi - e_lo, erel = el - e_lo;
+                #pragma unroll
+                for (int k = 0; k < NR; ++k) {
+                    if (k >= nr) break;
+                    const int i1 = r0 + k;
+                    const int ni1 = jlen1[i1];
+                    const int64_t dst0 = line_off + (int64_t)nc23 * pref1[i1] + ni1 * e_lo;
+                    const int len = ni1 * nseg;
+                    const int hv = (int)dst0 & 1, hc = (int)dst0 & 3;
+                    if (lane == 0) bulk_wait_read<0>();  // the previous row's copy has read the staging buffer
+                    __syncwarp();
+                    if (live) {
+                        double *svl = Sv + hv + ni1 * erel;
+                        int32_t *scl = Sc + hc + ni1 * erel;
+                        const int cb = jlo1[i1] + colbase;
+                        if (ni1 == K) {
+                            #pragma unroll
+                            for (int t = 0; t < K; ++t) { svl[t] = acc[k][t]; scl[t] = cb + t; }
+                        } else {
+                            #pragma unroll
+                            for (int t = 0; t < K; ++t)
+                                if (t < ni1) { svl[t] = acc[k][t]; scl[t] = cb + t; }
                         }
-                }
-                if (!(a.dbg & 64)) fence_async_smem();
-                __syncwarp();
-                // 16-B aligned middle by TMA bulk copies (lane 0); the <= 1 + 1 unaligned values and
-                // <= 3 + 3 unaligned columns at the ends by single lanes in parallel
-                double *dv = a.val + dst0;
-                const int nbv = len > hv ? (len - hv) & ~1 : 0, tv = hv + nbv;
-                const int h4 = (4 - hc) & 3, hcn = h4 < len ? h4 : len;
-                const int nbc = len > hcn ? (len - hcn) & ~3 : 0, tc = hcn + nbc;
-                if (lane == 0) {
-                    if (nbv > 0 && !(a.dbg & 2)) bulk_s2g(dv + hv, sv + hv, (unsigned)nbv * 8u);
-                    if (a.col && nbc > 0 && !(a.dbg & 2)) bulk_s2g(a.col + dst0 + hcn, sc + hcn, (unsigned)nbc * 4u);
-                    bulk_commit();
-                }
-                if (lane == 1 && hv && len > 0) dv[0] = sv[0];
-                if (lane == 2 && tv < len) dv[tv] = sv[tv];
-                if (a.col) {
-                    if (lane >= 4 && lane < 4 + hcn) a.col[dst0 + (lane - 4)] = sc[lane - 4];
-                    if (lane >= 8 && tc + (lane - 8) < len) a.col[dst0 + tc + (lane - 8)] = sc[tc + (lane - 8)];
+                    }
+                    fence_async_smem();
+                    __syncwarp();
+                    const int nbv = (len - hv) & ~1, tv = hv + nbv;
+                    const int h4 = min((4 - hc) & 3, len);
+                    const int nbc = (len - h4) & ~3, tc = h4 + nbc;
+                    double *dv = a.val + dst0;
+                    int32_t *dc = a.col + dst0;
+                    if (lane == 0) {
+                        if (nbv > 0) bulk_s2g(dv + hv, Sv + 2 * hv, (unsigned)nbv * 8u);
+                        if (a.col && nbc > 0) bulk_s2g(dc + h4, Sc + hc + h4, (unsigned)nbc * 4u);
+                        bulk_commit();
+                    } else if (lane == 1) {
+                        if (hv) dv[0] = Sv[1];
+                    } else if (lane == 2) {
+                        if (tv < len) dv[tv] = Sv[hv + tv];
+                    } else if (a.col && lane < 7) {
+                        if (lane - 4 >= 0 && lane - 4 < h4) dc[lane - 4] = Sc[hc + lane - 4];
+                    } else if (a.col && lane >= 8 && lane < 12) {
+                        if (tc + lane - 8 < len) dc[tc + lane - 8] = Sc[hc + tc + lane - 8];
+                    }
                 }
             }
         }
@@ -588,10 +655,10 @@ int num_sms(int dev) {
     return n > 0 ? n : 148;
 }
 
-template <int P>
+template <int P, bool BND>
 wq_status launch_line_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, double *val, int32_t *col,
                         int64_t val_base, cudaStream_t s) {
-    using CF = LnCfg<P>;
+    using CF = LnCfg<P, BND>;
     if constexpr (!CF::FITS) {
         wq_set_error("line kernel not configured for this degree");
         return WQ_EINVAL;
@@ -622,7 +689,7 @@ wq_status launch_line_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, do
                               (cuuint64_t)(Pl->cq_e - Pl->cq_b), (cuuint64_t)Pl->ncomp};
         cuuint64_t strides[3] = {(cuuint64_t)Pl->cld1 * 8, (cuuint64_t)Pl->cld1 * Pl->dir[1].nq * 8,
                                  (cuuint64_t)Pl->cstride * 8};
-        cuuint32_t box[4] = {2, (cuuint32_t)CF::QI, (cuuint32_t)CF::QI, 6};
+        cuuint32_t box[4] = {2, (cuuint32_t)CF::QX, (cuuint32_t)CF::QX, 6};
         cuuint32_t es[4] = {1, 1, 1, 1};
         if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void *)Pl->coef, dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -635,39 +702,49 @@ wq_status launch_line_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, do
             wq_set_error("line kernel: direction-1 tables exceed shared memory");
             return WQ_EINVAL;
         }
-        cudaFuncSetAttribute(k_line<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_line<P, BND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int64_t grid = num_sms(Pl->device);
         if (grid > n_lines) grid = n_lines;
-        k_line<P><<<(unsigned)grid, CF::NT, smem, s>>>(m, a);
+        k_line<P, BND><<<(unsigned)grid, CF::NT, smem, s>>>(m, a);
         wq_count_launches(1);
         return wq_cuda_status(cudaGetLastError(), "line assembly kernel");
     }
 }
 
-}  // namespace
 
-bool line_supported(const wq_plan_s *P, int matrix) {
-    if (matrix != WQ_STIFFNESS || P->d != 3 || !P->need_stiff) return false;
-    if (!encode_fn()) return false;
-    const int64_t n1 = P->dir[0].n, nq1 = P->dir[0].nq;
-    switch (P->p) {
-    case 2: return LnCfg<2>::FITS && LnCfg<2>::SMEM + LnCfg<2>::d1_bytes(n1, nq1) <= 227 * 1024;
-    case 3: return LnCfg<3>::FITS && LnCfg<3>::SMEM + LnCfg<3>::d1_bytes(n1, nq1) <= 227 * 1024;
-    case 4: return LnCfg<4>::FITS && LnCfg<4>::SMEM + LnCfg<4>::d1_bytes(n1, nq1) <= 227 * 1024;
+template <bool BND>
+bool fits_line(int p, int64_t n1, int64_t nq1) {
+    switch (p) {
+    case 2: return LnCfg<2, BND>::FITS && LnCfg<2, BND>::SMEM + LnCfg<2, BND>::d1_bytes(n1, nq1) <= 227 * 1024;
+    case 3: return LnCfg<3, BND>::FITS && LnCfg<3, BND>::SMEM + LnCfg<3, BND>::d1_bytes(n1, nq1) <= 227 * 1024;
+    case 4: return LnCfg<4, BND>::FITS && LnCfg<4, BND>::SMEM + LnCfg<4, BND>::d1_bytes(n1, nq1) <= 227 * 1024;
     }
     return false;
 }
 
-wq_status launch_assemble_line(wq_plan_s *P, int matrix, const int32_t *lines, int64_t n_lines, double *val,
+}  // namespace
+
+bool line_supported(const wq_plan_s *P, int matrix, bool bnd) {
+    if (matrix != WQ_STIFFNESS || P->d != 3 || !P->need_stiff) return false;
+    if (!encode_fn()) return false;
+    for (int l = 0; l < 3; ++l)
+        if (P->dir[l].maxq > 3 * P->p + 1) return false;  // a support holding both boundary spans
+    return bnd ? fits_line<true>(P->p, P->dir[0].n, P->dir[0].nq) : fits_line<false>(P->p, P->dir[0].n, P->dir[0].nq);
+}
+
+wq_status launch_assemble_line(wq_plan_s *P, int matrix, bool bnd, const int32_t *lines, int64_t n_lines, double *val,
                                int32_t *col, int64_t val_base, cudaStream_t s) {
-    if (!line_supported(P, matrix)) {
+    if (!line_supported(P, matrix, bnd)) {
         wq_set_error("line kernel not available for this plan");
         return WQ_EINVAL;
     }
-    switch (P->p) {
-    case 2: return launch_line_p<2>(P, lines, n_lines, val, col, val_base, s);
-    case 3: return launch_line_p<3>(P, lines, n_lines, val, col, val_base, s);
-    case 4: return launch_line_p<4>(P, lines, n_lines, val, col, val_base, s);
+    switch (P->p * 2 + (bnd ? 1 : 0)) {
+    case 4: return launch_line_p<2, false>(P, lines, n_lines, val, col, val_base, s);
+    case 5: return launch_line_p<2, true>(P, lines, n_lines, val, col, val_base, s);
+    case 6: return launch_line_p<3, false>(P, lines, n_lines, val, col, val_base, s);
+    case 7: return launch_line_p<3, true>(P, lines, n_lines, val, col, val_base, s);
+    case 8: return launch_line_p<4, false>(P, lines, n_lines, val, col, val_base, s);
+    case 9: return launch_line_p<4, true>(P, lines, n_lines, val, col, val_base, s);
     }
     return WQ_EINVAL;
 }

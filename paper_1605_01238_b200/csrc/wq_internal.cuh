@@ -97,9 +97,10 @@ bool tile_supported(const wq_plan_s *P, int matrix);
 wq_status launch_assemble_ws(wq_plan_s *P, int matrix, double *val, int32_t *col, int64_t plane_lo,
                              int64_t plane_hi, int64_t val_base, cudaStream_t s);
 bool ws_supported(const wq_plan_s *P, int matrix);
-wq_status launch_assemble_line(wq_plan_s *P, int matrix, const int32_t *lines, int64_t n_lines, double *val,
-                               int32_t *col, int64_t val_base, cudaStream_t s);
-bool line_supported(const wq_plan_s *P, int matrix);
+// line kernel over a list of lines; bnd = lines touching a boundary span in direction 2 or 3
+wq_status launch_assemble_line(wq_plan_s *P, int matrix, bool bnd, const int32_t *lines, int64_t n_lines,
+                               double *val, int32_t *col, int64_t val_base, cudaStream_t s);
+bool line_supported(const wq_plan_s *P, int matrix, bool bnd);
 // tile kernel over an explicit list of lines of the plan's slab
 wq_status launch_assemble_tile_list(wq_plan_s *P, int matrix, const int32_t *lines, int64_t n_lines, double *val,
                                     int32_t *col, int64_t val_base, cudaStream_t s);

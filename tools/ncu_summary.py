@@ -57,3 +57,24 @@ tot = sum(by.values())
 for ln, val in by.most_common(ntop):
     top = reason[ln].most_common(3)
     print(f"{ln:4d} {val / tot * 100:5.1f}% {src.get(ln, '').strip()[:62]:62s} {[(k[6:], int(x)) for k, x in top]}")
+
+# per-region totals: instructions executed and stall samples by source line ranges (argv[3:] as "name:lo-hi")
+if len(sys.argv) > 3:
+    ie_col = h.index("Instructions Executed")
+    inst = collections.Counter()
+    cur = None
+    for r in rows[hi + 1:]:
+        if len(r) < 5 or (r[0] and not r[0].isdigit()):
+            continue
+        if r[0]:
+            cur = int(r[0])
+        try:
+            inst[cur] += float(r[ie_col] or 0)
+        except ValueError:
+            pass
+    for spec in sys.argv[3:]:
+        name, rng = spec.split(":")
+        lo, hi_ = map(int, rng.split("-"))
+        ii = sum(v for k, v in inst.items() if k and lo <= k <= hi_)
+        ss_ = sum(v for k, v in by.items() if k and lo <= k <= hi_)
+        print(f"region {name}: instr {ii:.3g}  stall-samples {ss_ / tot * 100:.1f}%")

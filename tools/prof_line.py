@@ -32,4 +32,4 @@ nw = int(sys.argv[2]) if len(sys.argv) > 2 else 11
 a = np.frombuffer(buf, dtype=np.uint64)[: 148 * nw * 4].reshape(148, nw, 4).astype(np.float64)
 for w in range(nw):
     tot = a[:, w, 0].mean()
-    print(f"warp {w:2d}: total {tot/1e6:7.3f} Mcyc  waitA {a[:, w, 1].mean()/tot*100:5.1f}%  waitB {a[:, w, 2].mean()/tot*100:5.1f}%")
+    print(f"warp {w:2d}: total {tot/1e6:7.3f} Mcyc  waitA {a[:, w, 1].mean()/tot*100:5.1f}%  waitB {a[:, w, 2].mean()/tot*100:5.1f}%  waitC {a[:, w, 3].mean()/tot*100:5.1f}%")
