@@ -45,62 +45,99 @@ def peaks():
 
 
 def fp64_peak_tflops(sm_mhz):
-    # 148 SMs x 64 FP64 FMA/clk/SM x 2 FLOP (B200: 1/2 of the FP32 FMA rate per SM)
+    # 148 SMs x 64 FP64 FMA/clk/SM x 2 FLOP; at 1965 MHz 37.2 TF, which the DMMA microbenchmark
+    # reaches (37.1 TF) and DFMA nearly (34.2 TF): profiles/r01_fp64_peak.jsonl (tools/fp64_peak.cu)
     return 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
 
 
+def stiffness_flops(plan_h, p):
+    """Algorithmic FLOPs of the stiffness row-block step: (4 S1 + 6 T1) R with
+    S1 = sum_i #I_1 #Q_1, T1 = sum_i #Q_1, R = (sum_i #I_i)^2 over the other directions."""
+    import paper_1605_01238_b200 as wq
+    info = wq.wq_plan_info(plan_h)
+    n = info["n_dof"][0]
+    R1 = wq.wq_export_rules(plan_h, 0, p)
+    qlen = R1["qlen"].astype(np.int64)
+    ilen = np.array([min(n - 1, i + p) - max(0, i - p) + 1 for i in range(n)], dtype=np.int64)
+    S1, T1 = int((ilen * qlen).sum()), int(qlen.sum())
+    R = info["nnz_local"] / int(ilen.sum())
+    return (4 * S1 + 6 * T1) * R
+
+
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled during the timed region.
+
+    NVML (pynvml) polled every ~2 ms from a thread, so that even a ~100 ms timed
+    region gets dozens of samples; falls back to `nvidia-smi -lms 100`."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, gpu_index=0):
         self.gpu = gpu_index
+        self.samples = []  # (sm_mhz, reasons_mask)
+        self.max_mhz = None
+        self.stop = False
         self.proc = None
-        self.lines = []
+
+    def _poll_nvml(self, nv, h):
+        while not self.stop:
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                     nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._poll_nvml, args=(nv, h), daemon=True)
             self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+            self.mode = "nvml"
+        except Exception:
+            self.mode = "nvidia-smi"
+            q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}",
+                                              "--format=csv,noheader,nounits", "-lms", "100"],
+                                             stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=self._read_smi, daemon=True)
+                self.t.start()
+            except FileNotFoundError:
+                self.proc = None
         return self
 
-    def _read(self):
+    def _read_smi(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            f = [x.strip() for x in line.split(",")]
+            try:
+                self.max_mhz = float(f[1])
+                self.samples.append((float(f[0]), int(f[2], 16)))
+            except (ValueError, IndexError):
+                pass
 
     def __exit__(self, *a):
+        self.stop = True
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        if hasattr(self, "t"):
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"], "samples": 0}
+        sm = [x[0] for x in self.samples]
+        reasons = sorted({nm for _, m in self.samples for nm, bit in self.REASONS.items() if m & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(sm), "source": self.mode}
 
 
 # ------------------------------------------------------------------- ours
@@ -116,6 +153,8 @@ def run_ours(cfg, steps, warmup, rank, world, device, dist, want_e2e=True, want_
     plan = wq.Plan(cfg.p, knots, slab=(cuts[rank], cuts[rank + 1]), need_mass=False, need_stiffness=True,
                    device=device)
     info = plan.info
+    wq.wq_build_rules(plan.h)
+    flops = stiffness_flops(plan.h, cfg.p)
     stream = torch.cuda.Stream(device)
     d_ctrl = torch.from_numpy(ctrl).to(device)
     rp, col, val = plan.alloc_csr()
@@ -169,7 +208,7 @@ def run_ours(cfg, steps, warmup, rank, world, device, dist, want_e2e=True, want_
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_total, t_asm_max = float(tt[0]), float(tt[1])
         dist.barrier()
-    res = dict(nnz=info["nnz_total"], nnz_local=info["nnz_local"], rows_local=info["n_rows_local"],
+    res = dict(nnz=info["nnz_total"], nnz_local=info["nnz_local"], rows_local=info["n_rows_local"], flops=flops,
                t_total=t_total, t_step=t_total / steps, t_asm=t_asm_mean, launches=launches // steps,
                clocks=clk.summary(), coef_points=info["coef_points"], n_dof=info["n_dof_total"])
     # end to end through the public host-buffer call (rank-local block)
@@ -290,11 +329,18 @@ def main():
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
         traffic = json.load(open(tf)).get(f"C4p{cfg.p}")
-    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-            "traffic": traffic, "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": res["t_asm"] * 1e3,
-            "kernel_share_of_step": res["t_asm"] / res["t_step"],
-            "fp64_flop_frac": None}
+    fp64_max = fp64_peak_tflops(res["clocks"]["sm_max_mhz"] or 1965.0)
+    t_hbm, t_fp = alg_bytes / (hbm_peak * 1e9), res["flops"] / (fp64_max * 1e12)
+    roof = {"bound": "hbm" if t_hbm >= t_fp else "fp64", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+            "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": alg_bytes,
+            "algorithmic_bytes": "12 B/nnz (8 value + 4 column) + 48 B per coefficient point read",
+            "kernel": "wq_assemble (line kernel: interior + boundary-line launches)",
+            "kernel_ms": res["t_asm"] * 1e3, "kernel_share_of_step": res["t_asm"] / res["t_step"],
+            "fp64": {"algorithmic_flops_per_launch": res["flops"], "achieved_tflops": res["flops"] / res["t_asm"] / 1e12,
+                     "peak_tflops": fp64_max, "frac": res["flops"] / res["t_asm"] / 1e12 / fp64_max,
+                     "peak_source": "148 SM x 64 DFMA/clk x 2 at max SM clock (DMMA microbenchmark 37.1 TF)"},
+            "roofline_time_ms": max(t_hbm, t_fp) * 1e3, "frac_of_roofline": max(t_hbm, t_fp) / res["t_asm"]}
     line = {"metric": "CSR nonzeros assembled/sec (FP64, 3D, p=2..10) and % of HBM-write roofline",
             "value": value, "unit": "nnz/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": res["t_total"] / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
@@ -320,8 +366,11 @@ def main():
             c = baseline_config("C4", p)
             rr = run_ours(c, 3, 3, rank, world, device, dist, want_e2e=False)
             ab = 12 * rr["nnz_local"] + 8 * rr["coef_points"] * 6
+            th, tf_ = ab / (hbm_peak * 1e9), rr["flops"] / (fp64_peak_tflops(1965.0) * 1e12)
             sweep.append({"p": p, "nnz": rr["nnz"], "value": rr["nnz"] / rr["t_step"], "ms_per_step": rr["t_step"] * 1e3,
                           "asm_ms": rr["t_asm"] * 1e3, "hbm_frac": ab / rr["t_asm"] / 1e9 / hbm_peak,
+                          "fp64_frac": rr["flops"] / rr["t_asm"] / 1e12 / fp64_peak_tflops(1965.0),
+                          "bound": "hbm" if th >= tf_ else "fp64", "frac_of_roofline": max(th, tf_) / rr["t_asm"],
                           "sm_mhz": rr["clocks"]["sm_mhz"]})
             torch.cuda.empty_cache()
         line["sweep"] = sweep
