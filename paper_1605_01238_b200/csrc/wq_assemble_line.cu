@@ -45,7 +45,7 @@ __host__ __device__ constexpr LnPar ln_par(int p, bool bnd) {
         switch (p) {
         case 2: return {4, 8, 6, 20, 1};
         case 3: return {4, 4, 6, 16, 1};
-        case 4: return {3, 2, 4, 12, 1};
+        case 4: return {3, 2, 3, 12, 1};
         default: return {0, 0, 0, 0, 0};
         }
     }
@@ -86,8 +86,9 @@ struct LnCfg {
     static constexpr int BOXD = (6 * QX * QX * 2 + 15) / 16 * 16;
     static constexpr int YD = BND ? (3 * 2 * QX * K * 2 + 15) / 16 * 16 : 0;
     static constexpr int TABD = 4 * QX * NP + 4 * QX + 4 * QX + QX;  // per-warp line tables (doubles; + offsets)
-    static constexpr int SSTV = 32 * K + 2;
-    static constexpr int SSTC = 32 * K + 4;
+    // team staging: one row of the team (K^3 entries max) per buffer, 2 buffers (row parity)
+    static constexpr int SSTV = (K * K * K + 2 + 1) / 2 * 2;
+    static constexpr int SSTC = (K * K * K + 4 + 3) / 4 * 4;
     __host__ __device__ static constexpr size_t al(size_t x) { return (x + 127) & ~(size_t)127; }
     static constexpr size_t O_BAR = 0;
     static constexpr size_t O_BOX = al(8 * (2 * NWP + 2 * NTS + 2 * NWC));
@@ -97,8 +98,8 @@ struct LnCfg {
     static constexpr size_t O_W1 = al(O_B1 + (size_t)RING * NP * 16);
     static constexpr size_t W1D = (size_t)NR * QB * 4;  // doubles per W1 buffer (rows x max #Q x 4 families)
     static constexpr size_t O_SV = al(O_W1 + (size_t)NWC * 2 * W1D * 8);
-    static constexpr size_t O_SC = al(O_SV + (size_t)NWC * SSTV * 8);
-    static constexpr size_t SMEM = al(O_SC + (size_t)NWC * SSTC * 4);
+    static constexpr size_t O_SC = al(O_SV + (size_t)NTEAM * 2 * SSTV * 8);
+    static constexpr size_t SMEM = al(O_SC + (size_t)NTEAM * 2 * SSTC * 4);
     // direction-1 index tables (qlo, qlen, jlo, jlen [n1] int32, pref [n1+1] int64, span [nq1] int32)
     // follow at SMEM (size depends on n1: d1_bytes)
     __host__ __device__ static constexpr size_t d1_bytes(int64_t n1, int64_t nq1) {
@@ -142,8 +143,18 @@ __device__ __forceinline__ LItem ln_item(const LnArgs &a, int64_t it) {
     return I;
 }
 
+// debug builds (-DWQ_LINE_DEBUG): ablation mask WQ_LINE_DBG and per-warp wait-cycle accounting
+// WQ_LINE_PROF (tools/prof_line.py); compiled out of the product build
+#ifdef WQ_LINE_DEBUG
+#define LDBG(bit) (a.dbg & (bit))
+#define LPROF true
+#else
+#define LDBG(bit) false
+#define LPROF false
+#endif
+
 __device__ __forceinline__ void twait(uint64_t *b, unsigned par, unsigned long long *acc) {
-    if (acc) {
+    if (LPROF && acc) {
         const long long t0 = clock64();
         mbar_wait(b, par);
         *acc += clock64() - t0;
@@ -195,9 +206,10 @@ __global__ void __launch_bounds__(LnCfg<P, BND>::NT, 1)
     const int64_t n_tasks = my_items * NTASK;
     const long long t_start = clock64();
     unsigned long long wA = 0, wB = 0, wC = 0;
-    unsigned long long *pA = a.prof ? &wA : nullptr, *pB = a.prof ? &wB : nullptr, *pC = a.prof ? &wC : nullptr;
+    unsigned long long *pA = LPROF && a.prof ? &wA : nullptr, *pB = LPROF && a.prof ? &wB : nullptr,
+                       *pC = LPROF && a.prof ? &wC : nullptr;
     auto prof_out = [&]() {
-        if (a.prof && lane == 0) {
+        if (LPROF && a.prof && lane == 0) {
             unsigned long long *o = a.prof + ((size_t)blockIdx.x * (blockDim.x / 32) + warp) * 4;
             o[0] = clock64() - t_start; o[1] = wA; o[2] = wB; o[3] = wC;
         }
@@ -227,7 +239,7 @@ __global__ void __launch_bounds__(LnCfg<P, BND>::NT, 1)
         int64_t ik = -1;
         int iq2 = 0, iq3 = 0;
         auto issue = [&](int64_t T, int b) {  // lane 0: TMA of task T into buffer b
-            if (T >= n_tasks || (a.dbg & 1)) return;
+            if (T >= n_tasks || LDBG(1)) return;
             const int64_t k = T / NTASK;
             const int tau = (int)(T % NTASK);
             if (k != ik) {
@@ -280,7 +292,7 @@ __global__ void __launch_bounds__(LnCfg<P, BND>::NT, 1)
             const int b1pt = lane / NP, b1r = lane % NP;
             const int b1q = q0 + 2 * tau + b1pt;
             if (lane < 2 * NP && b1q < q_end) b1v = __ldg((const double2 *)(v1.B + (int64_t)b1q * BS) + b1r);
-            if (!(a.dbg & 1)) twait(&pfull[wp * 2 + b], (CF::NB == 2 ? use >> 1 : use) & 1, pA);
+            if (!LDBG(1)) twait(&pfull[wp * 2 + b], (CF::NB == 2 ? use >> 1 : use) & 1, pA);
             const double *bx = box[b];  // [comp][c3][c2][pt]
             // ---------------- stage 3: fibre (m, c2), both points, chains a1 = 0 (y0), 1 (y1)
             // Y layout: [m][a1][c2][t3][pt]; interior: over the consumed box, BND: own buffer
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(LnCfg<P, BND>::NT, 1)
                 for (int pt = 0; pt < 2; ++pt)
                     #pragma unroll
                     for (int t = 0; t < K; ++t) { y0[pt][t] = 0.0; y1[pt][t] = 0.0; }
-                if (fv && !(a.dbg & 4)) {
+                if (fv && !LDBG(4)) {
                     const int ka = m, kb = m == 0 ? 1 : (m == 1 ? 3 : 4), kc = m == 0 ? 2 : (m == 1 ? 4 : 5);
                     const double w2a = W2t[c2 * 4 + (m == 1 ? 2 : 0)];  // w2^(0,b2)
                     const double w2b = W2t[c2 * 4 + (m == 1 ? 3 : 1)];  // w2^(1,b2)
@@ -350,7 +362,7 @@ __global__ void __launch_bounds__(LnCfg<P, BND>::NT, 1)
                 for (int pt = 0; pt < 2; ++pt)
                     #pragma unroll
                     for (int t = 0; t < K; ++t) g[a1][pt][t] = 0.0;
-            if (fl && !(a.dbg & 8)) {
+            if (fl && !LDBG(8)) {
                 const int m = fm, t3 = fc;
                 const double *B2c = m == 1 ? B2d : B2v;
                 const double *Ya0 = Y + ((m * 2 + 0) * QX) * K * 2 + t3 * 2;
@@ -420,8 +432,9 @@ __global__ void __launch_bounds__(LnCfg<P, BND>::NT, 1)
     const int t2c = colx % K, t3c = colx / K;
     bool live = colx < COLS;
     double *W1b = (double *)W1all + cw * 2 * CF::W1D;  // [2][NR][maxq][4]
-    double *Sv = Svall + cw * CF::SSTV;
-    int32_t *Sc = Scall + cw * CF::SSTC;
+    double *Sv0 = Svall + team * 2 * CF::SSTV;  // [2][SSTV] team staging (row parity)
+    int32_t *Sc0 = Scall + team * 2 * CF::SSTC;
+    int spar = 0;
     const int mq1 = v1.maxq;
     // W1 rows of a batch are contiguous in global memory ([i][c][f]): one bulk copy per batch,
     // prefetched one batch ahead into a double buffer
@@ -439,13 +452,7 @@ __global__ void __launch_bounds__(LnCfg<P, BND>::NT, 1)
     unsigned wuse[2] = {0, 0};
     if (lane == 0 && my_first < n1 && first < a.n_items) w1_issue(my_first, 0);
     // entry of column (t2, t3) in a row, in units of ni1: t2 + ni2 * t3 (interior: colx)
-    int el = colx, e_lo = 0, e_hi = 0, nc23 = K * K;
-    auto seg = [&]() {
-        const unsigned lm = __ballot_sync(0xffffffffu, live);
-        e_lo = lm ? __shfl_sync(0xffffffffu, el, __ffs(lm) - 1) : 0;
-        e_hi = lm ? __shfl_sync(0xffffffffu, el, 31 - __clz(lm)) + 1 : 0;
-    };
-    if (!BND) seg();
+    int el = colx, nc23 = K * K;
     uint32_t got = 0, rel = 0, Tbase = 0;  // tasks waited for / released, first task of the item
     for (int64_t it = first; it < a.n_items; it += step) {
         const LItem I = ln_item(a, it);
@@ -453,7 +460,6 @@ __global__ void __launch_bounds__(LnCfg<P, BND>::NT, 1)
             live = colx < COLS && t2c < I.ni2 && t3c < I.ni3;
             el = t2c + I.ni2 * t3c;
             nc23 = I.ni2 * I.ni3;
-            seg();
         }
         const int64_t line_off = a.g.offset(0, I.i2, I.i3) - a.val_base;
         const int colbase = n1 * ((I.jl2 + t2c) + (int)a.g.n[1] * (I.jl3 + t3c));
@@ -500,7 +506,7 @@ __global__ void __launch_bounds__(LnCfg<P, BND>::NT, 1)
                 g11 = Gs[(3 * RING + slot) * COLS + colx];
             };
             const bool interior = nr == NR && r0 >= P + 1 && r0 + NR - 1 <= n1 - P - 2;
-            if (live && !(a.dbg & 16)) {
+            if (live && !LDBG(16)) {
                 if (interior) {
                     const int slot0 = slot_of(qlo1[r0]);
                     constexpr int UW = 2 * (NR - 1) + 2 * P + 1;
@@ -568,23 +574,27 @@ __global__ void __launch_bounds__(LnCfg<P, BND>::NT, 1)
                     ++rel;
                 }
             }
-            // write the batch's rows: stage the warp's slice of each row in CSR order, TMA bulk copy
-            // of its 16-B aligned middle, <= 1 + 1 values and <= 3 + 3 columns at the ends by single lanes
-            if (e_hi > e_lo) {
-                const int nseg = e_hi - e_lo, erel = el - e_lo;
+            // write the batch's rows: the team's warps stage their slices of a row in CSR order in the
+            // team buffer; one lane of the team's first warp copies the row (contiguous in the CSR)
+            // with TMA bulk stores, the <= 1 + 1 unaligned values and <= 3 + 3 unaligned columns at
+            // the ends by single lanes; two named barriers per row (team only)
+            {
+                const int nall = TW * 32;
                 #pragma unroll
                 for (int k = 0; k < NR; ++k) {
                     if (k >= nr) break;
                     const int i1 = r0 + k;
                     const int ni1 = jlen1[i1];
-                    const int64_t dst0 = line_off + (int64_t)nc23 * pref1[i1] + ni1 * e_lo;
-                    const int len = ni1 * nseg;
+                    const int64_t dst0 = line_off + (int64_t)nc23 * pref1[i1];
+                    const int len = ni1 * nc23;
                     const int hv = (int)dst0 & 1, hc = (int)dst0 & 3;
-                    if (lane == 0) bulk_wait_read<0>();  // the previous row's copy has read the staging buffer
-                    __syncwarp();
+                    double *Sv = Sv0 + spar * CF::SSTV;
+                    int32_t *Sc = Sc0 + spar * CF::SSTC;
+                    if (wt == 0 && lane == 0) bulk_wait_read<1>();  // this buffer's copy (two rows ago) is done
+                    bar_sync(1 + team, nall);
                     if (live) {
-                        double *svl = Sv + hv + ni1 * erel;
-                        int32_t *scl = Sc + hc + ni1 * erel;
+                        double *svl = Sv + hv + ni1 * el;
+                        int32_t *scl = Sc + hc + ni1 * el;
                         const int cb = jlo1[i1] + colbase;
                         if (ni1 == K) {
                             #pragma unroll
@@ -596,25 +606,28 @@ __global__ void __launch_bounds__(LnCfg<P, BND>::NT, 1)
                         }
                     }
                     fence_async_smem();
-                    __syncwarp();
-                    const int nbv = (len - hv) & ~1, tv = hv + nbv;
-                    const int h4 = min((4 - hc) & 3, len);
-                    const int nbc = (len - h4) & ~3, tc = h4 + nbc;
-                    double *dv = a.val + dst0;
-                    int32_t *dc = a.col + dst0;
-                    if (lane == 0) {
-                        if (nbv > 0) bulk_s2g(dv + hv, Sv + 2 * hv, (unsigned)nbv * 8u);
-                        if (a.col && nbc > 0) bulk_s2g(dc + h4, Sc + hc + h4, (unsigned)nbc * 4u);
-                        bulk_commit();
-                    } else if (lane == 1) {
-                        if (hv) dv[0] = Sv[1];
-                    } else if (lane == 2) {
-                        if (tv < len) dv[tv] = Sv[hv + tv];
-                    } else if (a.col && lane < 7) {
-                        if (lane - 4 >= 0 && lane - 4 < h4) dc[lane - 4] = Sc[hc + lane - 4];
-                    } else if (a.col && lane >= 8 && lane < 12) {
-                        if (tc + lane - 8 < len) dc[tc + lane - 8] = Sc[hc + tc + lane - 8];
+                    bar_sync(1 + team, nall);
+                    if (wt == 0) {
+                        const int nbv = (len - hv) & ~1, tv = hv + nbv;
+                        const int h4 = min((4 - hc) & 3, len);
+                        const int nbc = (len - h4) & ~3, tc = h4 + nbc;
+                        double *dv = a.val + dst0;
+                        int32_t *dc = a.col + dst0;
+                        if (lane == 0) {
+                            if (nbv > 0) bulk_s2g(dv + hv, Sv + 2 * hv, (unsigned)nbv * 8u);
+                            if (a.col && nbc > 0) bulk_s2g(dc + h4, Sc + hc + h4, (unsigned)nbc * 4u);
+                            bulk_commit();
+                        } else if (lane == 1) {
+                            if (hv) dv[0] = Sv[1];
+                        } else if (lane == 2) {
+                            if (tv < len) dv[tv] = Sv[hv + tv];
+                        } else if (a.col && lane >= 4 && lane < 7) {
+                            if (lane - 4 < h4) dc[lane - 4] = Sc[hc + lane - 4];
+                        } else if (a.col && lane >= 8 && lane < 12) {
+                            if (tc + lane - 8 < len) dc[tc + lane - 8] = Sc[hc + tc + lane - 8];
+                        }
                     }
+                    spar ^= 1;
                 }
             }
         }
@@ -675,7 +688,7 @@ wq_status launch_line_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, do
         a.val_base = val_base;
         a.dbg = getenv("WQ_LINE_DBG") ? atoi(getenv("WQ_LINE_DBG")) : 0;
         a.prof = nullptr;
-        if (getenv("WQ_LINE_PROF")) {  // debug: cycle accounting per warp, read back with wq_debug_prof
+        if (LPROF && getenv("WQ_LINE_PROF")) {  // debug: cycle accounting per warp, read back with wq_debug_prof
             static unsigned long long *buf = nullptr;
             if (!buf) cudaMalloc(&buf, sizeof(unsigned long long) * 148 * 32 * 4);
             cudaMemset(buf, 0, sizeof(unsigned long long) * 148 * 32 * 4);

@@ -6,11 +6,21 @@ import sys
 os.environ["WQ_LINE_PROF"] = "1"
 os.environ.setdefault("WQ_LINE_ONLY", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import subprocess  # noqa: E402
+
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_1605_01238_b200 as wq  # noqa: E402
 from wqinputs import baseline_config  # noqa: E402
+
+_cs = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1605_01238_b200", "csrc")
+_lib = "/tmp/libwq_linedebug.so"
+if not os.path.exists(_lib):
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-DWQ_LINE_DEBUG",
+                    "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177", "-o", _lib,
+                    *sorted(os.path.join(_cs, f) for f in os.listdir(_cs) if f.endswith(".cu"))], check=True)
+wq.load_library(_lib)
 
 p = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 cfg = baseline_config("C4", p)
