@@ -45,14 +45,14 @@ __host__ __device__ constexpr LnPar ln_par(int p, bool bnd) {
         switch (p) {
         case 2: return {4, 8, 6, 20, 1};
         case 3: return {4, 4, 6, 16, 1};
-        case 4: return {3, 2, 3, 12, 1};
+        case 4: return {3, 2, 4, 11, 1};
         default: return {0, 0, 0, 0, 0};
         }
     }
     switch (p) {
     case 2: return {4, 8, 8, 24, 2};
     case 3: return {4, 4, 8, 18, 2};
-    case 4: return {3, 2, 6, 20, 1};
+    case 4: return {2, 3, 7, 14, 1};
     default: return {0, 0, 0, 0, 0};
     }
 }
@@ -73,7 +73,7 @@ struct LnCfg {
     static constexpr int NWP = ENABLED ? W.nwp : 1;
     // roles by SM sub-partition (warp % 4): 0, 1 producers, 2, 3 consumers, so that each SMSP runs
     // one role's code (instruction-cache locality) and the FP64 pipes split evenly between the roles
-    static constexpr int RW = (NWC + 1) / 2;  // warps per SMSP
+    static constexpr int RW = (NWP + NWC + 3) / 4;  // warps per SMSP
     static constexpr int NT = 32 * 4 * RW;
     static constexpr int NTS = ENABLED ? W.nts : 2;  // task slots (2 points each) in the G ring
     static constexpr int NB = ENABLED ? W.nb : 1;
@@ -105,7 +105,7 @@ struct LnCfg {
     __host__ __device__ static constexpr size_t d1_bytes(int64_t n1, int64_t nq1) {
         return al(16 * (size_t)n1 + 8 * (size_t)(n1 + 1) + 4 * (size_t)nq1);
     }
-    static constexpr bool FITS = ENABLED && (BND || NF <= 32) && 3 * K <= 32 && NWC % 2 == 0 && NWP <= 2 * RW && SMEM + d1_bytes(128, 2 * 128 + 2 * P + 1) <= 227 * 1024 &&
+    static constexpr bool FITS = ENABLED && (BND || NF <= 32) && 3 * K <= 32 &&  SMEM + d1_bytes(128, 2 * 128 + 2 * P + 1) <= 227 * 1024 &&
                                  NT <= 1024;
 };
 
@@ -223,10 +223,38 @@ __global__ void __launch_bounds__(LnCfg<P, BND>::NT, 1)
     }
     __syncthreads();
 
-    const int smsp = warp & 3, wrow = warp >> 2;
-    if (smsp < 2) {
+    // role of this warp: consumers fill SM sub-partitions 2 and 3 first (then 1, then 0, highest
+    // warp first), producers take the remaining warps
+    int cw = -1, wp = 0;
+    {
+        int pos = 0;
+        for (int pass = 0; pass < 3 && cw < 0; ++pass)
+            for (int w = pass == 0 ? 0 : CF::RW * 4 - 1; pass == 0 ? w < CF::RW * 4 : w >= 0; w += pass == 0 ? 1 : -1) {
+                const int sp = w & 3;
+                const bool take = pass == 0 ? sp >= 2 : (pass == 1 ? sp == 1 : sp == 0);
+                if (!take) continue;
+                if (pos >= CF::NWC) break;
+                if (w == warp) { cw = pos; break; }
+                ++pos;
+            }
+        if (cw < 0) {
+            for (int w = 0; w < warp; ++w) {
+                int p2 = 0, c2 = -1;
+                for (int pass = 0; pass < 3 && c2 < 0; ++pass)
+                    for (int x = pass == 0 ? 0 : CF::RW * 4 - 1; pass == 0 ? x < CF::RW * 4 : x >= 0; x += pass == 0 ? 1 : -1) {
+                        const int sp = x & 3;
+                        const bool take = pass == 0 ? sp >= 2 : (pass == 1 ? sp == 1 : sp == 0);
+                        if (!take) continue;
+                        if (p2 >= CF::NWC) break;
+                        if (x == w) { c2 = p2; break; }
+                        ++p2;
+                    }
+                if (c2 < 0) ++wp;
+            }
+        }
+    }
+    if (cw < 0) {
         // ============================================================ producer warp
-        const int wp = wrow * 2 + smsp;
         if (wp >= NWP) return;
         double *wbase = Boxes + wp * (CF::NB * BOXD + CF::YD);
         double *box[2] = {wbase, wbase + (CF::NB - 1) * BOXD};
@@ -426,7 +454,7 @@ __global__ void __launch_bounds__(LnCfg<P, BND>::NT, 1)
     }
 
     // ============================================================ stage 1 consumers
-    const int cw = wrow * 2 + (smsp - 2);
+
     const int team = cw / TW, wt = cw % TW;
     const int colx = wt * 32 + lane;
     const int t2c = colx % K, t3c = colx / K;
