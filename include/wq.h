@@ -68,9 +68,14 @@ typedef enum {
     WQ_KERNEL_WS = 3,     /* same arithmetic as TILE, warp-specialised
                              persistent pipeline (TMA coefficient stream,
                              stage-3/2 producer warps, stage-1 consumer warps) */
-    WQ_KERNEL_LINE = 4    /* lines interior in directions 2, 3 by the
+    WQ_KERNEL_LINE = 4,   /* lines interior in directions 2, 3 by the
                              warp-specialised line kernel (independent producer
                              warps, 2-point TMA tasks), the others by TILE    */
+    WQ_KERNEL_ZLINE = 5   /* stiffness, d = 3, p <= 4: lines along direction 3
+                             (rows share the direction-1/2 mode products, the
+                             direction-3 product per row) with direct coalesced
+                             stores; needs the z coefficient layout (default
+                             for such plans, see wq_plan_desc.coef_layout)    */
 } wq_kernel;
 
 typedef struct wq_plan_s *wq_plan;
@@ -86,6 +91,12 @@ typedef struct {
     int need_mass;                /* allocate for WQ_MASS                       */
     int need_stiffness;           /* allocate for WQ_STIFFNESS                  */
     int device;                   /* CUDA device ordinal                        */
+    int coef_layout;              /* 0: the library's choice (the stiffness
+                                     components in the z layout when
+                                     WQ_KERNEL_ZLINE applies; then the TILE /
+                                     WS / LINE / DIRECT kernels are unavailable
+                                     for WQ_STIFFNESS); 1: standard layout for
+                                     every component (all kernels but ZLINE)  */
 } wq_plan_desc;
 
 #define WQ_MAX_DEGREE 10

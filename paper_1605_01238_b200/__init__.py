@@ -20,7 +20,8 @@ LIB_PATH = os.path.join(_HERE, "libwq.so")
 
 WQ_OK, WQ_EINVAL, WQ_EKNOTS, WQ_ESINGULAR, WQ_EGEOMETRY, WQ_ENOMEM, WQ_ECUDA, WQ_ERANGE = range(8)
 WQ_MASS, WQ_STIFFNESS = 0, 1
-WQ_KERNEL_AUTO, WQ_KERNEL_DIRECT, WQ_KERNEL_TILE, WQ_KERNEL_WS, WQ_KERNEL_LINE = 0, 1, 2, 3, 4
+WQ_KERNEL_AUTO, WQ_KERNEL_DIRECT, WQ_KERNEL_TILE, WQ_KERNEL_WS, WQ_KERNEL_LINE, WQ_KERNEL_ZLINE = 0, 1, 2, 3, 4, 5
+WQ_LAYOUT_AUTO, WQ_LAYOUT_STANDARD = 0, 1
 WQ_MAX_DEGREE = 10
 
 EXPORTED = ("wq_plan_create", "wq_plan_destroy", "wq_plan_info", "wq_build_rules", "wq_build_coef",
@@ -38,7 +39,7 @@ class WQError(RuntimeError):
 class _Desc(C.Structure):
     _fields_ = [("d", C.c_int), ("p", C.c_int), ("n_knots", C.POINTER(C.c_int64)),
                 ("knots", C.POINTER(C.POINTER(C.c_double))), ("slab_begin", C.c_int64), ("slab_end", C.c_int64),
-                ("need_mass", C.c_int), ("need_stiffness", C.c_int), ("device", C.c_int)]
+                ("need_mass", C.c_int), ("need_stiffness", C.c_int), ("device", C.c_int), ("coef_layout", C.c_int)]
 
 
 class _Info(C.Structure):
@@ -109,14 +110,14 @@ def _stream(stream):
 
 
 # ---------------------------------------------------------------- C names
-def wq_plan_create(p, knots, slab=(0, -1), need_mass=True, need_stiffness=True, device=0):
+def wq_plan_create(p, knots, slab=(0, -1), need_mass=True, need_stiffness=True, device=0, coef_layout=0):
     lib = load_library()
     ks = [np.ascontiguousarray(k, dtype=np.float64) for k in knots]
     d = len(ks)
     nk = (C.c_int64 * d)(*[k.size for k in ks])
     arr = (C.POINTER(C.c_double) * d)(*[k.ctypes.data_as(C.POINTER(C.c_double)) for k in ks])
     desc = _Desc(d, int(p), nk, arr, int(slab[0]), int(slab[1]), int(bool(need_mass)), int(bool(need_stiffness)),
-                 int(device))
+                 int(device), int(coef_layout))
     h = C.c_void_p()
     _chk(lib.wq_plan_create(C.byref(desc), C.byref(h)), "wq_plan_create")
     return h.value
@@ -192,11 +193,11 @@ def wq_launch_count() -> int:
 class Plan:
     """RAII wrapper: one plan (one GPU, one slab) + torch-allocated buffers."""
 
-    def __init__(self, p, knots, slab=(0, -1), need_mass=True, need_stiffness=True, device=0):
+    def __init__(self, p, knots, slab=(0, -1), need_mass=True, need_stiffness=True, device=0, coef_layout=0):
         self.p = int(p)
         self.d = len(knots)
         self.device = device
-        self.h = wq_plan_create(p, knots, slab, need_mass, need_stiffness, device)
+        self.h = wq_plan_create(p, knots, slab, need_mass, need_stiffness, device, coef_layout)
         self.info = wq_plan_info(self.h)
 
     def close(self):

@@ -3,6 +3,7 @@
 // the host-buffer end-to-end call.  Host logic only; every arithmetic step of
 // the WQ path runs in the CUDA kernels of this directory.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -39,6 +40,8 @@ wq_status fail(wq_status st, const std::string &msg) {
     return st;
 }
 }  // namespace
+
+int64_t wq_host_qlo(int64_t i, int64_t E, int p) { return host_qlo(i, E, p); }
 
 static std::atomic<uint64_t> g_launches{0};
 void wq_count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
@@ -156,6 +159,20 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     P->cstride = d == 3 ? cp / P->dir[0].nq * P->cld1 : cp;
     P->ncomp_s = P->need_stiff ? d * (d + 1) / 2 : 0;
     P->ncomp = P->ncomp_s + P->need_mass;
+    // z layout for the stiffness components when the z-line kernel applies (wq.h coef_layout)
+    {
+        int64_t nn[3];
+        int32_t mq[3];
+        for (int l = 0; l < 3; ++l) { nn[l] = P->dir[l].n; mq[l] = P->dir[l].maxq; }
+        P->zlayout = d == 3 && P->need_stiff && desc->coef_layout == 0 &&
+                     zline_supported_p(d, p, nn, mq, e - b, P->cq_e - P->cq_b);
+    }
+    P->ncomp_std = P->zlayout ? P->need_mass : P->ncomp;
+    P->comp_mass = P->zlayout ? 0 : P->ncomp_s;
+    if (P->zlayout) {
+        P->zld = (P->cq_e - P->cq_b + 1) / 2 * 2;
+        P->zcs = P->dir[0].nq * P->dir[1].nq * P->zld;
+    }
 
     // ---- device allocations
     cudaError_t ce = cudaSetDevice(P->device);
@@ -203,12 +220,43 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     }
     P->gl = (double *)(A + o_gl);
     P->flags = (Flags *)(A + o_fl);
-    size_t cbytes = sizeof(double) * (size_t)P->ncomp * (size_t)P->cstride;
-    ce = cudaMalloc((void **)&P->coef, cbytes);
-    if (ce != cudaSuccess) {
-        P->coef = nullptr;
-        wq_plan_destroy(P);
-        return fail(WQ_ENOMEM, "coefficient field allocation failed (" + std::to_string(cbytes) + " bytes)");
+    size_t cbytes = sizeof(double) * (size_t)P->ncomp_std * (size_t)P->cstride;
+    if (cbytes > 0) {
+        ce = cudaMalloc((void **)&P->coef, cbytes);
+        if (ce != cudaSuccess) {
+            P->coef = nullptr;
+            wq_plan_destroy(P);
+            return fail(WQ_ENOMEM, "coefficient field allocation failed (" + std::to_string(cbytes) + " bytes)");
+        }
+    }
+    if (P->zlayout) {
+        const size_t zb = sizeof(double) * 6 * (size_t)P->zcs;
+        ce = cudaMalloc((void **)&P->coefz, zb);
+        if (ce != cudaSuccess) {
+            P->coefz = nullptr;
+            wq_plan_destroy(P);
+            return fail(WQ_ENOMEM, "z-layout coefficient field allocation failed (" + std::to_string(zb) + " bytes)");
+        }
+        cudaMemset(P->coefz, 0, zb);  // row padding stays zero
+        cbytes += zb;
+        // lines (i1, i2) of the z-line kernel: interior in directions 1 and 2 first, then the rest
+        const int64_t n0 = P->dir[0].n, n1 = P->dir[1].n;
+        auto interz = [&](int l, int64_t i) {
+            const int64_t E = P->dir[l].E, n = P->dir[l].n;
+            return i >= p + 1 && i <= n - p - 2 && host_qhi(i, E, p) - host_qlo(i, E, p) + 1 == 2 * p + 1;
+        };
+        for (int64_t i1 = 0; i1 < n1; ++i1)
+            for (int64_t i0 = 0; i0 < n0; ++i0)
+                (interz(0, i0) && interz(1, i1) ? P->zlines_int : P->zlines_bnd).push_back((int32_t)(i0 + n0 * i1));
+        const size_t zl = sizeof(int32_t) * (P->zlines_int.size() + P->zlines_bnd.size());
+        ce = cudaMalloc((void **)&P->zlines_dev, zl);
+        if (ce != cudaSuccess) { P->zlines_dev = nullptr; wq_plan_destroy(P); return fail(WQ_ENOMEM, "z line lists"); }
+        if (!P->zlines_int.empty())
+            cudaMemcpy(P->zlines_dev, P->zlines_int.data(), sizeof(int32_t) * P->zlines_int.size(), cudaMemcpyHostToDevice);
+        if (!P->zlines_bnd.empty())
+            cudaMemcpy(P->zlines_dev + P->zlines_int.size(), P->zlines_bnd.data(),
+                       sizeof(int32_t) * P->zlines_bnd.size(), cudaMemcpyHostToDevice);
+        cbytes += zl;
     }
     // row lines of the slab, split for the line kernel (interior in directions 2 and 3) vs the rest
     P->lines_dev = nullptr;
@@ -243,6 +291,8 @@ wq_status wq_plan_destroy(wq_plan P) {
     cudaSetDevice(P->device);
     if (P->arena) cudaFree(P->arena);
     if (P->coef) cudaFree(P->coef);
+    if (P->coefz) cudaFree(P->coefz);
+    if (P->zlines_dev) cudaFree(P->zlines_dev);
     if (P->lines_dev) cudaFree(P->lines_dev);
     if (P->ctrl_dev) cudaFree(P->ctrl_dev);
     if (P->stage_val) cudaFree(P->stage_val);
@@ -300,6 +350,17 @@ static wq_status assemble_range(wq_plan_s *P, int matrix, wq_kernel kernel, doub
                                 int64_t pl_lo, int64_t pl_hi, int64_t val_base, cudaStream_t s) {
     if (matrix == WQ_MASS && !P->need_mass) return fail(WQ_EINVAL, "plan was created without need_mass");
     if (matrix == WQ_STIFFNESS && !P->need_stiff) return fail(WQ_EINVAL, "plan was created without need_stiffness");
+    if (matrix == WQ_STIFFNESS && P->zlayout) {
+        if (kernel != WQ_KERNEL_AUTO && kernel != WQ_KERNEL_ZLINE)
+            return fail(WQ_EINVAL, "plan holds the stiffness coefficients in the z layout: only WQ_KERNEL_ZLINE applies "
+                                   "(create the plan with coef_layout = 1 for the other kernels)");
+        const int64_t ni = (int64_t)P->zlines_int.size(), nb = (int64_t)P->zlines_bnd.size();
+        wq_status st = launch_assemble_zline(P, false, P->zlines_dev, ni, pl_lo, pl_hi, val, col, val_base, s);
+        if (!st && nb > 0)
+            st = launch_assemble_zline(P, true, P->zlines_dev + ni, nb, pl_lo, pl_hi, val, col, val_base, s);
+        return st;
+    }
+    if (kernel == WQ_KERNEL_ZLINE) return fail(WQ_EINVAL, "z-line kernel not available for this plan (matrix, d, p, layout)");
     const bool tile = tile_supported(P, matrix);
     const bool ws = ws_supported(P, matrix);
     const bool line = line_supported(P, matrix, false) && (line_supported(P, matrix, true) || tile);
@@ -383,6 +444,7 @@ wq_status wq_form_host(wq_plan P, wq_matrix matrix, const double *h_ctrl, int64_
         return m * (2 * P->p + 1);
     }();
     int64_t target = (int64_t)1 << 26;  // ~64M nnz per chunk (768 MB of CSR)
+    if (const char *e = getenv("WQ_FORM_CHUNK_NNZ")) target = atoll(e) > 0 ? atoll(e) : target;  // tests
     int64_t ppc = target / max_plane_nnz;
     if (ppc < 1) ppc = 1;
     if (ppc > nplanes) ppc = nplanes;
@@ -499,7 +561,22 @@ wq_status wq_export_coef(wq_plan P, double *h_out, int64_t *n_values, int32_t *n
     cudaError_t ce = cudaDeviceSynchronize();
     // d = 3: un-pad the q_1 leading dimension (rows of nq_1 values at column offset c0off)
     const int64_t nq1 = P->dir[0].nq, rows = P->coef_points / nq1;
-    if (P->d < 3) {
+    if (P->zlayout) {
+        // stiffness components from the z layout [comp][q_1][q_2][q_3 - cq_b], then c (standard layout)
+        const int64_t nqa = P->dir[0].nq, nqb = P->dir[1].nq, nqc = P->cq_e - P->cq_b;
+        std::vector<double> z((size_t)6 * P->zcs);
+        if (!ce) ce = cudaMemcpy(z.data(), P->coefz, sizeof(double) * z.size(), cudaMemcpyDeviceToHost);
+        if (!ce)
+            for (int k = 0; k < 6; ++k)
+                for (int64_t qc = 0; qc < nqc; ++qc)
+                    for (int64_t qb = 0; qb < nqb; ++qb)
+                        for (int64_t qa = 0; qa < nqa; ++qa)
+                            h_out[k * P->coef_points + (qc * nqb + qb) * nqa + qa] =
+                                z[k * P->zcs + (qa * nqb + qb) * P->zld + qc];
+        if (!ce && P->need_mass)
+            ce = cudaMemcpy2D(h_out + 6 * P->coef_points, sizeof(double) * nq1, P->coef + P->c0off,
+                              sizeof(double) * P->cld1, sizeof(double) * nq1, (size_t)rows, cudaMemcpyDeviceToHost);
+    } else if (P->d < 3) {
         if (!ce) ce = cudaMemcpy(h_out, P->coef, sizeof(double) * P->ncomp * P->coef_points, cudaMemcpyDeviceToHost);
     } else if (!ce) ce = cudaMemcpy2D(h_out, sizeof(double) * nq1, P->coef + P->c0off, sizeof(double) * P->cld1, sizeof(double) * nq1,
                                (size_t)(rows * P->ncomp), cudaMemcpyDeviceToHost);

@@ -108,6 +108,10 @@ __global__ void __launch_bounds__(128) k_direct(DirectArgs a) {
 
 wq_status launch_assemble_direct(wq_plan_s *P, int matrix, double *val, int32_t *col, int64_t plane_lo,
                                  int64_t plane_hi, int64_t val_base, cudaStream_t s) {
+    if (matrix == WQ_STIFFNESS && P->zlayout) {
+        wq_set_error("direct kernel needs the standard coefficient layout (plan uses the z layout)");
+        return WQ_EINVAL;
+    }
     int64_t rpp = 1;
     for (int l = 0; l < P->d - 1; ++l) rpp *= P->dir[l].n;
     const int64_t row_lo = plane_lo * rpp, row_hi = plane_hi * rpp;
@@ -124,7 +128,7 @@ wq_status launch_assemble_direct(wq_plan_s *P, int matrix, double *val, int32_t 
     a.nq2 = P->dir[1].nq;
     a.cq_b = P->cq_b;
     a.ncomp_s = P->ncomp_s;
-    a.comp_mass = P->need_stiff ? P->ncomp_s : 0;
+    a.comp_mass = P->comp_mass;
     a.val = val;
     a.col = col;
     a.row_lo = row_lo;

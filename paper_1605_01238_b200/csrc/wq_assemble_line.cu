@@ -727,7 +727,7 @@ wq_status launch_line_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, do
         auto fn = encode_fn();
         if (!fn) { wq_set_error("cuTensorMapEncodeTiled unavailable"); return WQ_ECUDA; }
         cuuint64_t dims[4] = {(cuuint64_t)(Pl->dir[0].nq + Pl->c0off), (cuuint64_t)Pl->dir[1].nq,
-                              (cuuint64_t)(Pl->cq_e - Pl->cq_b), (cuuint64_t)Pl->ncomp};
+                              (cuuint64_t)(Pl->cq_e - Pl->cq_b), (cuuint64_t)Pl->ncomp_std};
         cuuint64_t strides[3] = {(cuuint64_t)Pl->cld1 * 8, (cuuint64_t)Pl->cld1 * Pl->dir[1].nq * 8,
                                  (cuuint64_t)Pl->cstride * 8};
         cuuint32_t box[4] = {2, (cuuint32_t)CF::QX, (cuuint32_t)CF::QX, 6};
@@ -766,7 +766,7 @@ bool fits_line(int p, int64_t n1, int64_t nq1) {
 }  // namespace
 
 bool line_supported(const wq_plan_s *P, int matrix, bool bnd) {
-    if (matrix != WQ_STIFFNESS || P->d != 3 || !P->need_stiff) return false;
+    if (matrix != WQ_STIFFNESS || P->d != 3 || !P->need_stiff || P->zlayout) return false;
     if (!encode_fn()) return false;
     for (int l = 0; l < 3; ++l)
         if (P->dir[l].maxq > 3 * P->p + 1) return false;  // a support holding both boundary spans

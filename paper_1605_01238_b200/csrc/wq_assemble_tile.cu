@@ -506,7 +506,7 @@ wq_status launch_tile_p(wq_plan_s *Pl, double *val, int32_t *col, int64_t pl_lo,
     a.nq2 = Pl->dir[1].nq;
     a.cq_b = Pl->cq_b;
     a.npts = Pl->cstride;
-    a.comp_mass = Pl->need_stiff ? Pl->ncomp_s : 0;
+    a.comp_mass = Pl->comp_mass;
     a.val = val;
     a.col = col;
     a.val_base = val_base;
@@ -548,8 +548,8 @@ wq_status dispatch_p(wq_plan_s *Pl, double *val, int32_t *col, int64_t lo, int64
 }  // namespace
 
 bool tile_supported(const wq_plan_s *P, int matrix) {
-    (void)matrix;
     if (P->d != 3 || P->p < 1 || P->p > 10) return false;
+    if (matrix == WQ_STIFFNESS && P->zlayout) return false;  // stiffness components are in the z layout
     for (int l = 0; l < 3; ++l)
         if (P->dir[l].maxq > 3 * P->p + 1) return false;  // a support holding both boundary spans
     return true;

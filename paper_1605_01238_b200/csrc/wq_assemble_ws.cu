@@ -689,7 +689,7 @@ bool make_map(CUtensorMap *m, const wq_plan_s *Pl, int box_q1, int box_q2, int b
     auto fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[4] = {(cuuint64_t)(Pl->dir[0].nq + Pl->c0off), (cuuint64_t)Pl->dir[1].nq, (cuuint64_t)(Pl->cq_e - Pl->cq_b),
-                          (cuuint64_t)Pl->ncomp};
+                          (cuuint64_t)Pl->ncomp_std};
     cuuint64_t strides[3] = {(cuuint64_t)Pl->cld1 * 8, (cuuint64_t)Pl->cld1 * Pl->dir[1].nq * 8,
                              (cuuint64_t)Pl->cstride * 8};
     cuuint32_t box[4] = {(cuuint32_t)box_q1, (cuuint32_t)box_q2, 1, (cuuint32_t)box_comp};
@@ -719,7 +719,7 @@ wq_status launch_ws_p(wq_plan_s *Pl, double *val, int32_t *col, int64_t pl_lo, i
         a.g.init(Pl);
         for (int l = 0; l < 3; ++l) a.v[l] = Pl->dir[l];
         a.cq_b = Pl->cq_b;
-        a.comp0 = STIFF ? 0 : (Pl->need_stiff ? Pl->ncomp_s : 0);
+        a.comp0 = STIFF ? 0 : Pl->comp_mass;
         a.val = val;
         a.col = col;
         a.val_base = val_base;
@@ -785,6 +785,7 @@ bool fits_p(int p) {
 
 bool ws_supported(const wq_plan_s *P, int matrix) {
     if (P->d != 3 || P->p < 1 || P->p > 10) return false;
+    if (matrix == WQ_STIFFNESS && P->zlayout) return false;  // stiffness components are in the z layout
     for (int l = 0; l < 3; ++l)
         if (P->dir[l].maxq > 3 * P->p + 1) return false;  // a support holding both boundary spans
     if (P->dir[0].n < 2) return false;

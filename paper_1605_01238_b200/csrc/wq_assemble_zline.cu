@@ -1,0 +1,707 @@
+// wq_assemble_zline.cu -- step 7 for the stiffness matrix in 3D: the z-line
+// kernel (WQ_KERNEL_ZLINE), warp-specialised persistent kernel, compile-time P.
+//
+// Arithmetic (Eq. sumfactorization P:837 / Alg. 3; stiffness
+// reading R8, families R3).  A LINE is the set of rows i = (i0, i1, i2) with
+// (i0, i1) fixed and i2 running over the plan's slab; its rows share the first
+// two mode products, the third one is done per row:
+//   stage A (contract c0):
+//     Y_{m,a2}(pt; c1, t0) = sum_c0 B0^{[m==0]}_{t0}(c0) H_{m,a2}(c0, c1)
+//     H_{m,1} = w0^(0,b0) w1^(0,b1) C_2m
+//     H_{m,0} = w0^(1,b0) w1^(0,b1) C_0m + w0^(0,b0) w1^(1,b1) C_1m,   b_k = [m==k]
+//   stage B (contract c1):
+//     G[b2][a2](pt; t0, t1) = sum_{m: [m==2]=b2} sum_c1 B1^{[m==1]}_{t1}(c1) Y_{m,a2}(pt; c1, t0)
+//   stage C (contract c2, per row i2):
+//     S(i; t0, t1, t2) = sum_c2 B2_{t2}(c2) U0(c2) + B2'_{t2}(c2) U1(c2),
+//     U0 = w2^(0,0) G[0][0] + w2^(1,0) G[0][1],  U1 = w2^(0,1) G[1][0] + w2^(1,1) G[1][1].
+// Direction 2 is the slowest index of a row's CSR segment (columns ascend with
+// j0 fastest), so a lane that owns one column pair (t0, t1) writes S for every
+// t2 with plain coalesced stores straight from registers: no staging buffer,
+// no barrier among the consumers.
+//
+// Roles inside one persistent CTA per SM (roles fixed by SM sub-partition):
+//   producer warps (warp % 4 in {0, 1}): task = 2 consecutive points q2 of a
+//     line.  Lane 0 TMA-loads the task's coefficient box (2 points x #Q0 x #Q1
+//     x 6 components) from the z-layout field [comp][q0][q1][q2]; stage A with
+//     lanes = (m, c1), Y over the consumed box (separate buffer for boundary
+//     lines), stage B with lanes = (m, t0); G of the two points and their
+//     direction-2 basis pairs go to a ring of NTS task slots (mbarriers
+//     gfull / gempty).
+//   consumer warps (warp % 4 in {2, 3}): batches of NR consecutive rows,
+//     batches round-robin over the consumer warps; each lane owns CPL columns
+//     (t0, t1); per-row weights w2 come in by one bulk copy per batch.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cstdlib>
+#include "wq_rows.cuh"
+#include "wq_dev.cuh"
+
+using namespace wqdev;
+
+namespace {
+
+struct ZPar {
+    int nr, rw, nts, nb;  // rows per consumer batch, warps per SM sub-partition, task slots, box buffers per producer
+};
+__host__ __device__ constexpr ZPar z_par(int p, bool bnd) {
+    switch (p) {
+    case 2: return bnd ? ZPar{4, 3, 12, 1} : ZPar{4, 3, 16, 2};
+    case 3: return bnd ? ZPar{3, 2, 12, 1} : ZPar{3, 2, 16, 2};
+    case 4: return bnd ? ZPar{2, 2, 12, 1} : ZPar{2, 2, 16, 2};
+    default: return {0, 0, 0, 0};
+    }
+}
+
+template <int P, bool BND>
+struct ZCfg {
+    static constexpr ZPar W = z_par(P, BND);
+    static constexpr bool ENABLED = W.nr > 0;
+    static constexpr int K = 2 * P + 1;   // #I of an interior row = #Q of an interior row
+    static constexpr int QI = 2 * P + 1;
+    static constexpr int QB = 3 * P + 1;  // max #Q of a row
+    static constexpr int NP = P + 1;
+    static constexpr int COLS = K * K;
+    static constexpr int CPL = (COLS + 31) / 32;  // columns (t0, t1) per consumer lane
+    static constexpr int NR = ENABLED ? W.nr : 1;
+    static constexpr int RW = ENABLED ? W.rw : 1;
+    static constexpr int NWC = 2 * RW, NWP = 2 * RW;
+    static constexpr int NT = 128 * RW;
+    static constexpr int NTS = ENABLED ? W.nts : 2;
+    static constexpr int NB = ENABLED ? W.nb : 1;
+    static constexpr int RING = 2 * NTS;
+    static constexpr int QX = BND ? QB : QI;         // box / table extent in directions 0, 1
+    static constexpr int NF = 3 * QX;                // stage-A fibres (m, c1)
+    static constexpr int NPASS = (NF + 31) / 32;
+    static constexpr int BOXD = (6 * QX * QX * 2 + 15) / 16 * 16;
+    static constexpr int YD = BND ? (3 * 2 * QX * K * 2 + 15) / 16 * 16 : 0;
+    static constexpr int TABD = 4 * QX * NP + 8 * QX + QX;  // B0v B0d B1v B1d, W0 W1, offsets (int pairs)
+    static constexpr int W2D = NR * QB * 4;                  // doubles per consumer weight buffer
+    __host__ __device__ static constexpr size_t al(size_t x) { return (x + 127) & ~(size_t)127; }
+    static constexpr size_t O_BAR = 0;
+    static constexpr size_t O_BOX = al(8 * (NB * NWP + 2 * NTS + 2 * NWC));
+    static constexpr size_t O_TAB = al(O_BOX + (size_t)NWP * (NB * BOXD + YD) * 8);
+    static constexpr size_t O_G = al(O_TAB + (size_t)NWP * TABD * 8);
+    static constexpr size_t O_B2 = al(O_G + (size_t)RING * 2 * COLS * 16);
+    static constexpr size_t O_W2 = al(O_B2 + (size_t)RING * NP * 16);
+    static constexpr size_t SMEM = al(O_W2 + (size_t)NWC * 2 * W2D * 8);
+    // direction-2 tables of the slab follow at SMEM: pref [n2l+1] int64 (relative to the slab), then
+    // qlo (local point), qlen, jlo, jlen [n2l] int32, span [nq2l] int32
+    __host__ __device__ static constexpr size_t d2_bytes(int64_t n2l, int64_t nq2l) {
+        return al(8 * (size_t)(n2l + 1) + 16 * (size_t)n2l + 4 * (size_t)nq2l);
+    }
+    static constexpr bool FITS = ENABLED && (BND || NF <= 32) && 3 * K <= 32 && NT <= 1024 &&
+                                 SMEM + d2_bytes(64, 2 * 64 + 2 * P + 1) <= 227 * 1024;
+};
+
+struct ZArgs {
+    DirView v[3];
+    int64_t L0, L1;        // sum_i #I_{0,i}, sum_i #I_{1,i}
+    int64_t slab_b;        // first owned plane of i2 (CSR offsets are relative to it)
+    int64_t i2b, n2l;      // rows of this launch: planes [i2b, i2b + n2l) of the slab
+    int64_t cq_b;          // first q2 of the coefficient sub-grid
+    int64_t qoff;          // even local q2 (relative to cq_b) of this launch's first task point
+    const int32_t *lines;  // line = i0 + n0 * i1
+    int64_t n_items;
+    double *val;
+    int32_t *col;
+    int64_t val_base;
+};
+
+struct ZItem {
+    int i0, i1, ql0, ql1, jl0, jl1, nq0, nq1, ni0, ni1;
+};
+
+__device__ __forceinline__ ZItem z_item(const ZArgs &a, int64_t it) {
+    ZItem I;
+    const int line = a.lines[it];
+    const int n0 = (int)a.v[0].n;
+    I.i0 = line % n0;
+    I.i1 = line / n0;
+    I.ql0 = a.v[0].qlo[I.i0];
+    I.jl0 = a.v[0].jlo[I.i0];
+    I.nq0 = a.v[0].qlen[I.i0];
+    I.ni0 = a.v[0].jlen[I.i0];
+    I.ql1 = a.v[1].qlo[I.i1];
+    I.jl1 = a.v[1].jlo[I.i1];
+    I.nq1 = a.v[1].qlen[I.i1];
+    I.ni1 = a.v[1].jlen[I.i1];
+    return I;
+}
+
+template <int P, bool BND>
+__global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
+    k_zline(const __grid_constant__ CUtensorMap tm, ZArgs a) {
+    using CF = ZCfg<P, BND>;
+    constexpr int QX = CF::QX;
+    constexpr int K = CF::K, QI = CF::QI, NP = CF::NP, COLS = CF::COLS, CPL = CF::CPL;
+    constexpr int NR = CF::NR, NWC = CF::NWC, NWP = CF::NWP, NTS = CF::NTS, RING = CF::RING, NB = CF::NB;
+    constexpr int NF = CF::NF, BOXD = CF::BOXD;
+    constexpr int BS = wq_bstride(P);
+    extern __shared__ __align__(128) unsigned char smb[];
+    uint64_t *pfull = (uint64_t *)(smb + CF::O_BAR);  // [NWP][NB]
+    uint64_t *gfull = pfull + NB * NWP;                // [NTS]
+    uint64_t *gempty = gfull + NTS;                    // [NTS]
+    uint64_t *wfull = gempty + NTS;                    // [NWC][2]
+    double *Boxes = (double *)(smb + CF::O_BOX);
+    double *Tabs = (double *)(smb + CF::O_TAB);
+    double2 *Gs = (double2 *)(smb + CF::O_G);  // [RING][b2][COLS] (a2 = 0, 1) pairs
+    double2 *B2r = (double2 *)(smb + CF::O_B2);  // [RING][NP] (value, derivative) of direction 2
+    double *W2all = (double *)(smb + CF::O_W2);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const DirView &v2 = a.v[2];
+    const int n2l = (int)a.n2l;
+    const int i2b = (int)a.i2b;
+    const int cqb = (int)(a.cq_b + a.qoff);  // local point 0 of this launch (even offset in the z field)
+    // direction-2 tables of the slab (shared by every line)
+    int64_t *pref2 = (int64_t *)(smb + CF::SMEM);
+    int *qlo2 = (int *)(pref2 + n2l + 1), *qlen2 = qlo2 + n2l, *jlo2 = qlen2 + n2l, *jlen2 = jlo2 + n2l;
+    int *span2 = jlen2 + n2l;
+    const int q_end = v2.qlo[i2b + n2l - 1] + v2.qlen[i2b + n2l - 1] - cqb;  // local end of the last row's Q
+    const int nq2l = q_end;
+    for (int x = tid; x < n2l; x += blockDim.x) {
+        qlo2[x] = v2.qlo[i2b + x] - cqb; qlen2[x] = v2.qlen[i2b + x]; jlo2[x] = v2.jlo[i2b + x]; jlen2[x] = v2.jlen[i2b + x];
+    }
+    for (int x = tid; x <= n2l; x += blockDim.x) pref2[x] = v2.pref[i2b + x] - v2.pref[a.slab_b];
+    for (int x = tid; x < nq2l; x += blockDim.x) span2[x] = v2.span[cqb + x];
+    // tasks: local points (2 tau, 2 tau + 1); the slab's first point is local 0
+    const int NTASK = (q_end + 1) / 2;
+    const int64_t first = blockIdx.x, step = gridDim.x;
+    const int64_t my_items = first < a.n_items ? (a.n_items - first + step - 1) / step : 0;
+    const int64_t n_tasks = my_items * NTASK;
+
+    if (tid == 0) {
+        for (int s = 0; s < NB * NWP; ++s) mbar_init(&pfull[s], 1);
+        for (int s = 0; s < NTS; ++s) { mbar_init(&gfull[s], 32); mbar_init(&gempty[s], NWC); }
+        for (int s = 0; s < 2 * NWC; ++s) mbar_init(&wfull[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int smsp = warp & 3, wrow = warp >> 2;
+    if (smsp < 2) {
+        // ============================================================ producer warp
+        const int wp = wrow * 2 + smsp;
+        double *wbase = Boxes + wp * (NB * BOXD + CF::YD);
+        double *Ybuf = wbase + NB * BOXD;  // BND only
+        double *tab = Tabs + wp * CF::TABD;
+        double *B0v = tab, *B0d = B0v + QX * NP, *B1v = B0d + QX * NP, *B1d = B1v + QX * NP;
+        double *W0t = B1d + QX * NP, *W1t = W0t + 4 * QX;  // [c][f], f = a + 2b
+        int *off0 = (int *)(W1t + 4 * QX), *off1 = off0 + QX;  // BND: staircase offsets span - jlo
+        constexpr unsigned BOX_BYTES = 6 * QX * QX * 2 * 8;
+        // task T = k * NTASK + tau of this warp (T = wp, wp + NWP, ...): item k, point pair tau; the
+        // issue stream (TMA of the coefficient boxes) runs NB tasks ahead of the compute stream
+        int64_t ik = -1, is_k = wp / NTASK, is_T = wp;
+        int is_tau = wp % NTASK;
+        int iq0 = 0, iq1 = 0;
+        auto issue = [&](int b) {  // lane 0: TMA of the next task of the issue stream into buffer b
+            if (is_T >= n_tasks) return;
+            if (is_k != ik) {
+                const ZItem I = z_item(a, first + is_k * step);
+                ik = is_k; iq0 = I.ql0; iq1 = I.ql1;
+            }
+            mbar_arrive_tx(&pfull[wp * NB + b], BOX_BYTES);
+            tma_load_4d(wbase + b * BOXD, &tm, &pfull[wp * NB + b], (int)a.qoff + 2 * is_tau, iq1, iq0, 0);
+            is_T += NWP;
+            is_tau += NWP;
+            while (is_tau >= NTASK) { is_tau -= NTASK; ++is_k; }
+        };
+        if (lane == 0) {
+            issue(0);
+            if (NB == 2) issue(1);
+        }
+        int64_t k = wp / NTASK;
+        int tau = wp % NTASK;
+        int64_t cur_item = -1;
+        const int fm = lane / K, fc = lane % K;  // stage B lanes (m, t0)
+        const bool fl = lane < 3 * K;
+        int cq0 = QI, cq1 = QI;
+        int use = 0;
+        for (int64_t T = wp; T < n_tasks; T += NWP, ++use) {
+            const int b = NB == 2 ? (use & 1) : 0;
+            if (use > 0) {
+                tau += NWP;
+                while (tau >= NTASK) { tau -= NTASK; ++k; }
+            }
+            if (k != cur_item) {
+                cur_item = k;
+                const ZItem I = z_item(a, first + k * step);
+                const DirView &v0 = a.v[0], &v1 = a.v[1];
+                __syncwarp();
+                if (BND) { cq0 = I.nq0; cq1 = I.nq1; }
+                for (int x = lane; x < QX * NP; x += 32) {
+                    const int c = x / NP, r = x % NP;
+                    const double2 b0 = c < cq0 ? __ldg((const double2 *)(v0.B + (int64_t)(I.ql0 + c) * BS) + r) : make_double2(0.0, 0.0);
+                    const double2 b1 = c < cq1 ? __ldg((const double2 *)(v1.B + (int64_t)(I.ql1 + c) * BS) + r) : make_double2(0.0, 0.0);
+                    B0v[x] = b0.x; B0d[x] = b0.y; B1v[x] = b1.x; B1d[x] = b1.y;
+                }
+                for (int x = lane; x < 4 * QX; x += 32) {
+                    W0t[x] = x / 4 < cq0 ? __ldg(v0.W + (int64_t)I.i0 * v0.maxq * 4 + x) : 0.0;
+                    W1t[x] = x / 4 < cq1 ? __ldg(v1.W + (int64_t)I.i1 * v1.maxq * 4 + x) : 0.0;
+                }
+                if (BND)
+                    for (int x = lane; x < QX; x += 32) {
+                        off0[x] = x < cq0 ? v0.span[I.ql0 + x] - I.jl0 : 0;
+                        off1[x] = x < cq1 ? v1.span[I.ql1 + x] - I.jl1 : 0;
+                    }
+                __syncwarp();
+            }
+            // direction-2 basis pairs of the task's points (published with G)
+            double2 b2v = make_double2(0.0, 0.0);
+            const int b2pt = lane / NP, b2r = lane % NP;
+            const int b2q = 2 * tau + b2pt;
+            if (lane < 2 * NP && b2q < q_end) b2v = __ldg((const double2 *)(v2.B + (int64_t)(cqb + b2q) * BS) + b2r);
+            mbar_wait(&pfull[wp * NB + b], (NB == 2 ? use >> 1 : use) & 1);
+            const double *bx = wbase + b * BOXD;  // [comp][c0][c1][pt]
+            // ---------------- stage A: fibre (m, c1), both points, chains a2 = 0 (y0), 1 (y1)
+            // Y layout: [m][a2][c1][t0][pt]; interior: over the consumed box, BND: own buffer
+            double *Y = BND ? Ybuf : wbase + b * BOXD;
+            #pragma unroll
+            for (int pass = 0; pass < CF::NPASS; ++pass) {
+                const int f = lane + 32 * pass;
+                const int m = f / QX, c1 = f % QX;
+                const bool fv = f < NF && (!BND || c1 < cq1);
+                double y0[2][K], y1[2][K];
+                #pragma unroll
+                for (int pt = 0; pt < 2; ++pt)
+                    #pragma unroll
+                    for (int t = 0; t < K; ++t) { y0[pt][t] = 0.0; y1[pt][t] = 0.0; }
+                if (fv) {
+                    // components: a2 = 1 chain C_2m, a2 = 0 chain C_0m and C_1m (C_00 C_01 C_02 C_11 C_12 C_22)
+                    const int ka = m == 0 ? 2 : (m == 1 ? 4 : 5);
+                    const int kb = m == 0 ? 0 : (m == 1 ? 1 : 2);
+                    const int kc = m == 0 ? 1 : (m == 1 ? 3 : 4);
+                    const double w1a = W1t[c1 * 4 + (m == 1 ? 2 : 0)];  // w1^(0,b1)
+                    const double w1b = W1t[c1 * 4 + (m == 1 ? 3 : 1)];  // w1^(1,b1)
+                    const double *B0c = m == 0 ? B0d : B0v;
+                    const int w0o = m == 0 ? 2 : 0;
+                    auto plane = [&](int c0, auto O) {
+                        constexpr int o0 = decltype(O)::value;
+                        const double w0a = W0t[c0 * 4 + w0o], w0b = W0t[c0 * 4 + w0o + 1];  // w0^(0,b0), w0^(1,b0)
+                        const double s1 = w0a * w1a, s2 = w0b * w1a, s3 = w0a * w1b;
+                        const double2 ca = *(const double2 *)(bx + ((ka * QX + c0) * QX + c1) * 2);
+                        const double2 cb = *(const double2 *)(bx + ((kb * QX + c0) * QX + c1) * 2);
+                        const double2 cc = *(const double2 *)(bx + ((kc * QX + c0) * QX + c1) * 2);
+                        const double h1a = s1 * ca.x, h1b = s1 * ca.y;                                // l = 2
+                        const double h0a = fma(s2, cb.x, s3 * cc.x), h0b = fma(s2, cb.y, s3 * cc.y);  // l = 0, 1
+                        #pragma unroll
+                        for (int r = 0; r <= P; ++r) {
+                            const double bv = B0c[c0 * NP + r];
+                            y1[0][o0 + r] = fma(bv, h1a, y1[0][o0 + r]);
+                            y1[1][o0 + r] = fma(bv, h1b, y1[1][o0 + r]);
+                            y0[0][o0 + r] = fma(bv, h0a, y0[0][o0 + r]);
+                            y0[1][o0 + r] = fma(bv, h0b, y0[1][o0 + r]);
+                        }
+                    };
+                    if constexpr (BND) {
+                        #pragma unroll 1
+                        for (int c0 = 0; c0 < cq0; ++c0)
+                            dispatch<0, K - NP>(off0[c0], [&](auto O) { plane(c0, O); });
+                    } else {
+                        unroll<QI>([&](auto C0) {
+                            constexpr int c0 = decltype(C0)::value;
+                            plane(c0, std::integral_constant<int, (c0 + 1) / 2>{});
+                        });
+                    }
+                }
+                if (!BND) __syncwarp();  // every lane has read the box: Y may overwrite it
+                if (fv) {
+                    double *Y0 = Y + ((m * 2 + 0) * QX + c1) * K * 2;
+                    double *Y1 = Y + ((m * 2 + 1) * QX + c1) * K * 2;
+                    #pragma unroll
+                    for (int t = 0; t < K; ++t) {
+                        *(double2 *)(Y0 + t * 2) = make_double2(y0[0][t], y0[1][t]);
+                        *(double2 *)(Y1 + t * 2) = make_double2(y1[0][t], y1[1][t]);
+                    }
+                }
+            }
+            __syncwarp();
+            // ---------------- stage B: lane (m, t0): g[a2][pt][t1]
+            double g[2][2][K];
+            #pragma unroll
+            for (int a2 = 0; a2 < 2; ++a2)
+                #pragma unroll
+                for (int pt = 0; pt < 2; ++pt)
+                    #pragma unroll
+                    for (int t = 0; t < K; ++t) g[a2][pt][t] = 0.0;
+            if (fl) {
+                const int m = fm, t0 = fc;
+                const double *B1c = m == 1 ? B1d : B1v;
+                const double *Ya0 = Y + ((m * 2 + 0) * QX) * K * 2 + t0 * 2;
+                const double *Ya1 = Y + ((m * 2 + 1) * QX) * K * 2 + t0 * 2;
+                auto point1 = [&](int c1, auto O) {
+                    constexpr int o1 = decltype(O)::value;
+                    const double2 ya0 = *(const double2 *)(Ya0 + c1 * K * 2);
+                    const double2 ya1 = *(const double2 *)(Ya1 + c1 * K * 2);
+                    #pragma unroll
+                    for (int r = 0; r <= P; ++r) {
+                        const double bv = B1c[c1 * NP + r];
+                        g[0][0][o1 + r] = fma(bv, ya0.x, g[0][0][o1 + r]);
+                        g[0][1][o1 + r] = fma(bv, ya0.y, g[0][1][o1 + r]);
+                        g[1][0][o1 + r] = fma(bv, ya1.x, g[1][0][o1 + r]);
+                        g[1][1][o1 + r] = fma(bv, ya1.y, g[1][1][o1 + r]);
+                    }
+                };
+                if constexpr (BND) {
+                    #pragma unroll 1
+                    for (int c1 = 0; c1 < cq1; ++c1) dispatch<0, K - NP>(off1[c1], [&](auto O) { point1(c1, O); });
+                } else {
+                    unroll<QI>([&](auto C1) {
+                        constexpr int c1 = decltype(C1)::value;
+                        point1(c1, std::integral_constant<int, (c1 + 1) / 2>{});
+                    });
+                }
+            }
+            // G of the slot: lanes m = 1 (partial of b2 = 0) and m = 2 (b2 = 1) store, then lanes
+            // m = 0 add their part to the b2 = 0 partial in place
+            const uint32_t Tl = (uint32_t)T;
+            const int slot_t = (int)(Tl % NTS);
+            mbar_wait(&gempty[slot_t], ((Tl / NTS) & 1) ^ 1);
+            if (fl && fm != 0) {
+                const int b2 = fm == 2 ? 1 : 0, t0 = fc;
+                #pragma unroll
+                for (int pt = 0; pt < 2; ++pt) {
+                    double2 *Gd = Gs + ((slot_t * 2 + pt) * 2 + b2) * COLS + t0;
+                    #pragma unroll
+                    for (int t = 0; t < K; ++t) Gd[K * t] = make_double2(g[0][pt][t], g[1][pt][t]);
+                }
+            }
+            __syncwarp();
+            if (fl && fm == 0) {
+                const int t0 = fc;
+                #pragma unroll
+                for (int pt = 0; pt < 2; ++pt) {
+                    double2 *Gd = Gs + ((slot_t * 2 + pt) * 2 + 0) * COLS + t0;
+                    #pragma unroll
+                    for (int t = 0; t < K; ++t) {
+                        const double2 o = Gd[K * t];
+                        Gd[K * t] = make_double2(g[0][pt][t] + o.x, g[1][pt][t] + o.y);
+                    }
+                }
+            }
+            if (lane < 2 * NP) B2r[(slot_t * 2 + b2pt) * NP + b2r] = b2v;
+            mbar_arrive(&gfull[slot_t]);
+            // the buffer is free again (all lanes done with Y): prefetch the task after next into it
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) issue(b);
+        }
+        return;
+    }
+
+    // ============================================================ stage C consumers
+    const int cw = wrow * 2 + (smsp - 2);
+    const DirView &v0 = a.v[0], &v1 = a.v[1];
+    const int n0 = (int)v0.n, n01 = n0 * (int)v1.n;
+    int colx[CPL], colr[CPL], t0c[CPL], t1c[CPL];
+    #pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+        colx[j] = lane + 32 * j;
+        colr[j] = colx[j] < COLS ? colx[j] : COLS - 1;  // clamped column for shared-memory reads
+        t0c[j] = colx[j] % K;
+        t1c[j] = colx[j] / K;
+    }
+    double *W2b = W2all + cw * 2 * CF::W2D;  // [2][NR][mq2][4]
+    const int mq2 = v2.maxq;
+    // W2 rows of a batch are contiguous in global memory ([i][c][f]): one bulk copy per batch,
+    // prefetched one batch ahead into a double buffer
+    auto w2_issue = [&](int r0, int buf) {
+        const int nr = n2l - r0 < NR ? n2l - r0 : NR;
+        const unsigned bytes = (unsigned)(nr * mq2 * 32);
+        mbar_arrive_tx(&wfull[cw * 2 + buf], bytes);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(W2b + buf * CF::W2D)),
+                     "l"(v2.W + (int64_t)(i2b + r0) * mq2 * 4), "r"(bytes), "r"(smem_u32(&wfull[cw * 2 + buf]))
+                     : "memory");
+    };
+    const int my_first = cw * NR;
+    int wbuf = 0;
+    unsigned wuse[2] = {0, 0};
+    if (lane == 0 && my_first < n2l && first < a.n_items) w2_issue(my_first, 0);
+    uint32_t got = 0, rel = 0, Tbase = 0;  // tasks waited for / released, first task of the item
+    for (int64_t it = first; it < a.n_items; it += step) {
+        const ZItem I = z_item(a, it);
+        bool live[CPL];
+        int el[CPL], colb[CPL];
+        #pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+            live[j] = colx[j] < COLS && t0c[j] < I.ni0 && t1c[j] < I.ni1;
+            el[j] = t0c[j] + I.ni0 * t1c[j];
+            colb[j] = (I.jl0 + t0c[j]) + n0 * (I.jl1 + t1c[j]);
+        }
+        const int nc01 = I.ni0 * I.ni1;
+        const int64_t A = v1.pref[I.i1] * a.L0 + (int64_t)I.ni1 * v0.pref[I.i0];
+        const int64_t L01 = a.L0 * a.L1;
+        for (int r0 = cw * NR; r0 < n2l; r0 += NWC * NR) {
+            const int nr = n2l - r0 < NR ? n2l - r0 : NR;
+            const int rl = r0 + nr - 1;
+            const uint32_t t_hi = Tbase + (uint32_t)((qlo2[rl] + qlen2[rl] - 1) / 2);
+            const uint32_t t_lo = Tbase + (uint32_t)(qlo2[r0] / 2);
+            mbar_wait(&wfull[cw * 2 + wbuf], wuse[wbuf] & 1);
+            ++wuse[wbuf];
+            const double2 *W2w = (const double2 *)(W2b + wbuf * CF::W2D);  // [row][c][2] double2, row stride mq2
+            if (lane == 0) {
+                int nxt = r0 + NWC * NR;
+                bool more = true;
+                if (nxt >= n2l) { nxt = my_first; more = it + step < a.n_items; }
+                if (more) w2_issue(nxt, wbuf ^ 1);
+            }
+            wbuf ^= 1;
+            __syncwarp();
+            while (rel < got && rel < t_lo) {
+                if (lane == 0) mbar_arrive(&gempty[rel % NTS]);
+                ++rel;
+            }
+            while (got <= t_hi) {
+                mbar_wait(&gfull[got % NTS], (got / NTS) & 1);
+                ++got;
+                while (rel < got && rel < t_lo) {
+                    if (lane == 0) mbar_arrive(&gempty[rel % NTS]);
+                    ++rel;
+                }
+            }
+            __syncwarp();
+            double acc[NR][CPL][K];
+            #pragma unroll
+            for (int k = 0; k < NR; ++k)
+                #pragma unroll
+                for (int j = 0; j < CPL; ++j)
+                    #pragma unroll
+                    for (int t = 0; t < K; ++t) acc[k][j][t] = 0.0;
+            auto slot_of = [&](int q) { return (int)((Tbase * 2 + (uint32_t)q) % RING); };
+            const bool interior = nr == NR && i2b + r0 >= P + 1 && i2b + r0 + NR - 1 <= (int)v2.n - P - 2;
+            if (interior) {
+                const int slot0 = slot_of(qlo2[r0]);
+                constexpr int UW = 2 * (NR - 1) + 2 * P + 1;
+                #pragma unroll
+                for (int u = 0; u < UW; ++u) {
+                    int slot = slot0 + u;
+                    if (slot >= RING) slot -= RING;
+                    double2 g0[CPL], g1[CPL];
+                    #pragma unroll
+                    for (int j = 0; j < CPL; ++j) {
+                        g0[j] = Gs[(slot * 2 + 0) * COLS + colr[j]];
+                        g1[j] = Gs[(slot * 2 + 1) * COLS + colr[j]];
+                    }
+                    double2 bb[NP];
+                    #pragma unroll
+                    for (int r = 0; r <= P; ++r) bb[r] = B2r[slot * NP + r];
+                    #pragma unroll
+                    for (int k = 0; k < NR; ++k) {
+                        if (u >= 2 * k && u <= 2 * k + 2 * P) {
+                            const int c = u - 2 * k;
+                            const int o0 = (c + 1) / 2;
+                            const double2 *wr = W2w + (k * mq2 + c) * 2;
+                            const double2 wA = wr[0], wB = wr[1];
+                            #pragma unroll
+                            for (int j = 0; j < CPL; ++j) {
+                                const double u0 = fma(wA.x, g0[j].x, wA.y * g0[j].y);
+                                const double u1 = fma(wB.x, g1[j].x, wB.y * g1[j].y);
+                                #pragma unroll
+                                for (int r = 0; r <= P; ++r)
+                                    acc[k][j][o0 + r] = fma(bb[r].x, u0, fma(bb[r].y, u1, acc[k][j][o0 + r]));
+                            }
+                        }
+                    }
+                }
+            } else {
+                #pragma unroll
+                for (int k = 0; k < NR; ++k) {
+                    if (k >= nr) break;
+                    const int r = r0 + k;
+                    const int qb = qlo2[r], nq = qlen2[r], jl = jlo2[r];
+                    #pragma unroll 1
+                    for (int c = 0; c < nq; ++c) {
+                        const int q = qb + c;
+                        const int slot = slot_of(q);
+                        const double2 *bp = B2r + slot * NP;
+                        const double2 *wr = W2w + (k * mq2 + c) * 2;
+                        const double2 wA = wr[0], wB = wr[1];
+                        double u0[CPL], u1[CPL];
+                        #pragma unroll
+                        for (int j = 0; j < CPL; ++j) {
+                            const double2 g0 = Gs[(slot * 2 + 0) * COLS + colr[j]];
+                            const double2 g1 = Gs[(slot * 2 + 1) * COLS + colr[j]];
+                            u0[j] = fma(wA.x, g0.x, wA.y * g0.y);
+                            u1[j] = fma(wB.x, g1.x, wB.y * g1.y);
+                        }
+                        const int off = span2[q] - jl;
+                        dispatch<0, K - NP>(off, [&](auto O) {
+                            constexpr int o0 = decltype(O)::value;
+                            #pragma unroll
+                            for (int r = 0; r <= P; ++r) {
+                                const double2 bq = bp[r];
+                                #pragma unroll
+                                for (int j = 0; j < CPL; ++j)
+                                    acc[k][j][o0 + r] = fma(bq.x, u0[j], fma(bq.y, u1[j], acc[k][j][o0 + r]));
+                            }
+                        });
+                    }
+                }
+            }
+            {
+                const int nb = r0 + NWC * NR;
+                const int low = nb < n2l ? qlo2[nb] : q_end;
+                const uint32_t t_rel = Tbase + (uint32_t)(low / 2);
+                __syncwarp();
+                while (rel < t_rel && rel < got) {
+                    if (lane == 0) mbar_arrive(&gempty[rel % NTS]);
+                    ++rel;
+                }
+            }
+            // stores straight from registers: for fixed (row, t2) the lanes' columns are consecutive;
+            // interior lines have the compile-time stride K*K between the t2 slices of a row
+            const int nc = BND ? nc01 : K * K;
+            #pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                if (k >= nr) break;
+                const int r = r0 + k;
+                const int ni2 = jlen2[r];
+                const int64_t ro = pref2[r] * L01 + (int64_t)ni2 * A - a.val_base;
+                const int cb2 = n01 * jlo2[r];
+                #pragma unroll
+                for (int j = 0; j < CPL; ++j) {
+                    if (!live[j]) continue;
+                    double *dv = a.val + ro + el[j];
+                    int32_t *dc = a.col + ro + el[j];
+                    const int c0 = colb[j] + cb2;
+                    if (ni2 == K) {
+                        #pragma unroll
+                        for (int t = 0; t < K; ++t) __stcs(dv + nc * t, acc[k][j][t]);
+                        if (a.col) {
+                            #pragma unroll
+                            for (int t = 0; t < K; ++t) __stcs(dc + nc * t, c0 + n01 * t);
+                        }
+                    } else {
+                        #pragma unroll
+                        for (int t = 0; t < K; ++t)
+                            if (t < ni2) __stcs(dv + nc * t, acc[k][j][t]);
+                        if (a.col) {
+                            #pragma unroll
+                            for (int t = 0; t < K; ++t)
+                                if (t < ni2) __stcs(dc + nc * t, c0 + n01 * t);
+                        }
+                    }
+                }
+            }
+        }
+        const uint32_t t_end = Tbase + (uint32_t)NTASK;
+        while (rel < t_end) {
+            if (got <= rel) {
+                mbar_wait(&gfull[got % NTS], (got / NTS) & 1);
+                ++got;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&gempty[rel % NTS]);
+            ++rel;
+        }
+        Tbase = t_end;
+    }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 z_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+int z_num_sms(int dev) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+
+template <int P, bool BND>
+wq_status launch_zline_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, int64_t pl_lo, int64_t pl_hi,
+                         double *val, int32_t *col, int64_t val_base, cudaStream_t s) {
+    using CF = ZCfg<P, BND>;
+    if constexpr (!CF::FITS) {
+        wq_set_error("z-line kernel not configured for this degree");
+        return WQ_EINVAL;
+    } else {
+        if (n_lines <= 0) return WQ_OK;
+        ZArgs a;
+        for (int l = 0; l < 3; ++l) a.v[l] = Pl->dir[l];
+        a.L0 = Pl->L[0];
+        a.L1 = Pl->L[1];
+        a.slab_b = Pl->slab_b;
+        a.i2b = Pl->slab_b + pl_lo;
+        a.n2l = pl_hi - pl_lo;
+        a.cq_b = Pl->cq_b;
+        a.qoff = (wq_host_qlo(a.i2b, Pl->dir[2].E, Pl->p) - Pl->cq_b) & ~(int64_t)1;
+        a.lines = lines;
+        a.n_items = n_lines;
+        a.val = val;
+        a.col = col;
+        a.val_base = val_base;
+        CUtensorMap m;
+        auto fn = z_encode_fn();
+        if (!fn) { wq_set_error("cuTensorMapEncodeTiled unavailable"); return WQ_ECUDA; }
+        const int64_t nq0 = Pl->dir[0].nq, nq1 = Pl->dir[1].nq;
+        cuuint64_t dims[4] = {(cuuint64_t)Pl->zld, (cuuint64_t)nq1, (cuuint64_t)nq0, 6};
+        cuuint64_t strides[3] = {(cuuint64_t)Pl->zld * 8, (cuuint64_t)Pl->zld * nq1 * 8, (cuuint64_t)Pl->zcs * 8};
+        cuuint32_t box[4] = {2, (cuuint32_t)CF::QX, (cuuint32_t)CF::QX, 6};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void *)Pl->coefz, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            wq_set_error("cuTensorMapEncodeTiled failed for the z-layout coefficient field");
+            return WQ_ECUDA;
+        }
+        const size_t smem = CF::SMEM + CF::d2_bytes(a.n2l, Pl->cq_e - Pl->cq_b - a.qoff);
+        if (smem > 227 * 1024) {
+            wq_set_error("z-line kernel: direction-2 tables exceed shared memory");
+            return WQ_EINVAL;
+        }
+        cudaFuncSetAttribute(k_zline<P, BND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int64_t grid = z_num_sms(Pl->device);
+        if (grid > n_lines) grid = n_lines;
+        k_zline<P, BND><<<(unsigned)grid, CF::NT, smem, s>>>(m, a);
+        wq_count_launches(1);
+        return wq_cuda_status(cudaGetLastError(), "z-line assembly kernel");
+    }
+}
+
+template <bool BND>
+bool fits_z(int p, int64_t n2l, int64_t nq2l) {
+    switch (p) {
+    case 2: return ZCfg<2, BND>::FITS && ZCfg<2, BND>::SMEM + ZCfg<2, BND>::d2_bytes(n2l, nq2l) <= 227 * 1024;
+    case 3: return ZCfg<3, BND>::FITS && ZCfg<3, BND>::SMEM + ZCfg<3, BND>::d2_bytes(n2l, nq2l) <= 227 * 1024;
+    case 4: return ZCfg<4, BND>::FITS && ZCfg<4, BND>::SMEM + ZCfg<4, BND>::d2_bytes(n2l, nq2l) <= 227 * 1024;
+    }
+    return false;
+}
+
+}  // namespace
+
+bool zline_supported_p(int d, int p, const int64_t *n, const int32_t *maxq, int64_t n2l, int64_t nq2l) {
+    if (d != 3 || !z_encode_fn()) return false;
+    for (int l = 0; l < 3; ++l)
+        if (maxq[l] > 3 * p + 1 || n[l] < 2) return false;  // a support holding both boundary spans
+    return fits_z<false>(p, n2l, nq2l) && fits_z<true>(p, n2l, nq2l);
+}
+
+wq_status launch_assemble_zline(wq_plan_s *P, bool bnd, const int32_t *lines, int64_t n_lines, int64_t pl_lo,
+                                int64_t pl_hi, double *val, int32_t *col, int64_t val_base, cudaStream_t s) {
+    if (!P->coefz) {
+        wq_set_error("z-line kernel needs the z-layout coefficient field");
+        return WQ_EINVAL;
+    }
+    switch (P->p * 2 + (bnd ? 1 : 0)) {
+    case 4: return launch_zline_p<2, false>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, s);
+    case 5: return launch_zline_p<2, true>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, s);
+    case 6: return launch_zline_p<3, false>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, s);
+    case 7: return launch_zline_p<3, true>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, s);
+    case 8: return launch_zline_p<4, false>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, s);
+    case 9: return launch_zline_p<4, true>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, s);
+    }
+    wq_set_error("z-line kernel not available for this degree");
+    return WQ_EINVAL;
+}

@@ -31,6 +31,10 @@ struct CoefArgs {
     int ncomp_s, ncomp;
     int need_s, need_m;
     Flags *flags;
+    // z layout of the stiffness components (wq_internal.cuh): [comp][q_1][q_2][q_3 - cq_b]
+    int zlayout;
+    double *coefz;
+    int64_t zld, zcs;
 };
 
 // table rows at grid point q: N = degree p (functions span..span+p, stride 2:
@@ -49,9 +53,10 @@ __global__ void __launch_bounds__(NTC) k_coef(CoefArgs a) {
     extern __shared__ __align__(16) double sm[];
     const int p = a.p;
     const DirView &v1 = a.v[0], &v2 = a.v[1], &v3 = a.v[2];
-    const int64_t q1a = (int64_t)blockIdx.x * TQ1;
-    const int64_t q2a = D >= 2 ? (int64_t)blockIdx.y * TQ2 : 0;
-    const int64_t q3l = D == 3 ? (int64_t)blockIdx.z : 0;  // local plane
+    // d = 3: blockIdx.x = q_3 plane (consecutive CTAs write neighbouring q_3 of the z layout)
+    const int64_t q1a = (int64_t)(D == 3 ? blockIdx.y : blockIdx.x) * TQ1;
+    const int64_t q2a = D >= 2 ? (int64_t)(D == 3 ? blockIdx.z : blockIdx.y) * TQ2 : 0;
+    const int64_t q3l = D == 3 ? (int64_t)blockIdx.x : 0;  // local plane
     const int64_t q3 = D == 3 ? a.cq_b + q3l : 0;
     const int64_t q1off = D == 1 ? a.cq_b : 0;  // D == 1: direction 1 is the slab direction
     const int64_t nq1 = D == 1 ? a.nq_loc_d : v1.nq;
@@ -231,11 +236,14 @@ __global__ void __launch_bounds__(NTC) k_coef(CoefArgs a) {
                     double s = 0.0;
                     #pragma unroll
                     for (int k = 0; k < D; ++k) s = fma(adj[l][k], adj[m][k], s);
-                    a.coef[(int64_t)comp * npts + pt] = s * inv;
+                    if (D == 3 && a.zlayout)
+                        a.coefz[(int64_t)comp * a.zcs + (q1 * v2.nq + q2a + t2) * a.zld + q3l] = s * inv;
+                    else
+                        a.coef[(int64_t)comp * npts + pt] = s * inv;
                     ++comp;
                 }
         }
-        if (a.need_m) a.coef[(int64_t)comp * npts + pt] = ad;
+        if (a.need_m) a.coef[(int64_t)(a.zlayout ? 0 : comp) * npts + pt] = ad;
     }
 }
 
@@ -258,13 +266,17 @@ wq_status launch_coef(wq_plan_s *P, const double *ctrl, cudaStream_t s) {
     a.need_s = P->need_stiff;
     a.need_m = P->need_mass;
     a.flags = P->flags;
+    a.zlayout = P->zlayout;
+    a.coefz = P->coefz;
+    a.zld = P->zld;
+    a.zcs = P->zcs;
     const int K1M = TQ1 + P->p + 1, K2M = TQ2 + P->p + 1;
     if (P->d == 3) {
         size_t sm = (size_t)(9 * K2M * K1M + TQ2 * 9 * K1M) * sizeof(double);
         static bool set = false;
         if (!set) { cudaFuncSetAttribute(k_coef<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024); set = true; }
-        dim3 g((unsigned)((P->dir[0].nq + TQ1 - 1) / TQ1), (unsigned)((P->dir[1].nq + TQ2 - 1) / TQ2),
-               (unsigned)a.nq_loc_d);
+        dim3 g((unsigned)a.nq_loc_d, (unsigned)((P->dir[0].nq + TQ1 - 1) / TQ1),
+               (unsigned)((P->dir[1].nq + TQ2 - 1) / TQ2));
         k_coef<3><<<g, NTC, sm, s>>>(a);
     } else if (P->d == 2) {
         size_t sm = (size_t)(TQ2 * 9 * K1M) * sizeof(double);

@@ -47,12 +47,14 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, unsigned bytes) {
                  "r"(bytes)
                  : "memory");
 }
+// try_wait with a suspend-time hint: the waiting warp sleeps in hardware (up to ~0.1 ms) until the
+// phase completes instead of re-issuing the test
 __device__ __forceinline__ bool mbar_try(uint64_t *b, unsigned parity) {
     unsigned ok;
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
         : "=r"(ok)
-        : "r"(smem_u32(b)), "r"(parity)
+        : "r"(smem_u32(b)), "r"(parity), "r"(100000u)
         : "memory");
     return ok != 0;
 }
@@ -63,10 +65,10 @@ __device__ __forceinline__ bool mbar_try(uint64_t *b, unsigned parity) {
 static __device__ unsigned long long *g_wq_diag;
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
-    long long spins = 0;
+    unsigned spins = 0;
     while (!mbar_try(b, parity)) {
 #ifdef WQ_DIAG
-        if (++spins > (1ll << 22)) {
+        if (++spins > (1u << 22)) {
             if (g_wq_diag) {
                 unsigned long long k = atomicAdd(&g_wq_diag[0], 1ull);
                 if (k < 64) {
@@ -79,7 +81,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
             asm volatile("exit;");
         }
 #else
-        if (++spins > (1ll << 28)) __trap();
+        if (++spins > (1u << 26)) __trap();
 #endif
     }
 }

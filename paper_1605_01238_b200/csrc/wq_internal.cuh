@@ -54,6 +54,7 @@ struct wq_plan_s {
     int64_t cld1;                  // leading dimension along q_1 (d = 3: nq_1 + 1 rounded up to even)
     int64_t cstride;               // doubles per component = cld1 * (points / nq_1)
     int ncomp_s, ncomp;            // stiffness components, total components
+    int ncomp_std;                 // components held in coef (standard layout)
     double *coef;                  // [ncomp][cstride], point (q1, q2, q3) at q1 + c0off + cld1 * (q2 + nq2 * (q3 - cq_b))
     // Gauss-Legendre rule on [-1,1] in double-double: [p+1] (hi, lo) pairs
     double *gl;                    // [2*(p+1)] t, [2*(p+1)] w
@@ -70,9 +71,20 @@ struct wq_plan_s {
     // Both sorted; device copy in lines_dev (interior at 0, boundary at n_lines_int).
     std::vector<int32_t> lines_int, lines_bnd;
     int32_t *lines_dev;
+    // z-line kernel (d = 3 stiffness): the stiffness components live in the z layout
+    // [comp][q_1][q_2][q_3 - cq_b] (q_3 fastest, row length zld even, zero padded) instead of coef;
+    // coef then holds only the mass component.  Lines (i1 + n1 * i2) interior in directions 1 and 2
+    // first, then the rest (device copy zlines_dev).
+    int zlayout;
+    double *coefz;
+    int64_t zld, zcs;              // row length along q_3, doubles per component
+    int comp_mass;                 // component index of c in coef
+    std::vector<int32_t> zlines_int, zlines_bnd;
+    int32_t *zlines_dev;
 };
 
 // host helpers
+int64_t wq_host_qlo(int64_t i, int64_t E, int p);  // first grid point of Q_i (Remark 1, reading R1)
 void wq_count_launches(int n);  // adds n to the process-wide launch counter
 void wq_set_error(const std::string &msg);
 wq_status wq_cuda_status(cudaError_t e, const char *what);
@@ -101,6 +113,11 @@ bool ws_supported(const wq_plan_s *P, int matrix);
 wq_status launch_assemble_line(wq_plan_s *P, int matrix, bool bnd, const int32_t *lines, int64_t n_lines,
                                double *val, int32_t *col, int64_t val_base, cudaStream_t s);
 bool line_supported(const wq_plan_s *P, int matrix, bool bnd);
+// z-line kernel (stiffness, d = 3, coefficients in the z layout) over a list of lines (i1 + n1 * i2)
+// and the planes [pl_lo, pl_hi) of the slab
+bool zline_supported_p(int d, int p, const int64_t *n, const int32_t *maxq, int64_t n2l, int64_t nq2l);
+wq_status launch_assemble_zline(wq_plan_s *P, bool bnd, const int32_t *lines, int64_t n_lines, int64_t pl_lo,
+                                int64_t pl_hi, double *val, int32_t *col, int64_t val_base, cudaStream_t s);
 // tile kernel over an explicit list of lines of the plan's slab
 wq_status launch_assemble_tile_list(wq_plan_s *P, int matrix, const int32_t *lines, int64_t n_lines, double *val,
                                     int32_t *col, int64_t val_base, cudaStream_t s);

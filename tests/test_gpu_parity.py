@@ -11,7 +11,12 @@ from wqinputs import baseline_config, control_net, graded_open_knots, uniform_op
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [wq.WQ_KERNEL_DIRECT, wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_WS, wq.WQ_KERNEL_LINE]
+KERNELS = [wq.WQ_KERNEL_DIRECT, wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_WS, wq.WQ_KERNEL_LINE, wq.WQ_KERNEL_ZLINE]
+
+
+def layout_for(kernel):
+    """The z-line kernel (and AUTO) use the library's layout choice; the others need the standard one."""
+    return wq.WQ_LAYOUT_AUTO if kernel in (wq.WQ_KERNEL_AUTO, wq.WQ_KERNEL_ZLINE) else wq.WQ_LAYOUT_STANDARD
 
 
 def _torch():
@@ -28,8 +33,9 @@ def make_case(d, p, E, geometry="grid", amp=0.1, knots="uniform", seed=0):
 
 def run_full(ks, ctrl, p, matrix, kernel=wq.WQ_KERNEL_AUTO, slab=(0, -1), fused_col=True):
     torch = _torch()
-    plan = wq.Plan(p, ks, slab=slab, need_mass=True, need_stiffness=True)
-    if kernel in (wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_WS, wq.WQ_KERNEL_LINE) and not _kernel_ok(plan, matrix, kernel):
+    plan = wq.Plan(p, ks, slab=slab, need_mass=True, need_stiffness=True, coef_layout=layout_for(kernel))
+    if kernel in (wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_WS, wq.WQ_KERNEL_LINE, wq.WQ_KERNEL_ZLINE) and \
+            not _kernel_ok(plan, matrix, kernel):
         plan.close()
         pytest.skip(f"kernel {kernel} not available for this (d, p)")
     d_ctrl = torch.from_numpy(ctrl).cuda()
@@ -260,8 +266,8 @@ def test_kernels_agree(p, E):
     for mat in (MASS, STIFFNESS):
         _, c1, v1, _ = run_full(ks, ctrl, p, mat, wq.WQ_KERNEL_DIRECT)
         a = v1.cpu().numpy()
-        for k in (wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_WS, wq.WQ_KERNEL_LINE):
-            if k == wq.WQ_KERNEL_LINE and mat == MASS:
+        for k in (wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_WS, wq.WQ_KERNEL_LINE, wq.WQ_KERNEL_ZLINE):
+            if k in (wq.WQ_KERNEL_LINE, wq.WQ_KERNEL_ZLINE) and mat == MASS:
                 continue
             _, c2, v2, _ = run_full(ks, ctrl, p, mat, k)
             assert np.array_equal(c1.cpu().numpy(), c2.cpu().numpy())
@@ -292,3 +298,38 @@ def test_ws_sub_slab_launch(p):
     assert np.array_equal(rp.cpu().numpy(), rp0[r0:r0 + n + 1].cpu().numpy())
     assert np.array_equal(col.cpu().numpy(), col0[lo:hi].cpu().numpy())
     assert np.array_equal(val.cpu().numpy(), val0[lo:hi].cpu().numpy())
+
+
+@pytest.mark.parametrize("p,E,chunk", [(2, 9, 4000), (3, 8, 9000), (4, 7, 20000)])
+def test_zline_plane_ranges(p, E, chunk, monkeypatch):
+    """z-line kernel over plane sub-ranges (wq_form_host chunks: odd first task
+    point, few rows per line) and over slabs equals the whole-plan launch bit for bit."""
+    torch = _torch()
+    ks, ctrl = make_case(3, p, E, "annulus", 0.05)
+    rp0, col0, val0, info = run_full(ks, ctrl, p, STIFFNESS, wq.WQ_KERNEL_ZLINE)
+    monkeypatch.setenv("WQ_FORM_CHUNK_NNZ", str(chunk))
+    plan = wq.Plan(p, ks, need_mass=False, need_stiffness=True)
+    n, nnz = plan.info["n_rows_local"], plan.info["nnz_local"]
+    hrp = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+    hcol = torch.empty(nnz, dtype=torch.int32).pin_memory()
+    hval = torch.empty(nnz, dtype=torch.float64).pin_memory()
+    wq.wq_form_host(plan.h, STIFFNESS, torch.from_numpy(ctrl).pin_memory(), 0, hrp, hcol, hval)
+    plan.close()
+    assert np.array_equal(hrp.numpy(), rp0.cpu().numpy())
+    assert np.array_equal(hcol.numpy(), col0.cpu().numpy())
+    assert np.array_equal(hval.numpy(), val0.cpu().numpy())
+
+
+def test_zline_layout_guard():
+    """A plan holding the stiffness field in the z layout refuses the kernels
+    that read the standard layout (loud error, no silent fallback)."""
+    torch = _torch()
+    ks, ctrl = make_case(3, 3, 6)
+    plan = wq.Plan(3, ks)
+    plan.setup(torch.from_numpy(ctrl).cuda())
+    v = torch.empty(plan.info["nnz_local"], dtype=torch.float64, device="cuda")
+    for k in (wq.WQ_KERNEL_DIRECT, wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_WS, wq.WQ_KERNEL_LINE):
+        with pytest.raises(wq.WQError):
+            wq.wq_assemble(plan.h, STIFFNESS, v, None, kernel=k)
+    wq.wq_assemble(plan.h, MASS, v, None, kernel=wq.WQ_KERNEL_TILE)
+    plan.close()
