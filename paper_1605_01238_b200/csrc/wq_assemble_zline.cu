@@ -72,9 +72,16 @@ struct ZCfg {
     static constexpr int QX = BND ? QB : QI;         // box / table extent in directions 0, 1
     static constexpr int NF = 3 * QX;                // stage-A fibres (m, c1)
     static constexpr int NPASS = (NF + 31) / 32;
-    static constexpr int BOXD = (6 * QX * QX * 2 + 15) / 16 * 16;
-    static constexpr int YD = BND ? (3 * 2 * QX * K * 2 + 15) / 16 * 16 : 0;
-    static constexpr int TABD = 4 * QX * NP + 8 * QX + QX;  // B0v B0d B1v B1d, W0 W1, offsets (int pairs)
+    static constexpr int NPP = (NP + 1) & ~1;        // table row length (r pairs)
+    // Y blocks (m*2 + a2) of QX*K*2 doubles, 128-B aligned block stride plus a per-block shift that
+    // spreads the stage-B lanes (g, t0) over distinct bank groups
+    static constexpr int YB = (QX * K * 2 + 4 + 15) / 16 * 16;
+    __host__ __device__ static constexpr int yoff(int bi) { return bi * YB + (bi == 1 || bi == 3 ? 2 : (bi >= 4 ? 4 : 0)); }
+    static constexpr int YTOT = 6 * YB;
+    static constexpr int BOXD = BND ? (6 * QX * QX * 2 + 15) / 16 * 16
+                                    : ((6 * QX * QX * 2 > YTOT ? 6 * QX * QX * 2 : YTOT) + 15) / 16 * 16;
+    static constexpr int YD = BND ? YTOT : 0;
+    static constexpr int TABD = (4 * QX * NPP + 8 * QX + QX + 1) & ~1;  // T0, T1, W0, W1, offsets (ints); 16-B multiple
     static constexpr int W2D = NR * QB * 4;                  // doubles per consumer weight buffer
     __host__ __device__ static constexpr size_t al(size_t x) { return (x + 127) & ~(size_t)127; }
     static constexpr size_t O_BAR = 0;
@@ -135,7 +142,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
     constexpr int QX = CF::QX;
     constexpr int K = CF::K, QI = CF::QI, NP = CF::NP, COLS = CF::COLS, CPL = CF::CPL;
     constexpr int NR = CF::NR, NWC = CF::NWC, NWP = CF::NWP, NTS = CF::NTS, RING = CF::RING, NB = CF::NB;
-    constexpr int NF = CF::NF, BOXD = CF::BOXD;
+    constexpr int NF = CF::NF, BOXD = CF::BOXD, NPP = CF::NPP;
     constexpr int BS = wq_bstride(P);
     extern __shared__ __align__(128) unsigned char smb[];
     uint64_t *pfull = (uint64_t *)(smb + CF::O_BAR);  // [NWP][NB]
@@ -185,8 +192,10 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
         double *wbase = Boxes + wp * (NB * BOXD + CF::YD);
         double *Ybuf = wbase + NB * BOXD;  // BND only
         double *tab = Tabs + wp * CF::TABD;
-        double *B0v = tab, *B0d = B0v + QX * NP, *B1v = B0d + QX * NP, *B1d = B1v + QX * NP;
-        double *W0t = B1d + QX * NP, *W1t = W0t + 4 * QX;  // [c][f], f = a + 2b
+        // line tables: T0[sel][c0][NPP], T1[sel][c1][NPP] (sel 0: derivative, 1: value; r padded to
+        // NPP so that (r, r+1) pairs load as one 16-B word), W0t / W1t [c][f] (f = a + 2b)
+        double *T0 = tab, *T1 = T0 + 2 * QX * NPP;
+        double *W0t = T1 + 2 * QX * NPP, *W1t = W0t + 4 * QX;
         int *off0 = (int *)(W1t + 4 * QX), *off1 = off0 + QX;  // BND: staircase offsets span - jlo
         constexpr unsigned BOX_BYTES = 6 * QX * QX * 2 * 8;
         // task T = k * NTASK + tau of this warp (T = wp, wp + NWP, ...): item k, point pair tau; the
@@ -213,8 +222,12 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
         int64_t k = wp / NTASK;
         int tau = wp % NTASK;
         int64_t cur_item = -1;
-        const int fm = lane / K, fc = lane % K;  // stage B lanes (m, t0)
+        // stage B lanes (g, t0): g = 0, 1 -> b2 = 0, a2 = g (chains m = 0 and m = 1 summed in the lane);
+        // g = 2 -> b2 = 1 (chain m = 2, both a2).  Input blocks x = 0, 1 of Y and their tables:
+        const int fg = lane / K, fc = lane % K;
         const bool fl = lane < 3 * K;
+        const int ybx0 = fg == 0 ? 0 : (fg == 1 ? 1 : 4), ybx1 = fg == 0 ? 2 : (fg == 1 ? 3 : 5);  // Y blocks m*2+a2
+        const int tsel1 = fg == 2 ? 1 : 0;  // table of block x = 1: B1' for m = 1, B1 for m = 2
         int cq0 = QI, cq1 = QI;
         int use = 0;
         for (int64_t T = wp; T < n_tasks; T += NWP, ++use) {
@@ -229,11 +242,11 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 const DirView &v0 = a.v[0], &v1 = a.v[1];
                 __syncwarp();
                 if (BND) { cq0 = I.nq0; cq1 = I.nq1; }
-                for (int x = lane; x < QX * NP; x += 32) {
-                    const int c = x / NP, r = x % NP;
-                    const double2 b0 = c < cq0 ? __ldg((const double2 *)(v0.B + (int64_t)(I.ql0 + c) * BS) + r) : make_double2(0.0, 0.0);
-                    const double2 b1 = c < cq1 ? __ldg((const double2 *)(v1.B + (int64_t)(I.ql1 + c) * BS) + r) : make_double2(0.0, 0.0);
-                    B0v[x] = b0.x; B0d[x] = b0.y; B1v[x] = b1.x; B1d[x] = b1.y;
+                for (int x = lane; x < QX * NPP; x += 32) {
+                    const int c = x / NPP, r = x % NPP;
+                    const double2 b0 = c < cq0 && r < NP ? __ldg((const double2 *)(v0.B + (int64_t)(I.ql0 + c) * BS) + r) : make_double2(0.0, 0.0);
+                    const double2 b1 = c < cq1 && r < NP ? __ldg((const double2 *)(v1.B + (int64_t)(I.ql1 + c) * BS) + r) : make_double2(0.0, 0.0);
+                    T0[x] = b0.y; T0[QX * NPP + x] = b0.x; T1[x] = b1.y; T1[QX * NPP + x] = b1.x;
                 }
                 for (int x = lane; x < 4 * QX; x += 32) {
                     W0t[x] = x / 4 < cq0 ? __ldg(v0.W + (int64_t)I.i0 * v0.maxq * 4 + x) : 0.0;
@@ -254,7 +267,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             mbar_wait(&pfull[wp * NB + b], (NB == 2 ? use >> 1 : use) & 1);
             const double *bx = wbase + b * BOXD;  // [comp][c0][c1][pt]
             // ---------------- stage A: fibre (m, c1), both points, chains a2 = 0 (y0), 1 (y1)
-            // Y layout: [m][a2][c1][t0][pt]; interior: over the consumed box, BND: own buffer
+            // Y: block m*2+a2 at CF::yoff, [c1][t0][pt] inside; interior: over the consumed box
             double *Y = BND ? Ybuf : wbase + b * BOXD;
             #pragma unroll
             for (int pass = 0; pass < CF::NPASS; ++pass) {
@@ -271,26 +284,31 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     const int ka = m == 0 ? 2 : (m == 1 ? 4 : 5);
                     const int kb = m == 0 ? 0 : (m == 1 ? 1 : 2);
                     const int kc = m == 0 ? 1 : (m == 1 ? 3 : 4);
-                    const double w1a = W1t[c1 * 4 + (m == 1 ? 2 : 0)];  // w1^(0,b1)
-                    const double w1b = W1t[c1 * 4 + (m == 1 ? 3 : 1)];  // w1^(1,b1)
-                    const double *B0c = m == 0 ? B0d : B0v;
+                    const double2 w1p = *(const double2 *)(W1t + c1 * 4 + (m == 1 ? 2 : 0));  // w1^(0,b1), w1^(1,b1)
+                    const double *T0s = T0 + (m == 0 ? 0 : QX * NPP);
                     const int w0o = m == 0 ? 2 : 0;
                     auto plane = [&](int c0, auto O) {
                         constexpr int o0 = decltype(O)::value;
-                        const double w0a = W0t[c0 * 4 + w0o], w0b = W0t[c0 * 4 + w0o + 1];  // w0^(0,b0), w0^(1,b0)
-                        const double s1 = w0a * w1a, s2 = w0b * w1a, s3 = w0a * w1b;
+                        const double2 w0p = *(const double2 *)(W0t + c0 * 4 + w0o);  // w0^(0,b0), w0^(1,b0)
+                        const double s1 = w0p.x * w1p.x, s2 = w0p.y * w1p.x, s3 = w0p.x * w1p.y;
                         const double2 ca = *(const double2 *)(bx + ((ka * QX + c0) * QX + c1) * 2);
                         const double2 cb = *(const double2 *)(bx + ((kb * QX + c0) * QX + c1) * 2);
                         const double2 cc = *(const double2 *)(bx + ((kc * QX + c0) * QX + c1) * 2);
                         const double h1a = s1 * ca.x, h1b = s1 * ca.y;                                // l = 2
                         const double h0a = fma(s2, cb.x, s3 * cc.x), h0b = fma(s2, cb.y, s3 * cc.y);  // l = 0, 1
                         #pragma unroll
-                        for (int r = 0; r <= P; ++r) {
-                            const double bv = B0c[c0 * NP + r];
-                            y1[0][o0 + r] = fma(bv, h1a, y1[0][o0 + r]);
-                            y1[1][o0 + r] = fma(bv, h1b, y1[1][o0 + r]);
-                            y0[0][o0 + r] = fma(bv, h0a, y0[0][o0 + r]);
-                            y0[1][o0 + r] = fma(bv, h0b, y0[1][o0 + r]);
+                        for (int rr = 0; rr < NPP / 2; ++rr) {
+                            const double2 bp = *(const double2 *)(T0s + c0 * NPP + 2 * rr);
+                            #pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int r = 2 * rr + h;
+                                if (r > P) continue;
+                                const double bv = h ? bp.y : bp.x;
+                                y1[0][o0 + r] = fma(bv, h1a, y1[0][o0 + r]);
+                                y1[1][o0 + r] = fma(bv, h1b, y1[1][o0 + r]);
+                                y0[0][o0 + r] = fma(bv, h0a, y0[0][o0 + r]);
+                                y0[1][o0 + r] = fma(bv, h0b, y0[1][o0 + r]);
+                            }
                         }
                     };
                     if constexpr (BND) {
@@ -306,8 +324,8 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 }
                 if (!BND) __syncwarp();  // every lane has read the box: Y may overwrite it
                 if (fv) {
-                    double *Y0 = Y + ((m * 2 + 0) * QX + c1) * K * 2;
-                    double *Y1 = Y + ((m * 2 + 1) * QX + c1) * K * 2;
+                    double *Y0 = Y + CF::yoff(m * 2 + 0) + c1 * K * 2;
+                    double *Y1 = Y + CF::yoff(m * 2 + 1) + c1 * K * 2;
                     #pragma unroll
                     for (int t = 0; t < K; ++t) {
                         *(double2 *)(Y0 + t * 2) = make_double2(y0[0][t], y0[1][t]);
@@ -316,30 +334,37 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 }
             }
             __syncwarp();
-            // ---------------- stage B: lane (m, t0): g[a2][pt][t1]
+            // ---------------- stage B: lane (g, t0): acc[x][pt][t1] over the Y blocks x = 0, 1
             double g[2][2][K];
             #pragma unroll
-            for (int a2 = 0; a2 < 2; ++a2)
+            for (int x = 0; x < 2; ++x)
                 #pragma unroll
                 for (int pt = 0; pt < 2; ++pt)
                     #pragma unroll
-                    for (int t = 0; t < K; ++t) g[a2][pt][t] = 0.0;
+                    for (int t = 0; t < K; ++t) g[x][pt][t] = 0.0;
             if (fl) {
-                const int m = fm, t0 = fc;
-                const double *B1c = m == 1 ? B1d : B1v;
-                const double *Ya0 = Y + ((m * 2 + 0) * QX) * K * 2 + t0 * 2;
-                const double *Ya1 = Y + ((m * 2 + 1) * QX) * K * 2 + t0 * 2;
+                const int t0 = fc;
+                const double *Ya = Y + CF::yoff(ybx0) + t0 * 2;
+                const double *Yb = Y + CF::yoff(ybx1) + t0 * 2;
+                const double *Ta = T1 + QX * NPP, *Tb = T1 + tsel1 * QX * NPP;
                 auto point1 = [&](int c1, auto O) {
                     constexpr int o1 = decltype(O)::value;
-                    const double2 ya0 = *(const double2 *)(Ya0 + c1 * K * 2);
-                    const double2 ya1 = *(const double2 *)(Ya1 + c1 * K * 2);
+                    const double2 ya = *(const double2 *)(Ya + c1 * K * 2);
+                    const double2 yb = *(const double2 *)(Yb + c1 * K * 2);
                     #pragma unroll
-                    for (int r = 0; r <= P; ++r) {
-                        const double bv = B1c[c1 * NP + r];
-                        g[0][0][o1 + r] = fma(bv, ya0.x, g[0][0][o1 + r]);
-                        g[0][1][o1 + r] = fma(bv, ya0.y, g[0][1][o1 + r]);
-                        g[1][0][o1 + r] = fma(bv, ya1.x, g[1][0][o1 + r]);
-                        g[1][1][o1 + r] = fma(bv, ya1.y, g[1][1][o1 + r]);
+                    for (int rr = 0; rr < NPP / 2; ++rr) {
+                        const double2 pa = *(const double2 *)(Ta + c1 * NPP + 2 * rr);
+                        const double2 pb = *(const double2 *)(Tb + c1 * NPP + 2 * rr);
+                        #pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int r = 2 * rr + h;
+                            if (r > P) continue;
+                            const double ba = h ? pa.y : pa.x, bb = h ? pb.y : pb.x;
+                            g[0][0][o1 + r] = fma(ba, ya.x, g[0][0][o1 + r]);
+                            g[0][1][o1 + r] = fma(ba, ya.y, g[0][1][o1 + r]);
+                            g[1][0][o1 + r] = fma(bb, yb.x, g[1][0][o1 + r]);
+                            g[1][1][o1 + r] = fma(bb, yb.y, g[1][1][o1 + r]);
+                        }
                     }
                 };
                 if constexpr (BND) {
@@ -352,30 +377,22 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     });
                 }
             }
-            // G of the slot: lanes m = 1 (partial of b2 = 0) and m = 2 (b2 = 1) store, then lanes
-            // m = 0 add their part to the b2 = 0 partial in place
+            // G of the slot ([pt][b2][col] (a2 = 0, 1) pairs): lanes g = 0, 1 store the sum of their
+            // two chains as component a2 = g of b2 = 0; lanes g = 2 store both components of b2 = 1
             const uint32_t Tl = (uint32_t)T;
             const int slot_t = (int)(Tl % NTS);
             mbar_wait(&gempty[slot_t], ((Tl / NTS) & 1) ^ 1);
-            if (fl && fm != 0) {
-                const int b2 = fm == 2 ? 1 : 0, t0 = fc;
-                #pragma unroll
-                for (int pt = 0; pt < 2; ++pt) {
-                    double2 *Gd = Gs + ((slot_t * 2 + pt) * 2 + b2) * COLS + t0;
-                    #pragma unroll
-                    for (int t = 0; t < K; ++t) Gd[K * t] = make_double2(g[0][pt][t], g[1][pt][t]);
-                }
-            }
-            __syncwarp();
-            if (fl && fm == 0) {
+            if (fl) {
                 const int t0 = fc;
+                const double sum1 = fg < 2 ? 1.0 : 0.0;
+                const int b2 = fg == 2 ? 1 : 0, comp = fg == 1 ? 1 : 0;
                 #pragma unroll
                 for (int pt = 0; pt < 2; ++pt) {
-                    double2 *Gd = Gs + ((slot_t * 2 + pt) * 2 + 0) * COLS + t0;
+                    double *Gd = (double *)(Gs + ((slot_t * 2 + pt) * 2 + b2) * COLS + t0) + comp;
                     #pragma unroll
                     for (int t = 0; t < K; ++t) {
-                        const double2 o = Gd[K * t];
-                        Gd[K * t] = make_double2(g[0][pt][t] + o.x, g[1][pt][t] + o.y);
+                        Gd[2 * K * t] = fma(g[1][pt][t], sum1, g[0][pt][t]);
+                        if (fg == 2) Gd[2 * K * t + 1] = g[1][pt][t];
                     }
                 }
             }
