@@ -245,17 +245,20 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
             const int64_t E = P->dir[l].E, n = P->dir[l].n;
             return i >= p + 1 && i <= n - p - 2 && host_qhi(i, E, p) - host_qlo(i, E, p) + 1 == 2 * p + 1;
         };
+        auto uniz = [&](int l, int64_t i) { return i >= 2 * p && i <= P->dir[l].n - 1 - 2 * p; };
         for (int64_t i1 = 0; i1 < n1; ++i1)
-            for (int64_t i0 = 0; i0 < n0; ++i0)
-                (interz(0, i0) && interz(1, i1) ? P->zlines_int : P->zlines_bnd).push_back((int32_t)(i0 + n0 * i1));
-        const size_t zl = sizeof(int32_t) * (P->zlines_int.size() + P->zlines_bnd.size());
+            for (int64_t i0 = 0; i0 < n0; ++i0) {
+                const int32_t line = (int32_t)(i0 + n0 * i1);
+                if (!(interz(0, i0) && interz(1, i1))) P->zlines_bnd.push_back(line);
+                else (uniz(0, i0) && uniz(1, i1) ? P->zlines_uni : P->zlines_int).push_back(line);
+            }
+        std::vector<int32_t> all(P->zlines_uni);
+        all.insert(all.end(), P->zlines_int.begin(), P->zlines_int.end());
+        all.insert(all.end(), P->zlines_bnd.begin(), P->zlines_bnd.end());
+        const size_t zl = sizeof(int32_t) * (all.size() > 0 ? all.size() : 1);
         ce = cudaMalloc((void **)&P->zlines_dev, zl);
         if (ce != cudaSuccess) { P->zlines_dev = nullptr; wq_plan_destroy(P); return fail(WQ_ENOMEM, "z line lists"); }
-        if (!P->zlines_int.empty())
-            cudaMemcpy(P->zlines_dev, P->zlines_int.data(), sizeof(int32_t) * P->zlines_int.size(), cudaMemcpyHostToDevice);
-        if (!P->zlines_bnd.empty())
-            cudaMemcpy(P->zlines_dev + P->zlines_int.size(), P->zlines_bnd.data(),
-                       sizeof(int32_t) * P->zlines_bnd.size(), cudaMemcpyHostToDevice);
+        if (!all.empty()) cudaMemcpy(P->zlines_dev, all.data(), sizeof(int32_t) * all.size(), cudaMemcpyHostToDevice);
         cbytes += zl;
     }
     // row lines of the slab, split for the line kernel (interior in directions 2 and 3) vs the rest
@@ -354,10 +357,11 @@ static wq_status assemble_range(wq_plan_s *P, int matrix, wq_kernel kernel, doub
         if (kernel != WQ_KERNEL_AUTO && kernel != WQ_KERNEL_ZLINE)
             return fail(WQ_EINVAL, "plan holds the stiffness coefficients in the z layout: only WQ_KERNEL_ZLINE applies "
                                    "(create the plan with coef_layout = 1 for the other kernels)");
-        const int64_t ni = (int64_t)P->zlines_int.size(), nb = (int64_t)P->zlines_bnd.size();
-        wq_status st = launch_assemble_zline(P, false, P->zlines_dev, ni, pl_lo, pl_hi, val, col, val_base, s);
-        if (!st && nb > 0)
-            st = launch_assemble_zline(P, true, P->zlines_dev + ni, nb, pl_lo, pl_hi, val, col, val_base, s);
+        const int64_t nu = (int64_t)P->zlines_uni.size(), ni = (int64_t)P->zlines_int.size(),
+                      nb = (int64_t)P->zlines_bnd.size();
+        wq_status st = launch_assemble_zline(P, 0, P->zlines_dev, nu, pl_lo, pl_hi, val, col, val_base, s);
+        if (!st) st = launch_assemble_zline(P, 1, P->zlines_dev + nu, ni, pl_lo, pl_hi, val, col, val_base, s);
+        if (!st) st = launch_assemble_zline(P, 2, P->zlines_dev + nu + ni, nb, pl_lo, pl_hi, val, col, val_base, s);
         return st;
     }
     if (kernel == WQ_KERNEL_ZLINE) return fail(WQ_EINVAL, "z-line kernel not available for this plan (matrix, d, p, layout)");

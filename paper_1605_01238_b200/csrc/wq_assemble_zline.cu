@@ -33,6 +33,11 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdlib>
+#include <cstring>
+#include <cstdio>
+#include <cmath>
+#include <algorithm>
+#include <vector>
 #include "wq_rows.cuh"
 #include "wq_dev.cuh"
 
@@ -114,6 +119,16 @@ struct ZArgs {
     int64_t val_base;
 };
 
+// Interior rules of a uniform mesh (translation invariant: every interior row i has the same
+// weights w(c) on its points c = 0..2p, and the basis values at its points depend only on whether
+// the point is a span midpoint (c even) or a knot (c odd), Remark 1).  Verified against the
+// device-computed rules of every interior row before use (z_fetch_uniform).
+#define WQ_ZPMAX 4
+struct __align__(16) ZUni {
+    double w[3][2 * WQ_ZPMAX + 1][4];  // [dir][c][f], f = a + 2b
+    double b[3][2][WQ_ZPMAX + 1][2];   // [dir][c & 1][r][value, derivative] of functions span..span+p
+};
+
 struct ZItem {
     int i0, i1, ql0, ql1, jl0, jl1, nq0, nq1, ni0, ni1;
 };
@@ -135,9 +150,11 @@ __device__ __forceinline__ ZItem z_item(const ZArgs &a, int64_t it) {
     return I;
 }
 
-template <int P, bool BND>
+// PU: the line's producer tables from the uniform rules (lines with i0, i1 in [2p, n-1-2p]);
+// CU: rows i2 in [2p, n2-1-2p] take the uniform rules in the consumer
+template <int P, bool BND, bool PU, bool CU>
 __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
-    k_zline(const __grid_constant__ CUtensorMap tm, ZArgs a) {
+    k_zline(const __grid_constant__ CUtensorMap tm, ZArgs a, const __grid_constant__ ZUni u) {
     using CF = ZCfg<P, BND>;
     constexpr int QX = CF::QX;
     constexpr int K = CF::K, QI = CF::QI, NP = CF::NP, COLS = CF::COLS, CPL = CF::CPL;
@@ -228,6 +245,26 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
         const bool fl = lane < 3 * K;
         const int ybx0 = fg == 0 ? 0 : (fg == 1 ? 1 : 4), ybx1 = fg == 0 ? 2 : (fg == 1 ? 3 : 5);  // Y blocks m*2+a2
         const int tsel1 = fg == 2 ? 1 : 0;  // table of block x = 1: B1' for m = 1, B1 for m = 2
+        // PU: this lane's selections of the uniform tables (stage A: family b0 = [m == 0], weights of
+        // its c1; stage B: table of block x = 1)
+        double b0s[2][NP], w0s[QI][2], b1x[2][NP], w1u0 = 0.0, w1u1 = 0.0;
+        if constexpr (PU) {
+            const int m = lane / QX < 3 ? lane / QX : 2, c1 = lane % QX;
+            #pragma unroll
+            for (int par = 0; par < 2; ++par)
+                #pragma unroll
+                for (int r = 0; r <= P; ++r) {
+                    b0s[par][r] = u.b[0][par][r][m == 0 ? 1 : 0];
+                    b1x[par][r] = u.b[1][par][r][tsel1 ? 0 : 1];
+                }
+            #pragma unroll
+            for (int c = 0; c < QI; ++c) {
+                w0s[c][0] = u.w[0][c][m == 0 ? 2 : 0];
+                w0s[c][1] = u.w[0][c][m == 0 ? 3 : 1];
+            }
+            w1u0 = u.w[1][c1][m == 1 ? 2 : 0];
+            w1u1 = u.w[1][c1][m == 1 ? 3 : 1];
+        }
         int cq0 = QI, cq1 = QI;
         int use = 0;
         for (int64_t T = wp; T < n_tasks; T += NWP, ++use) {
@@ -236,7 +273,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 tau += NWP;
                 while (tau >= NTASK) { tau -= NTASK; ++k; }
             }
-            if (k != cur_item) {
+            if (!PU && k != cur_item) {
                 cur_item = k;
                 const ZItem I = z_item(a, first + k * step);
                 const DirView &v0 = a.v[0], &v1 = a.v[1];
@@ -284,12 +321,14 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     const int ka = m == 0 ? 2 : (m == 1 ? 4 : 5);
                     const int kb = m == 0 ? 0 : (m == 1 ? 1 : 2);
                     const int kc = m == 0 ? 1 : (m == 1 ? 3 : 4);
-                    const double2 w1p = *(const double2 *)(W1t + c1 * 4 + (m == 1 ? 2 : 0));  // w1^(0,b1), w1^(1,b1)
+                    const double2 w1p = PU ? make_double2(w1u0, w1u1)
+                                           : *(const double2 *)(W1t + c1 * 4 + (m == 1 ? 2 : 0));  // w1^(0,b1), w1^(1,b1)
                     const double *T0s = T0 + (m == 0 ? 0 : QX * NPP);
                     const int w0o = m == 0 ? 2 : 0;
                     auto plane = [&](int c0, auto O) {
                         constexpr int o0 = decltype(O)::value;
-                        const double2 w0p = *(const double2 *)(W0t + c0 * 4 + w0o);  // w0^(0,b0), w0^(1,b0)
+                        const double2 w0p = PU ? make_double2(w0s[c0 % QI][0], w0s[c0 % QI][1])
+                                               : *(const double2 *)(W0t + c0 * 4 + w0o);  // w0^(0,b0), w0^(1,b0)
                         const double s1 = w0p.x * w1p.x, s2 = w0p.y * w1p.x, s3 = w0p.x * w1p.y;
                         const double2 ca = *(const double2 *)(bx + ((ka * QX + c0) * QX + c1) * 2);
                         const double2 cb = *(const double2 *)(bx + ((kb * QX + c0) * QX + c1) * 2);
@@ -298,12 +337,12 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                         const double h0a = fma(s2, cb.x, s3 * cc.x), h0b = fma(s2, cb.y, s3 * cc.y);  // l = 0, 1
                         #pragma unroll
                         for (int rr = 0; rr < NPP / 2; ++rr) {
-                            const double2 bp = *(const double2 *)(T0s + c0 * NPP + 2 * rr);
+                            const double2 bp = PU ? make_double2(0.0, 0.0) : *(const double2 *)(T0s + c0 * NPP + 2 * rr);
                             #pragma unroll
                             for (int h = 0; h < 2; ++h) {
                                 const int r = 2 * rr + h;
                                 if (r > P) continue;
-                                const double bv = h ? bp.y : bp.x;
+                                const double bv = PU ? b0s[c0 & 1][r] : (h ? bp.y : bp.x);
                                 y1[0][o0 + r] = fma(bv, h1a, y1[0][o0 + r]);
                                 y1[1][o0 + r] = fma(bv, h1b, y1[1][o0 + r]);
                                 y0[0][o0 + r] = fma(bv, h0a, y0[0][o0 + r]);
@@ -353,13 +392,14 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     const double2 yb = *(const double2 *)(Yb + c1 * K * 2);
                     #pragma unroll
                     for (int rr = 0; rr < NPP / 2; ++rr) {
-                        const double2 pa = *(const double2 *)(Ta + c1 * NPP + 2 * rr);
-                        const double2 pb = *(const double2 *)(Tb + c1 * NPP + 2 * rr);
+                        const double2 pa = PU ? make_double2(0.0, 0.0) : *(const double2 *)(Ta + c1 * NPP + 2 * rr);
+                        const double2 pb = PU ? make_double2(0.0, 0.0) : *(const double2 *)(Tb + c1 * NPP + 2 * rr);
                         #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const int r = 2 * rr + h;
                             if (r > P) continue;
-                            const double ba = h ? pa.y : pa.x, bb = h ? pb.y : pb.x;
+                            const double ba = PU ? u.b[1][c1 & 1][r][0] : (h ? pa.y : pa.x);
+                            const double bb = PU ? b1x[c1 & 1][r] : (h ? pb.y : pb.x);
                             g[0][0][o1 + r] = fma(ba, ya.x, g[0][0][o1 + r]);
                             g[0][1][o1 + r] = fma(ba, ya.y, g[0][1][o1 + r]);
                             g[1][0][o1 + r] = fma(bb, yb.x, g[1][0][o1 + r]);
@@ -382,17 +422,20 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             const uint32_t Tl = (uint32_t)T;
             const int slot_t = (int)(Tl % NTS);
             mbar_wait(&gempty[slot_t], ((Tl / NTS) & 1) ^ 1);
-            if (fl) {
+            {
+                // lanes g = 0 receive the a2 = 1 sums of lanes g = 1 and store (a2 = 0, a2 = 1) pairs of
+                // b2 = 0; lanes g = 2 store their pairs of b2 = 1 (one 16-B store per lane and entry)
                 const int t0 = fc;
                 const double sum1 = fg < 2 ? 1.0 : 0.0;
-                const int b2 = fg == 2 ? 1 : 0, comp = fg == 1 ? 1 : 0;
+                const int b2 = fg == 2 ? 1 : 0;
                 #pragma unroll
                 for (int pt = 0; pt < 2; ++pt) {
-                    double *Gd = (double *)(Gs + ((slot_t * 2 + pt) * 2 + b2) * COLS + t0) + comp;
+                    double2 *Gd = Gs + ((slot_t * 2 + pt) * 2 + b2) * COLS + t0;
                     #pragma unroll
                     for (int t = 0; t < K; ++t) {
-                        Gd[2 * K * t] = fma(g[1][pt][t], sum1, g[0][pt][t]);
-                        if (fg == 2) Gd[2 * K * t + 1] = g[1][pt][t];
+                        const double v = fma(g[1][pt][t], sum1, g[0][pt][t]);
+                        const double o = __shfl_down_sync(0xffffffffu, v, K);
+                        if (fl && fg != 1) Gd[K * t] = make_double2(v, fg == 0 ? o : g[1][pt][t]);
                     }
                 }
             }
@@ -486,13 +529,16 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     #pragma unroll
                     for (int t = 0; t < K; ++t) acc[k][j][t] = 0.0;
             auto slot_of = [&](int q) { return (int)((Tbase * 2 + (uint32_t)q) % RING); };
-            const bool interior = nr == NR && i2b + r0 >= P + 1 && i2b + r0 + NR - 1 <= (int)v2.n - P - 2;
+            // fast path: a full batch of rows with the interior staircase; with CU only rows whose
+            // rules are the uniform ones (the others go through the generic path)
+            const int rlo = CU ? 2 * P : P + 1, rhi = CU ? (int)v2.n - 1 - 2 * P : (int)v2.n - P - 2;
+            const bool interior = nr == NR && i2b + r0 >= rlo && i2b + r0 + NR - 1 <= rhi;
             if (interior) {
                 const int slot0 = slot_of(qlo2[r0]);
                 constexpr int UW = 2 * (NR - 1) + 2 * P + 1;
                 #pragma unroll
-                for (int u = 0; u < UW; ++u) {
-                    int slot = slot0 + u;
+                for (int u_ = 0; u_ < UW; ++u_) {
+                    int slot = slot0 + u_;
                     if (slot >= RING) slot -= RING;
                     double2 g0[CPL], g1[CPL];
                     #pragma unroll
@@ -502,14 +548,16 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     }
                     double2 bb[NP];
                     #pragma unroll
-                    for (int r = 0; r <= P; ++r) bb[r] = B2r[slot * NP + r];
+                    for (int r = 0; r <= P; ++r)
+                        bb[r] = CU ? make_double2(u.b[2][u_ & 1][r][0], u.b[2][u_ & 1][r][1]) : B2r[slot * NP + r];
                     #pragma unroll
                     for (int k = 0; k < NR; ++k) {
-                        if (u >= 2 * k && u <= 2 * k + 2 * P) {
-                            const int c = u - 2 * k;
+                        if (u_ >= 2 * k && u_ <= 2 * k + 2 * P) {
+                            const int c = u_ - 2 * k;
                             const int o0 = (c + 1) / 2;
                             const double2 *wr = W2w + (k * mq2 + c) * 2;
-                            const double2 wA = wr[0], wB = wr[1];
+                            const double2 wA = CU ? make_double2(u.w[2][c][0], u.w[2][c][1]) : wr[0];
+                            const double2 wB = CU ? make_double2(u.w[2][c][2], u.w[2][c][3]) : wr[1];
                             #pragma unroll
                             for (int j = 0; j < CPL; ++j) {
                                 const double u0 = fma(wA.x, g0[j].x, wA.y * g0[j].y);
@@ -527,12 +575,15 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     if (k >= nr) break;
                     const int r = r0 + k;
                     const int qb = qlo2[r], nq = qlen2[r], jl = jlo2[r];
+                    // an interior row takes the uniform rules here too, so that its values do not
+                    // depend on how the rows were batched (bit-identical to the interior path)
+                    const bool ru = CU && i2b + r >= 2 * P && i2b + r <= (int)v2.n - 1 - 2 * P;
                     #pragma unroll 1
                     for (int c = 0; c < nq; ++c) {
                         const int q = qb + c;
                         const int slot = slot_of(q);
-                        const double2 *bp = B2r + slot * NP;
-                        const double2 *wr = W2w + (k * mq2 + c) * 2;
+                        const double2 *bp = ru ? (const double2 *)&u.b[2][c & 1][0][0] : B2r + slot * NP;
+                        const double2 *wr = ru ? (const double2 *)&u.w[2][c][0] : W2w + (k * mq2 + c) * 2;
                         const double2 wA = wr[0], wB = wr[1];
                         double u0[CPL], u1[CPL];
                         #pragma unroll
@@ -635,9 +686,9 @@ int z_num_sms(int dev) {
     return n > 0 ? n : 148;
 }
 
-template <int P, bool BND>
+template <int P, bool BND, bool PU, bool CU>
 wq_status launch_zline_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, int64_t pl_lo, int64_t pl_hi,
-                         double *val, int32_t *col, int64_t val_base, cudaStream_t s) {
+                         double *val, int32_t *col, int64_t val_base, const ZUni &un, cudaStream_t s) {
     using CF = ZCfg<P, BND>;
     if constexpr (!CF::FITS) {
         wq_set_error("z-line kernel not configured for this degree");
@@ -677,10 +728,10 @@ wq_status launch_zline_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, i
             wq_set_error("z-line kernel: direction-2 tables exceed shared memory");
             return WQ_EINVAL;
         }
-        cudaFuncSetAttribute(k_zline<P, BND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_zline<P, BND, PU, CU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int64_t grid = z_num_sms(Pl->device);
         if (grid > n_lines) grid = n_lines;
-        k_zline<P, BND><<<(unsigned)grid, CF::NT, smem, s>>>(m, a);
+        k_zline<P, BND, PU, CU><<<(unsigned)grid, CF::NT, smem, s>>>(m, a, un);
         wq_count_launches(1);
         return wq_cuda_status(cudaGetLastError(), "z-line assembly kernel");
     }
@@ -705,19 +756,92 @@ bool zline_supported_p(int d, int p, const int64_t *n, const int32_t *maxq, int6
     return fits_z<false>(p, n2l, nq2l) && fits_z<true>(p, n2l, nq2l);
 }
 
-wq_status launch_assemble_zline(wq_plan_s *P, bool bnd, const int32_t *lines, int64_t n_lines, int64_t pl_lo,
+namespace {
+// Uniform-mesh check of the device-computed rules (once per plan: the rules are a pure function of
+// the plan's knots and degree): every interior row of every direction must carry the same weights
+// on its points c = 0..2p and the same basis values at points of the same parity, to 1e-13 relative
+// (uniform knots k/E agree to ~3e-14 because of the FP64 rounding of the knots, exactly when E is a
+// power of two).  On success the representative row n/2 fills the kernel's uniform tables.
+#define ZFAIL(...) do { if (getenv("WQ_DEBUG")) { fprintf(stderr, "[wq] uniform rules rejected: " __VA_ARGS__); fprintf(stderr, "\n"); } return false; } while (0)
+bool z_fetch_uniform(wq_plan_s *P, cudaStream_t s, ZUni &U) {
+    const int p = P->p, K = 2 * p + 1, bs = wq_bstride(p);
+    if (p > WQ_ZPMAX || cudaStreamSynchronize(s) != cudaSuccess) ZFAIL("p or stream");
+    memset(&U, 0, sizeof(U));
+    for (int l = 0; l < 3; ++l) {
+        const DirView &v = P->dir[l];
+        const int64_t n = v.n, nq = v.nq;
+        if (n - 1 - 2 * p < 2 * p) ZFAIL("dir %d: no row with uniform rules", l);
+        std::vector<double> W((size_t)n * v.maxq * 4), B((size_t)nq * bs);
+        std::vector<int32_t> qlo(n), qlen(n), jlo(n), span(nq);
+        if (cudaMemcpy(W.data(), v.W, W.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(B.data(), v.B, B.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(qlo.data(), v.qlo, n * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(qlen.data(), v.qlen, n * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(jlo.data(), v.jlo, n * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(span.data(), v.span, nq * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return false;
+        const int64_t ir = n / 2;  // in [2p, n-1-2p]
+        const double *Wr = W.data() + (size_t)ir * v.maxq * 4;
+        double wsc[4] = {0, 0, 0, 0}, bsc[2] = {0, 0};
+        for (int c = 0; c < K; ++c)
+            for (int f = 0; f < 4; ++f) wsc[f] = std::max(wsc[f], std::fabs(Wr[c * 4 + f]));
+        for (int par = 0; par < 2; ++par)
+            for (int r = 0; r <= p; ++r)
+                for (int h = 0; h < 2; ++h) bsc[h] = std::max(bsc[h], std::fabs(B[(size_t)(qlo[ir] + par) * bs + 2 * r + h]));
+        const double tol = 1e-13;
+        for (int64_t i = 2 * p; i <= n - 1 - 2 * p; ++i) {
+            if (qlen[i] != K) ZFAIL("dir %d row %lld: #Q %d", l, (long long)i, qlen[i]);
+            const double *Wi = W.data() + (size_t)i * v.maxq * 4;
+            for (int c = 0; c < K; ++c) {
+                if (span[qlo[i] + c] - jlo[i] != (c + 1) / 2) ZFAIL("dir %d row %lld: staircase", l, (long long)i);
+                for (int f = 0; f < 4; ++f)
+                    if (std::fabs(Wi[c * 4 + f] - Wr[c * 4 + f]) > tol * wsc[f])
+                        ZFAIL("dir %d row %lld c %d f %d: w %.17g vs %.17g", l, (long long)i, c, f, Wi[c * 4 + f], Wr[c * 4 + f]);
+                for (int r = 0; r <= p; ++r)
+                    for (int h = 0; h < 2; ++h)
+                        if (std::fabs(B[(size_t)(qlo[i] + c) * bs + 2 * r + h] -
+                                      B[(size_t)(qlo[ir] + (c & 1)) * bs + 2 * r + h]) > tol * bsc[h])
+                            ZFAIL("dir %d row %lld c %d r %d h %d: B %.17g vs %.17g", l, (long long)i, c, r, h,
+                                  B[(size_t)(qlo[i] + c) * bs + 2 * r + h], B[(size_t)(qlo[ir] + (c & 1)) * bs + 2 * r + h]);
+            }
+        }
+        for (int c = 0; c < K; ++c)
+            for (int f = 0; f < 4; ++f) U.w[l][c][f] = Wr[c * 4 + f];
+        for (int par = 0; par < 2; ++par)
+            for (int r = 0; r <= p; ++r)
+                for (int h = 0; h < 2; ++h) U.b[l][par][r][h] = B[(size_t)(qlo[ir] + par) * bs + 2 * r + h];
+    }
+    return true;
+}
+}  // namespace
+
+wq_status launch_assemble_zline(wq_plan_s *P, int cls, const int32_t *lines, int64_t n_lines, int64_t pl_lo,
                                 int64_t pl_hi, double *val, int32_t *col, int64_t val_base, cudaStream_t s) {
     if (!P->coefz) {
         wq_set_error("z-line kernel needs the z-layout coefficient field");
         return WQ_EINVAL;
     }
-    switch (P->p * 2 + (bnd ? 1 : 0)) {
-    case 4: return launch_zline_p<2, false>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, s);
-    case 5: return launch_zline_p<2, true>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, s);
-    case 6: return launch_zline_p<3, false>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, s);
-    case 7: return launch_zline_p<3, true>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, s);
-    case 8: return launch_zline_p<4, false>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, s);
-    case 9: return launch_zline_p<4, true>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, s);
+    if (n_lines <= 0) return WQ_OK;
+    static_assert(sizeof(ZUni) <= sizeof(P->zuni_buf), "uniform table buffer");
+    if (P->zuni_state == 0) {
+        ZUni U;
+        const bool ok = !getenv("WQ_ZLINE_NO_UNIFORM") && z_fetch_uniform(P, s, U);
+        P->zuni_state = ok ? 1 : -1;
+        if (ok) memcpy(P->zuni_buf, &U, sizeof(U));
+    }
+    ZUni U;
+    memcpy(&U, P->zuni_buf, sizeof(U));
+    const bool cu = P->zuni_state == 1;
+    const bool bnd = cls == 2, pu = cls == 0 && cu;
+    switch (P->p * 8 + (bnd ? 4 : 0) + (pu ? 2 : 0) + (cu ? 1 : 0)) {
+#define WQ_ZL(PP, B, PUU, CUU) \
+    case PP * 8 + (B ? 4 : 0) + (PUU ? 2 : 0) + (CUU ? 1 : 0): \
+        return launch_zline_p<PP, B, PUU, CUU>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, U, s);
+#define WQ_ZLP(PP) WQ_ZL(PP, false, false, false) WQ_ZL(PP, false, false, true) WQ_ZL(PP, false, true, true) \
+                   WQ_ZL(PP, true, false, false) WQ_ZL(PP, true, false, true)
+        WQ_ZLP(2) WQ_ZLP(3) WQ_ZLP(4)
+#undef WQ_ZLP
+#undef WQ_ZL
     }
     wq_set_error("z-line kernel not available for this degree");
     return WQ_EINVAL;

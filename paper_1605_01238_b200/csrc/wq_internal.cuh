@@ -79,8 +79,12 @@ struct wq_plan_s {
     double *coefz;
     int64_t zld, zcs;              // row length along q_3, doubles per component
     int comp_mass;                 // component index of c in coef
-    std::vector<int32_t> zlines_int, zlines_bnd;
+    std::vector<int32_t> zlines_uni, zlines_int, zlines_bnd;
     int32_t *zlines_dev;
+    // uniform-mesh interior rules for the z-line kernel (fetched once per plan at the first
+    // assembly): 0 not checked yet, 1 usable (zuni_buf holds them), -1 not uniform
+    int zuni_state;
+    double zuni_buf[3 * 9 * 4 + 3 * 2 * 5 * 2];
 };
 
 // host helpers
@@ -116,7 +120,9 @@ bool line_supported(const wq_plan_s *P, int matrix, bool bnd);
 // z-line kernel (stiffness, d = 3, coefficients in the z layout) over a list of lines (i1 + n1 * i2)
 // and the planes [pl_lo, pl_hi) of the slab
 bool zline_supported_p(int d, int p, const int64_t *n, const int32_t *maxq, int64_t n2l, int64_t nq2l);
-wq_status launch_assemble_zline(wq_plan_s *P, bool bnd, const int32_t *lines, int64_t n_lines, int64_t pl_lo,
+// cls: 0 lines with i1, i2 in [2p, n-1-2p] (uniform rules possible), 1 other lines interior in
+// directions 1 and 2, 2 lines touching a boundary span
+wq_status launch_assemble_zline(wq_plan_s *P, int cls, const int32_t *lines, int64_t n_lines, int64_t pl_lo,
                                 int64_t pl_hi, double *val, int32_t *col, int64_t val_base, cudaStream_t s);
 // tile kernel over an explicit list of lines of the plan's slab
 wq_status launch_assemble_tile_list(wq_plan_s *P, int matrix, const int32_t *lines, int64_t n_lines, double *val,
