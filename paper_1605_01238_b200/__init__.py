@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwq.so")
+LIB_PATH = os.environ.get("WQ_LIB_DEBUG_PATH") or os.path.join(_HERE, "libwq.so")  # override: debug builds (tools/)
 
 WQ_OK, WQ_EINVAL, WQ_EKNOTS, WQ_ESINGULAR, WQ_EGEOMETRY, WQ_ENOMEM, WQ_ECUDA, WQ_ERANGE = range(8)
 WQ_MASS, WQ_STIFFNESS = 0, 1

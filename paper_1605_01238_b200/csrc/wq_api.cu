@@ -252,13 +252,52 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
                 if (!(interz(0, i0) && interz(1, i1))) P->zlines_bnd.push_back(line);
                 else (uniz(0, i0) && uniz(1, i1) ? P->zlines_uni : P->zlines_int).push_back(line);
             }
+        // boundary lines sorted by their row types (the kernel runs one unrolled staircase per type pair)
+        auto ztype = [&](int l, int64_t i) -> int64_t {
+            const int64_t n = P->dir[l].n;
+            return i <= p ? i + 1 : (i >= n - 1 - p ? n - 1 - i + p + 2 : 0);
+        };
+        std::stable_sort(P->zlines_bnd.begin(), P->zlines_bnd.end(), [&](int32_t x, int32_t y) {
+            const int64_t kx = ztype(0, x % n0) * 64 + ztype(1, x / n0), ky = ztype(0, y % n0) * 64 + ztype(1, y / n0);
+            return kx < ky;
+        });
         std::vector<int32_t> all(P->zlines_uni);
         all.insert(all.end(), P->zlines_int.begin(), P->zlines_int.end());
         all.insert(all.end(), P->zlines_bnd.begin(), P->zlines_bnd.end());
-        const size_t zl = sizeof(int32_t) * (all.size() > 0 ? all.size() : 1);
+        // contiguous chunks of the sorted boundary lines with about equal producer work per CTA
+        // (stage A: fibre passes x #Q_0 points, stage B: #Q_1 points, per task)
+        int nsm = 0;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P->device);
+        const int64_t G = std::min<int64_t>(nsm > 0 ? nsm : 148, (int64_t)P->zlines_bnd.size());
+        std::vector<int32_t> bounds;
+        if (G > 0) {
+            std::vector<double> cum(P->zlines_bnd.size() + 1, 0.0);
+            for (size_t k = 0; k < P->zlines_bnd.size(); ++k) {
+                const int32_t line = P->zlines_bnd[k];
+                const int64_t i0 = line % n0, i1 = line / n0;
+                const double q0 = (double)(host_qhi(i0, P->dir[0].E, p) - host_qlo(i0, P->dir[0].E, p) + 1);
+                const double q1 = (double)(host_qhi(i1, P->dir[1].E, p) - host_qlo(i1, P->dir[1].E, p) + 1);
+                const double passes = std::ceil(3.0 * q1 / 32.0);
+                cum[k + 1] = cum[k] + passes * q0 + q1;
+            }
+            bounds.resize(G + 1);
+            size_t k = 0;
+            for (int64_t c = 0; c <= G; ++c) {
+                const double target = cum.back() * (double)c / (double)G;
+                while (k < P->zlines_bnd.size() && cum[k] < target) ++k;
+                bounds[c] = (int32_t)(c == G ? P->zlines_bnd.size() : k);
+            }
+        }
+        P->zbounds_n = G;
+        const size_t zl = sizeof(int32_t) * (all.size() + bounds.size() + 1);
         ce = cudaMalloc((void **)&P->zlines_dev, zl);
         if (ce != cudaSuccess) { P->zlines_dev = nullptr; wq_plan_destroy(P); return fail(WQ_ENOMEM, "z line lists"); }
         if (!all.empty()) cudaMemcpy(P->zlines_dev, all.data(), sizeof(int32_t) * all.size(), cudaMemcpyHostToDevice);
+        P->zbounds_dev = nullptr;
+        if (!bounds.empty()) {
+            P->zbounds_dev = P->zlines_dev + all.size();
+            cudaMemcpy(P->zbounds_dev, bounds.data(), sizeof(int32_t) * bounds.size(), cudaMemcpyHostToDevice);
+        }
         cbytes += zl;
     }
     // row lines of the slab, split for the line kernel (interior in directions 2 and 3) vs the rest

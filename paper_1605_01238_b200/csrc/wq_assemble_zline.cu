@@ -105,6 +105,42 @@ struct ZCfg {
                                  SMEM + d2_bytes(64, 2 * 64 + 2 * P + 1) <= 227 * 1024;
 };
 
+// Row types of one direction (n >= 2p+3 rows, n_EL >= p+2): 0 interior (p+1 <= i <= n-p-2), 1..p+1
+// left boundary row i = t-1, p+2..2p+2 right boundary row i = n-1-(t-p-2).  Each type has a fixed
+// #Q and staircase offset of its point c (first nonzero function - jlo), from the point grid of
+// Remark 1 (reading R1):
+//   interior      [0, 1,1, 2,2, .., p,p]                      #Q = 2p+1
+//   left i        [0]*(p+1) + [1,1, .., i,i]                   #Q = p+1+2i
+//   right i'      [0] + [1,1, .., i'-1,i'-1] + [i'] + [i']*(p+1)  #Q = p+1+2i'
+// (verified against the device tables of every row by z_check_types before the first launch)
+template <int P>
+struct ZTy {
+    static constexpr int NTY = 2 * P + 3;
+    __host__ __device__ static constexpr int nq(int t) {
+        return t == 0 ? 2 * P + 1 : (t <= P + 1 ? P + 1 + 2 * (t - 1) : P + 1 + 2 * (t - P - 2));
+    }
+    __host__ __device__ static constexpr int off(int t, int c) {
+        if (t == 0) return (c + 1) / 2;
+        if (t <= P + 1) return c <= P ? 0 : (c - P + 1) / 2;
+        const int ip = t - P - 2;
+        if (ip == 0 || c == 0) return 0;
+        return c >= 2 * ip - 1 ? ip : (c + 1) / 2;
+    }
+    __host__ __device__ static int type(int64_t i, int64_t n) {
+        if (i <= P) return (int)i + 1;
+        if (i >= n - 1 - P) return (int)(n - 1 - i) + P + 2;
+        return 0;
+    }
+};
+// f(integral_constant<t>) for the runtime row type t in [0, 2P+2]
+template <int P, int T = 0, class F>
+__device__ __forceinline__ void zdispatch(int t, F &&f) {
+    if constexpr (T < ZTy<P>::NTY) {
+        if (t == T) f(std::integral_constant<int, T>{});
+        else zdispatch<P, T + 1>(t, f);
+    }
+}
+
 struct ZArgs {
     DirView v[3];
     int64_t L0, L1;        // sum_i #I_{0,i}, sum_i #I_{1,i}
@@ -114,10 +150,33 @@ struct ZArgs {
     int64_t qoff;          // even local q2 (relative to cq_b) of this launch's first task point
     const int32_t *lines;  // line = i0 + n0 * i1
     int64_t n_items;
+    const int32_t *bounds;  // boundary lines: [gridDim.x + 1] cost-balanced contiguous chunks, or null
     double *val;
     int32_t *col;
     int64_t val_base;
+    unsigned long long *prof;  // debug builds (-DWQ_ZL_PROF): per (block, warp) [total, wait1, wait2] cycles
 };
+
+// debug builds: per-warp wait accounting (tools/prof_zline.py); compiled out of the product build
+#ifdef WQ_ZL_MIXED
+#define ZMIXED 1
+#else
+#define ZMIXED 0
+#endif
+#ifdef WQ_ZL_PROF
+#define ZPROF 1
+#else
+#define ZPROF 0
+#endif
+__device__ __forceinline__ void zwait(uint64_t *b, unsigned par, unsigned long long &acc) {
+    if (ZPROF) {
+        const long long t0 = clock64();
+        mbar_wait(b, par);
+        acc += clock64() - t0;
+    } else {
+        mbar_wait(b, par);
+    }
+}
 
 // Interior rules of a uniform mesh (translation invariant: every interior row i has the same
 // weights w(c) on its points c = 0..2p, and the basis values at its points depend only on whether
@@ -190,8 +249,19 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
     for (int x = tid; x < nq2l; x += blockDim.x) span2[x] = v2.span[cqb + x];
     // tasks: local points (2 tau, 2 tau + 1); the slab's first point is local 0
     const int NTASK = (q_end + 1) / 2;
-    const int64_t first = blockIdx.x, step = gridDim.x;
-    const int64_t my_items = first < a.n_items ? (a.n_items - first + step - 1) / step : 0;
+    // items of this CTA: round-robin (neighbouring lines run concurrently and share their coefficient
+    // boxes in L2), or a contiguous chunk (boundary lines, sorted by row type: one code path per CTA)
+    // boundary lines: chunks of ZCH consecutive lines (same row types, sorted on the host) dealt
+    // round-robin, which keeps the per-CTA work balanced
+    constexpr int64_t ZCH = BND ? 4 : 1;
+    const int64_t G = gridDim.x, c_ = blockIdx.x;
+    int64_t my_items;
+    {
+        const int64_t R = a.n_items / (G * ZCH), rem = a.n_items - R * G * ZCH;
+        const int64_t ex = rem - c_ * ZCH;
+        my_items = R * ZCH + (ex < 0 ? 0 : (ex > ZCH ? ZCH : ex));
+    }
+    auto item_of = [&](int64_t k) { return ((k / ZCH) * G + c_) * ZCH + k % ZCH; };
     const int64_t n_tasks = my_items * NTASK;
 
     if (tid == 0) {
@@ -203,9 +273,20 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
     __syncthreads();
 
     const int smsp = warp & 3, wrow = warp >> 2;
-    if (smsp < 2) {
+    const long long t_start = clock64();
+    unsigned long long wt1 = 0, wt2 = 0;
+    auto prof_out = [&]() {
+        if (ZPROF && a.prof && lane == 0) {
+            unsigned long long *o = a.prof + ((size_t)blockIdx.x * (blockDim.x / 32) + warp) * 3;
+            o[0] = clock64() - t_start; o[1] = wt1; o[2] = wt2;
+        }
+    };
+    // roles: WQ_ZL_MIXED: warps 0..NWP-1 producers (one per SM sub-partition and row), the rest
+    // consumers; else by sub-partition (warp % 4 in {0, 1} producers)
+    const bool is_prod = ZMIXED ? warp < NWP : smsp < 2;
+    if (is_prod) {
         // ============================================================ producer warp
-        const int wp = wrow * 2 + smsp;
+        const int wp = ZMIXED ? warp : wrow * 2 + smsp;
         double *wbase = Boxes + wp * (NB * BOXD + CF::YD);
         double *Ybuf = wbase + NB * BOXD;  // BND only
         double *tab = Tabs + wp * CF::TABD;
@@ -213,7 +294,6 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
         // NPP so that (r, r+1) pairs load as one 16-B word), W0t / W1t [c][f] (f = a + 2b)
         double *T0 = tab, *T1 = T0 + 2 * QX * NPP;
         double *W0t = T1 + 2 * QX * NPP, *W1t = W0t + 4 * QX;
-        int *off0 = (int *)(W1t + 4 * QX), *off1 = off0 + QX;  // BND: staircase offsets span - jlo
         constexpr unsigned BOX_BYTES = 6 * QX * QX * 2 * 8;
         // task T = k * NTASK + tau of this warp (T = wp, wp + NWP, ...): item k, point pair tau; the
         // issue stream (TMA of the coefficient boxes) runs NB tasks ahead of the compute stream
@@ -223,7 +303,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
         auto issue = [&](int b) {  // lane 0: TMA of the next task of the issue stream into buffer b
             if (is_T >= n_tasks) return;
             if (is_k != ik) {
-                const ZItem I = z_item(a, first + is_k * step);
+                const ZItem I = z_item(a, item_of(is_k));
                 ik = is_k; iq0 = I.ql0; iq1 = I.ql1;
             }
             mbar_arrive_tx(&pfull[wp * NB + b], BOX_BYTES);
@@ -265,7 +345,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             w1u0 = u.w[1][c1][m == 1 ? 2 : 0];
             w1u1 = u.w[1][c1][m == 1 ? 3 : 1];
         }
-        int cq0 = QI, cq1 = QI;
+        int cq0 = QI, cq1 = QI, ty0 = 0, ty1 = 0;
         int use = 0;
         for (int64_t T = wp; T < n_tasks; T += NWP, ++use) {
             const int b = NB == 2 ? (use & 1) : 0;
@@ -275,10 +355,14 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             }
             if (!PU && k != cur_item) {
                 cur_item = k;
-                const ZItem I = z_item(a, first + k * step);
+                const ZItem I = z_item(a, item_of(k));
                 const DirView &v0 = a.v[0], &v1 = a.v[1];
                 __syncwarp();
-                if (BND) { cq0 = I.nq0; cq1 = I.nq1; }
+                if (BND) {
+                    cq0 = I.nq0; cq1 = I.nq1;
+                    ty0 = ZTy<P>::type(I.i0, v0.n);
+                    ty1 = ZTy<P>::type(I.i1, v1.n);
+                }
                 for (int x = lane; x < QX * NPP; x += 32) {
                     const int c = x / NPP, r = x % NPP;
                     const double2 b0 = c < cq0 && r < NP ? __ldg((const double2 *)(v0.B + (int64_t)(I.ql0 + c) * BS) + r) : make_double2(0.0, 0.0);
@@ -289,11 +373,6 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     W0t[x] = x / 4 < cq0 ? __ldg(v0.W + (int64_t)I.i0 * v0.maxq * 4 + x) : 0.0;
                     W1t[x] = x / 4 < cq1 ? __ldg(v1.W + (int64_t)I.i1 * v1.maxq * 4 + x) : 0.0;
                 }
-                if (BND)
-                    for (int x = lane; x < QX; x += 32) {
-                        off0[x] = x < cq0 ? v0.span[I.ql0 + x] - I.jl0 : 0;
-                        off1[x] = x < cq1 ? v1.span[I.ql1 + x] - I.jl1 : 0;
-                    }
                 __syncwarp();
             }
             // direction-2 basis pairs of the task's points (published with G)
@@ -301,7 +380,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             const int b2pt = lane / NP, b2r = lane % NP;
             const int b2q = 2 * tau + b2pt;
             if (lane < 2 * NP && b2q < q_end) b2v = __ldg((const double2 *)(v2.B + (int64_t)(cqb + b2q) * BS) + b2r);
-            mbar_wait(&pfull[wp * NB + b], (NB == 2 ? use >> 1 : use) & 1);
+            zwait(&pfull[wp * NB + b], (NB == 2 ? use >> 1 : use) & 1, wt1);
             const double *bx = wbase + b * BOXD;  // [comp][c0][c1][pt]
             // ---------------- stage A: fibre (m, c1), both points, chains a2 = 0 (y0), 1 (y1)
             // Y: block m*2+a2 at CF::yoff, [c1][t0][pt] inside; interior: over the consumed box
@@ -351,9 +430,13 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                         }
                     };
                     if constexpr (BND) {
-                        #pragma unroll 1
-                        for (int c0 = 0; c0 < cq0; ++c0)
-                            dispatch<0, K - NP>(off0[c0], [&](auto O) { plane(c0, O); });
+                        zdispatch<P>(ty0, [&](auto TT) {
+                            constexpr int t = decltype(TT)::value;
+                            unroll<ZTy<P>::nq(t)>([&](auto C0) {
+                                constexpr int c0 = decltype(C0)::value;
+                                plane(c0, std::integral_constant<int, ZTy<P>::off(t, c0)>{});
+                            });
+                        });
                     } else {
                         unroll<QI>([&](auto C0) {
                             constexpr int c0 = decltype(C0)::value;
@@ -373,6 +456,11 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 }
             }
             __syncwarp();
+            if constexpr (BND) {
+                // the box is consumed (Y has its own buffer): start the next task's box load now
+                fence_async_smem();
+                if (lane == 0) issue(b);
+            }
             // ---------------- stage B: lane (g, t0): acc[x][pt][t1] over the Y blocks x = 0, 1
             double g[2][2][K];
             #pragma unroll
@@ -408,8 +496,13 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     }
                 };
                 if constexpr (BND) {
-                    #pragma unroll 1
-                    for (int c1 = 0; c1 < cq1; ++c1) dispatch<0, K - NP>(off1[c1], [&](auto O) { point1(c1, O); });
+                    zdispatch<P>(ty1, [&](auto TT) {
+                        constexpr int t = decltype(TT)::value;
+                        unroll<ZTy<P>::nq(t)>([&](auto C1) {
+                            constexpr int c1 = decltype(C1)::value;
+                            point1(c1, std::integral_constant<int, ZTy<P>::off(t, c1)>{});
+                        });
+                    });
                 } else {
                     unroll<QI>([&](auto C1) {
                         constexpr int c1 = decltype(C1)::value;
@@ -421,7 +514,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             // two chains as component a2 = g of b2 = 0; lanes g = 2 store both components of b2 = 1
             const uint32_t Tl = (uint32_t)T;
             const int slot_t = (int)(Tl % NTS);
-            mbar_wait(&gempty[slot_t], ((Tl / NTS) & 1) ^ 1);
+            zwait(&gempty[slot_t], ((Tl / NTS) & 1) ^ 1, wt2);
             {
                 // lanes g = 0 receive the a2 = 1 sums of lanes g = 1 and store (a2 = 0, a2 = 1) pairs of
                 // b2 = 0; lanes g = 2 store their pairs of b2 = 1 (one 16-B store per lane and entry)
@@ -442,15 +535,18 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             if (lane < 2 * NP) B2r[(slot_t * 2 + b2pt) * NP + b2r] = b2v;
             mbar_arrive(&gfull[slot_t]);
             // the buffer is free again (all lanes done with Y): prefetch the task after next into it
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) issue(b);
+            if constexpr (!BND) {
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) issue(b);
+            }
         }
+        prof_out();
         return;
     }
 
     // ============================================================ stage C consumers
-    const int cw = wrow * 2 + (smsp - 2);
+    const int cw = ZMIXED ? warp - NWP : wrow * 2 + (smsp - 2);
     const DirView &v0 = a.v[0], &v1 = a.v[1];
     const int n0 = (int)v0.n, n01 = n0 * (int)v1.n;
     int colx[CPL], colr[CPL], t0c[CPL], t1c[CPL];
@@ -477,10 +573,10 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
     const int my_first = cw * NR;
     int wbuf = 0;
     unsigned wuse[2] = {0, 0};
-    if (lane == 0 && my_first < n2l && first < a.n_items) w2_issue(my_first, 0);
+    if (lane == 0 && my_first < n2l && my_items > 0) w2_issue(my_first, 0);
     uint32_t got = 0, rel = 0, Tbase = 0;  // tasks waited for / released, first task of the item
-    for (int64_t it = first; it < a.n_items; it += step) {
-        const ZItem I = z_item(a, it);
+    for (int64_t ik_ = 0; ik_ < my_items; ++ik_) {
+        const ZItem I = z_item(a, item_of(ik_));
         bool live[CPL];
         int el[CPL], colb[CPL];
         #pragma unroll
@@ -497,26 +593,26 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             const int rl = r0 + nr - 1;
             const uint32_t t_hi = Tbase + (uint32_t)((qlo2[rl] + qlen2[rl] - 1) / 2);
             const uint32_t t_lo = Tbase + (uint32_t)(qlo2[r0] / 2);
-            mbar_wait(&wfull[cw * 2 + wbuf], wuse[wbuf] & 1);
+            zwait(&wfull[cw * 2 + wbuf], wuse[wbuf] & 1, wt2);
             ++wuse[wbuf];
             const double2 *W2w = (const double2 *)(W2b + wbuf * CF::W2D);  // [row][c][2] double2, row stride mq2
             if (lane == 0) {
                 int nxt = r0 + NWC * NR;
                 bool more = true;
-                if (nxt >= n2l) { nxt = my_first; more = it + step < a.n_items; }
+                if (nxt >= n2l) { nxt = my_first; more = ik_ + 1 < my_items; }
                 if (more) w2_issue(nxt, wbuf ^ 1);
             }
             wbuf ^= 1;
             __syncwarp();
             while (rel < got && rel < t_lo) {
-                if (lane == 0) mbar_arrive(&gempty[rel % NTS]);
+                if (lane == 0) mbar_arrive_relaxed(&gempty[rel % NTS]);
                 ++rel;
             }
             while (got <= t_hi) {
-                mbar_wait(&gfull[got % NTS], (got / NTS) & 1);
+                zwait(&gfull[got % NTS], (got / NTS) & 1, wt1);
                 ++got;
                 while (rel < got && rel < t_lo) {
-                    if (lane == 0) mbar_arrive(&gempty[rel % NTS]);
+                    if (lane == 0) mbar_arrive_relaxed(&gempty[rel % NTS]);
                     ++rel;
                 }
             }
@@ -613,7 +709,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 const uint32_t t_rel = Tbase + (uint32_t)(low / 2);
                 __syncwarp();
                 while (rel < t_rel && rel < got) {
-                    if (lane == 0) mbar_arrive(&gempty[rel % NTS]);
+                    if (lane == 0) mbar_arrive_relaxed(&gempty[rel % NTS]);
                     ++rel;
                 }
             }
@@ -660,11 +756,12 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 ++got;
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&gempty[rel % NTS]);
+            if (lane == 0) mbar_arrive_relaxed(&gempty[rel % NTS]);
             ++rel;
         }
         Tbase = t_end;
     }
+    prof_out();
 }
 
 // ---------------------------------------------------------------- host side
@@ -679,6 +776,8 @@ PFN_cuTensorMapEncodeTiled_v12000 z_encode_fn() {
     }
     return fn;
 }
+
+unsigned long long *g_zprof = nullptr;
 
 int z_num_sms(int dev) {
     int n = 0;
@@ -706,9 +805,17 @@ wq_status launch_zline_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, i
         a.qoff = (wq_host_qlo(a.i2b, Pl->dir[2].E, Pl->p) - Pl->cq_b) & ~(int64_t)1;
         a.lines = lines;
         a.n_items = n_lines;
+        a.bounds = nullptr;
         a.val = val;
         a.col = col;
         a.val_base = val_base;
+        a.prof = nullptr;
+        if (ZPROF && getenv("WQ_ZL_PROF")) {  // debug: per-warp wait accounting, read back with wq_debug_zprof
+            if (!g_zprof) cudaMalloc(&g_zprof, sizeof(unsigned long long) * 148 * 32 * 3 * 3);
+            const int slot = BND ? 2 : (PU ? 0 : 1);
+            a.prof = g_zprof + (size_t)slot * 148 * 32 * 3;
+            cudaMemsetAsync(a.prof, 0, sizeof(unsigned long long) * 148 * 32 * 3, s);
+        }
         CUtensorMap m;
         auto fn = z_encode_fn();
         if (!fn) { wq_set_error("cuTensorMapEncodeTiled unavailable"); return WQ_ECUDA; }
@@ -763,10 +870,37 @@ namespace {
 // (uniform knots k/E agree to ~3e-14 because of the FP64 rounding of the knots, exactly when E is a
 // power of two).  On success the representative row n/2 fills the kernel's uniform tables.
 #define ZFAIL(...) do { if (getenv("WQ_DEBUG")) { fprintf(stderr, "[wq] uniform rules rejected: " __VA_ARGS__); fprintf(stderr, "\n"); } return false; } while (0)
-bool z_fetch_uniform(wq_plan_s *P, cudaStream_t s, ZUni &U) {
+template <int PP>
+bool z_types_match(const std::vector<int32_t> &qlo, const std::vector<int32_t> &qlen, const std::vector<int32_t> &jlo,
+                   const std::vector<int32_t> &span, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) {
+        const int t = ZTy<PP>::type(i, n);
+        if (qlen[i] != ZTy<PP>::nq(t)) return false;
+        for (int c = 0; c < qlen[i]; ++c)
+            if (span[qlo[i] + c] - jlo[i] != ZTy<PP>::off(t, c)) return false;
+    }
+    return true;
+}
+bool z_fetch_uniform(wq_plan_s *P, cudaStream_t s, ZUni &U, bool &types_ok) {
     const int p = P->p, K = 2 * p + 1, bs = wq_bstride(p);
+    types_ok = false;
     if (p > WQ_ZPMAX || cudaStreamSynchronize(s) != cudaSuccess) ZFAIL("p or stream");
     memset(&U, 0, sizeof(U));
+    // staircase types of every row (the boundary-line kernel unrolls them at compile time)
+    for (int l = 0; l < 3; ++l) {
+        const DirView &v = P->dir[l];
+        std::vector<int32_t> qlo(v.n), qlen(v.n), jlo(v.n), span(v.nq);
+        if (cudaMemcpy(qlo.data(), v.qlo, v.n * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(qlen.data(), v.qlen, v.n * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(jlo.data(), v.jlo, v.n * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(span.data(), v.span, v.nq * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+            ZFAIL("copy");
+        const bool ok = p == 2 ? z_types_match<2>(qlo, qlen, jlo, span, v.n)
+                      : p == 3 ? z_types_match<3>(qlo, qlen, jlo, span, v.n)
+                               : z_types_match<4>(qlo, qlen, jlo, span, v.n);
+        if (!ok) ZFAIL("dir %d: row staircase types do not match", l);
+    }
+    types_ok = true;
     for (int l = 0; l < 3; ++l) {
         const DirView &v = P->dir[l];
         const int64_t n = v.n, nq = v.nq;
@@ -825,7 +959,13 @@ wq_status launch_assemble_zline(wq_plan_s *P, int cls, const int32_t *lines, int
     static_assert(sizeof(ZUni) <= sizeof(P->zuni_buf), "uniform table buffer");
     if (P->zuni_state == 0) {
         ZUni U;
-        const bool ok = !getenv("WQ_ZLINE_NO_UNIFORM") && z_fetch_uniform(P, s, U);
+        bool types_ok = false;
+        bool ok = z_fetch_uniform(P, s, U, types_ok);
+        if (!types_ok) {
+            wq_set_error("z-line kernel: row staircases do not match the compiled row types");
+            return WQ_EINVAL;
+        }
+        if (getenv("WQ_ZLINE_NO_UNIFORM")) ok = false;
         P->zuni_state = ok ? 1 : -1;
         if (ok) memcpy(P->zuni_buf, &U, sizeof(U));
     }
@@ -845,4 +985,12 @@ wq_status launch_assemble_zline(wq_plan_s *P, int cls, const int32_t *lines, int
     }
     wq_set_error("z-line kernel not available for this degree");
     return WQ_EINVAL;
+}
+
+// debug only (-DWQ_ZL_PROF, WQ_ZL_PROF=1): per-warp cycle accounting of the last z-line launches,
+// [class uni/int/bnd][148 blocks][32 warps][total, wait1, wait2]
+extern "C" int wq_debug_zprof(unsigned long long *host, int n) {
+    if (!g_zprof) return -1;
+    cudaDeviceSynchronize();
+    return (int)cudaMemcpy(host, g_zprof, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost);
 }

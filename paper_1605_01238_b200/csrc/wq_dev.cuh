@@ -42,6 +42,12 @@ __device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
     asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(b)) : "memory");
 }
+// relaxed arrive: no release ordering of this thread's earlier memory operations (used by
+// consumers to hand a ring slot back once the values read from it have been consumed by
+// arithmetic; a release arrive would also wait for the warp's outstanding global stores)
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t *b) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.relaxed.cta.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, unsigned bytes) {
     asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(smem_u32(b)),
                  "r"(bytes)

@@ -83,6 +83,8 @@ struct wq_plan_s {
     int32_t *zlines_dev;
     // uniform-mesh interior rules for the z-line kernel (fetched once per plan at the first
     // assembly): 0 not checked yet, 1 usable (zuni_buf holds them), -1 not uniform
+    int32_t *zbounds_dev;          // cost-balanced chunks of the boundary lines for zbounds_n CTAs
+    int64_t zbounds_n;
     int zuni_state;
     double zuni_buf[3 * 9 * 4 + 3 * 2 * 5 * 2];
 };
