@@ -335,7 +335,7 @@ def main():
             "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": alg_bytes,
             "algorithmic_bytes": "12 B/nnz (8 value + 4 column) + 48 B per coefficient point read",
-            "kernel": "wq_assemble (line kernel: interior + boundary-line launches)",
+            "kernel": "wq_assemble (z-line kernel, p <= 4: uniform / interior / boundary line launches; row-tile kernel for p > 4)",
             "kernel_ms": res["t_asm"] * 1e3, "kernel_share_of_step": res["t_asm"] / res["t_step"],
             "fp64": {"algorithmic_flops_per_launch": res["flops"], "achieved_tflops": res["flops"] / res["t_asm"] / 1e12,
                      "peak_tflops": fp64_max, "frac": res["flops"] / res["t_asm"] / 1e12 / fp64_max,

@@ -247,6 +247,142 @@ __global__ void __launch_bounds__(NTC) k_coef(CoefArgs a) {
     }
 }
 
+// z layout (d = 3, stiffness for the z-line kernel): the same sum factorisation with the roles of
+// the directions permuted so that the fast thread index runs along q_3, the contiguous axis of
+// [comp][q_1][q_2][q_3], while stage A still reads the control net along its contiguous k_1:
+// CTA = TQF q_3 points x TQM q_1 points of one q_2 plane;
+//   stage A contracts k_2 (plane):   A0 = N2 . Q^1, A1 = M2 . Q^2, A2 = N2 . Q^3   (threads over k_1, k_3)
+//   stage B contracts k_1:           X0 = M1 . A0,  X1 = N1 . A1,  X2 = N1 . A2
+//   stage C contracts k_3 per point: J[:,0] = N3 . X0, J[:,1] = N3 . X1, J[:,2] = M3 . X2
+constexpr int TQF = 32, TQM = 8;
+__global__ void __launch_bounds__(TQF * TQM) k_coefz(CoefArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    const int p = a.p;
+    const DirView &v0 = a.v[0], &v1 = a.v[1], &v2 = a.v[2];
+    const int64_t q1p = blockIdx.z;  // plane (direction 2)
+    const int64_t qfa = (int64_t)blockIdx.x * TQF, qma = (int64_t)blockIdx.y * TQM;  // q_3 local, q_1
+    const int64_t nqf = a.nq_loc_d, nqm = v0.nq;
+    const int64_t qfe = qfa + TQF < nqf ? qfa + TQF : nqf, qme = qma + TQM < nqm ? qma + TQM : nqm;
+    const int ntf = (int)(qfe - qfa), ntm = (int)(qme - qma);
+    const int64_t cqb = a.cq_b;
+    const int64_t kfa = v2.span[cqb + qfa], kfe = v2.span[cqb + qfe - 1] + p + 1;
+    const int64_t kma = v0.span[qma], kme = v0.span[qme - 1] + p + 1;
+    const int KF = (int)(kfe - kfa), KM = (int)(kme - kma);
+    const int KFM = TQF + p + 1, KMM = TQM + p + 1;
+    double *Asm = sm;                      // [3 variants][3 comps][KFM][KMM]  (k_1 fastest)
+    double *Xsm = sm + 9 * KMM * KFM;      // [TQM][3 variants][3 comps][KFM]
+    const int tid = threadIdx.x;
+    const double *P = a.ctrl;
+    const int64_t n0 = v0.n, n1 = v1.n;
+    {
+        // stage A: contract k_2 with the plane's basis; threads over (k_3, k_1), k_1 fastest
+        const double *nt = Ntab(v1, p, q1p), *mt = Mtab(v1, p, q1p);
+        const int64_t e1 = v1.span[q1p];
+        for (int t = tid; t < KF * KM; t += blockDim.x) {
+            const int cf = t / KM, cm = t % KM;
+            const int64_t k0 = kma + cm, k2 = kfa + cf;
+            double A0[3] = {0, 0, 0}, A1[3] = {0, 0, 0}, A2[3] = {0, 0, 0}, prev[3] = {0, 0, 0};
+            const double s0 = k0 >= 1 ? dscale(v0, p, k0) : 0.0;
+            const double s2 = k2 >= 1 ? dscale(v2, p, k2) : 0.0;
+            for (int r = 0; r <= p; ++r) {
+                const int64_t k1 = e1 + r;
+                const int64_t k = k0 + n0 * (k1 + n1 * k2);
+                const double nv = nt[2 * r];
+                const double s1 = r >= 1 ? dscale(v1, p, k1) : 0.0;
+                #pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double cur = __ldg(P + k * 3 + c);
+                    const double d0 = k0 >= 1 ? (cur - __ldg(P + (k - 1) * 3 + c)) * s0 : 0.0;
+                    const double d2 = k2 >= 1 ? (cur - __ldg(P + (k - n0 * n1) * 3 + c)) * s2 : 0.0;
+                    A0[c] = fma(nv, d0, A0[c]);
+                    A2[c] = fma(nv, d2, A2[c]);
+                    if (r >= 1) A1[c] = fma(mt[r - 1], (cur - prev[c]) * s1, A1[c]);
+                    prev[c] = cur;
+                }
+            }
+            #pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                Asm[((0 * 3 + c) * KFM + cf) * KMM + cm] = A0[c];
+                Asm[((1 * 3 + c) * KFM + cf) * KMM + cm] = A1[c];
+                Asm[((2 * 3 + c) * KFM + cf) * KMM + cm] = A2[c];
+            }
+        }
+    }
+    __syncthreads();
+    // stage B: contract k_1 for each q_1 point of the tile
+    for (int t = tid; t < ntm * KF; t += blockDim.x) {
+        const int tm = t / KF, cf = t % KF;
+        const int64_t q0 = qma + tm;
+        const double *nt = Ntab(v0, p, q0), *mt = Mtab(v0, p, q0);
+        const int cms = (int)(v0.span[q0] - kma);
+        double X0[3] = {0, 0, 0}, X1[3] = {0, 0, 0}, X2[3] = {0, 0, 0};
+        for (int r = 0; r <= p; ++r) {
+            const double nv = nt[2 * r], mv = r < p ? mt[r] : 0.0;
+            #pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                X1[c] = fma(nv, Asm[((1 * 3 + c) * KFM + cf) * KMM + cms + r], X1[c]);
+                X2[c] = fma(nv, Asm[((2 * 3 + c) * KFM + cf) * KMM + cms + r], X2[c]);
+                if (r < p) X0[c] = fma(mv, Asm[((0 * 3 + c) * KFM + cf) * KMM + cms + 1 + r], X0[c]);
+            }
+        }
+        #pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            Xsm[((tm * 3 + 0) * 3 + c) * KFM + cf] = X0[c];
+            Xsm[((tm * 3 + 1) * 3 + c) * KFM + cf] = X1[c];
+            Xsm[((tm * 3 + 2) * 3 + c) * KFM + cf] = X2[c];
+        }
+    }
+    __syncthreads();
+    // stage C: one thread per point (q_3 fastest)
+    const int tf = tid % TQF, tm = tid / TQF;
+    if (tf >= ntf || tm >= ntm) return;
+    const int64_t q2l = qfa + tf, q0 = qma + tm;
+    const double *nt = Ntab(v2, p, cqb + q2l), *mt = Mtab(v2, p, cqb + q2l);
+    const int cfs = (int)(v2.span[cqb + q2l] - kfa);
+    double J[3][3];
+    #pragma unroll
+    for (int c = 0; c < 3; ++c)
+        #pragma unroll
+        for (int m = 0; m < 3; ++m) J[c][m] = 0.0;
+    const double *X = Xsm + (tm * 3) * 3 * KFM;
+    for (int r = 0; r <= p; ++r) {
+        const double nv = nt[2 * r], mv = r < p ? mt[r] : 0.0;
+        #pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            J[c][0] = fma(nv, X[(0 * 3 + c) * KFM + cfs + r], J[c][0]);
+            J[c][1] = fma(nv, X[(1 * 3 + c) * KFM + cfs + r], J[c][1]);
+            if (r < p) J[c][2] = fma(mv, X[(2 * 3 + c) * KFM + cfs + 1 + r], J[c][2]);
+        }
+    }
+    double adj[3][3];
+    adj[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    adj[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+    adj[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+    adj[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    adj[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+    adj[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+    adj[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    adj[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+    adj[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    const double det = J[0][0] * adj[0][0] + J[0][1] * adj[1][0] + J[0][2] * adj[2][0];
+    if (!(det > 0.0) && !(det < 0.0)) atomicOr(&a.flags->det_zero, 1);
+    else if (det > 0.0) { if (!a.flags->det_pos) atomicOr(&a.flags->det_pos, 1); }
+    else { if (!a.flags->det_neg) atomicOr(&a.flags->det_neg, 1); }
+    const double ad = fabs(det), inv = 1.0 / ad;
+    int comp = 0;
+    #pragma unroll
+    for (int l = 0; l < 3; ++l)
+        #pragma unroll
+        for (int m = l; m < 3; ++m) {
+            double sv = 0.0;
+            #pragma unroll
+            for (int k = 0; k < 3; ++k) sv = fma(adj[l][k], adj[m][k], sv);
+            a.coefz[(int64_t)comp * a.zcs + (q0 * v1.nq + q1p) * a.zld + q2l] = sv * inv;
+            ++comp;
+        }
+    if (a.need_m) a.coef[a.c0off + q0 + a.cld1 * (q1p + v1.nq * q2l)] = ad;  // standard layout, component 0
+}
+
 }  // namespace
 
 wq_status launch_coef(wq_plan_s *P, const double *ctrl, cudaStream_t s) {
@@ -271,7 +407,13 @@ wq_status launch_coef(wq_plan_s *P, const double *ctrl, cudaStream_t s) {
     a.zld = P->zld;
     a.zcs = P->zcs;
     const int K1M = TQ1 + P->p + 1, K2M = TQ2 + P->p + 1;
-    if (P->d == 3) {
+    if (P->d == 3 && P->zlayout) {
+        const size_t sm = (size_t)(9 * (TQM + P->p + 1) * (TQF + P->p + 1) + TQM * 9 * (TQF + P->p + 1)) * sizeof(double);
+        static bool setz = false;
+        if (!setz) { cudaFuncSetAttribute(k_coefz, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024); setz = true; }
+        dim3 g((unsigned)((a.nq_loc_d + TQF - 1) / TQF), (unsigned)((P->dir[0].nq + TQM - 1) / TQM), (unsigned)P->dir[1].nq);
+        k_coefz<<<g, TQF * TQM, sm, s>>>(a);
+    } else if (P->d == 3) {
         size_t sm = (size_t)(9 * K2M * K1M + TQ2 * 9 * K1M) * sizeof(double);
         static bool set = false;
         if (!set) { cudaFuncSetAttribute(k_coef<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024); set = true; }
