@@ -283,7 +283,8 @@ def test_ws_sub_slab_launch(p):
     ks, ctrl = make_case(3, p, 7, "grid", 0.1)
     rp0, col0, val0, info = run_full(ks, ctrl, p, STIFFNESS, wq.WQ_KERNEL_WS)
     n_d = 7 + p
-    plan = wq.Plan(p, ks, slab=(2, n_d - 1), need_mass=False, need_stiffness=True)
+    plan = wq.Plan(p, ks, slab=(2, n_d - 1), need_mass=False, need_stiffness=True,
+                   coef_layout=wq.WQ_LAYOUT_STANDARD)
     d_ctrl = torch.from_numpy(ctrl).cuda()
     rp, col, val = plan.alloc_csr()
     plan.setup(d_ctrl)
