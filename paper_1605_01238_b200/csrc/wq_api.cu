@@ -252,42 +252,49 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
                 if (!(interz(0, i0) && interz(1, i1))) P->zlines_bnd.push_back(line);
                 else (uniz(0, i0) && uniz(1, i1) ? P->zlines_uni : P->zlines_int).push_back(line);
             }
-        // boundary lines sorted by their row types (the kernel runs one unrolled staircase per type pair)
+        // boundary lines: greedy longest-processing-time assignment to the CTAs of one launch (cost:
+        // consumer work per line + producer stage-A fibre passes x #Q_0 + stage-B #Q_1), each CTA's
+        // list sorted by row types (the kernel runs one unrolled staircase per type pair); the
+        // lists are concatenated with bounds[c] = first item of CTA c
         auto ztype = [&](int l, int64_t i) -> int64_t {
             const int64_t n = P->dir[l].n;
             return i <= p ? i + 1 : (i >= n - 1 - p ? n - 1 - i + p + 2 : 0);
         };
-        std::stable_sort(P->zlines_bnd.begin(), P->zlines_bnd.end(), [&](int32_t x, int32_t y) {
-            const int64_t kx = ztype(0, x % n0) * 64 + ztype(1, x / n0), ky = ztype(0, y % n0) * 64 + ztype(1, y / n0);
-            return kx < ky;
-        });
-        std::vector<int32_t> all(P->zlines_uni);
-        all.insert(all.end(), P->zlines_int.begin(), P->zlines_int.end());
-        all.insert(all.end(), P->zlines_bnd.begin(), P->zlines_bnd.end());
-        // contiguous chunks of the sorted boundary lines with about equal producer work per CTA
-        // (stage A: fibre passes x #Q_0 points, stage B: #Q_1 points, per task)
+        auto zq = [&](int l, int64_t i) {
+            return (double)(host_qhi(i, P->dir[l].E, p) - host_qlo(i, P->dir[l].E, p) + 1);
+        };
         int nsm = 0;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P->device);
         const int64_t G = std::min<int64_t>(nsm > 0 ? nsm : 148, (int64_t)P->zlines_bnd.size());
         std::vector<int32_t> bounds;
         if (G > 0) {
-            std::vector<double> cum(P->zlines_bnd.size() + 1, 0.0);
-            for (size_t k = 0; k < P->zlines_bnd.size(); ++k) {
-                const int32_t line = P->zlines_bnd[k];
+            std::vector<std::pair<double, int32_t>> items;
+            for (int32_t line : P->zlines_bnd) {
                 const int64_t i0 = line % n0, i1 = line / n0;
-                const double q0 = (double)(host_qhi(i0, P->dir[0].E, p) - host_qlo(i0, P->dir[0].E, p) + 1);
-                const double q1 = (double)(host_qhi(i1, P->dir[1].E, p) - host_qlo(i1, P->dir[1].E, p) + 1);
-                const double passes = std::ceil(3.0 * q1 / 32.0);
-                cum[k + 1] = cum[k] + passes * q0 + q1;
+                const double q0 = zq(0, i0), q1 = zq(1, i1);
+                items.push_back({2.0 * (2 * p + 1) + std::ceil(3.0 * q1 / 32.0) * q0 + q1, line});
             }
-            bounds.resize(G + 1);
-            size_t k = 0;
-            for (int64_t c = 0; c <= G; ++c) {
-                const double target = cum.back() * (double)c / (double)G;
-                while (k < P->zlines_bnd.size() && cum[k] < target) ++k;
-                bounds[c] = (int32_t)(c == G ? P->zlines_bnd.size() : k);
+            std::stable_sort(items.begin(), items.end(), [](auto &x, auto &y) { return x.first > y.first; });
+            std::vector<double> load(G, 0.0);
+            std::vector<std::vector<int32_t>> per(G);
+            for (auto &it : items) {
+                const int64_t c = std::min_element(load.begin(), load.end()) - load.begin();
+                load[c] += it.first;
+                per[c].push_back(it.second);
+            }
+            P->zlines_bnd.clear();
+            bounds.push_back(0);
+            for (int64_t c = 0; c < G; ++c) {
+                std::stable_sort(per[c].begin(), per[c].end(), [&](int32_t x, int32_t y) {
+                    return ztype(0, x % n0) * 64 + ztype(1, x / n0) < ztype(0, y % n0) * 64 + ztype(1, y / n0);
+                });
+                P->zlines_bnd.insert(P->zlines_bnd.end(), per[c].begin(), per[c].end());
+                bounds.push_back((int32_t)P->zlines_bnd.size());
             }
         }
+        std::vector<int32_t> all(P->zlines_uni);
+        all.insert(all.end(), P->zlines_int.begin(), P->zlines_int.end());
+        all.insert(all.end(), P->zlines_bnd.begin(), P->zlines_bnd.end());
         P->zbounds_n = G;
         const size_t zl = sizeof(int32_t) * (all.size() + bounds.size() + 1);
         ce = cudaMalloc((void **)&P->zlines_dev, zl);

@@ -253,15 +253,19 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
     // boxes in L2), or a contiguous chunk (boundary lines, sorted by row type: one code path per CTA)
     // boundary lines: chunks of ZCH consecutive lines (same row types, sorted on the host) dealt
     // round-robin, which keeps the per-CTA work balanced
+    // (with a.bounds: the host's cost-balanced per-CTA item ranges)
     constexpr int64_t ZCH = BND ? 4 : 1;
     const int64_t G = gridDim.x, c_ = blockIdx.x;
-    int64_t my_items;
-    {
+    int64_t my_items, ib = 0;
+    if (a.bounds) {
+        ib = a.bounds[c_];
+        my_items = a.bounds[c_ + 1] - ib;
+    } else {
         const int64_t R = a.n_items / (G * ZCH), rem = a.n_items - R * G * ZCH;
         const int64_t ex = rem - c_ * ZCH;
         my_items = R * ZCH + (ex < 0 ? 0 : (ex > ZCH ? ZCH : ex));
     }
-    auto item_of = [&](int64_t k) { return ((k / ZCH) * G + c_) * ZCH + k % ZCH; };
+    auto item_of = [&](int64_t k) { return a.bounds ? ib + k : ((k / ZCH) * G + c_) * ZCH + k % ZCH; };
     const int64_t n_tasks = my_items * NTASK;
 
     if (tid == 0) {
@@ -387,9 +391,11 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             double *Y = BND ? Ybuf : wbase + b * BOXD;
             #pragma unroll
             for (int pass = 0; pass < CF::NPASS; ++pass) {
+                // boundary lines: the 3 #Q_1 fibres of this line packed densely (one pass when #Q_1 <= 10)
+                if (BND && 32 * pass >= 3 * cq1) break;
                 const int f = lane + 32 * pass;
-                const int m = f / QX, c1 = f % QX;
-                const bool fv = f < NF && (!BND || c1 < cq1);
+                const int m = BND ? f / cq1 : f / QX, c1 = BND ? f % cq1 : f % QX;
+                const bool fv = BND ? f < 3 * cq1 : f < NF;
                 double y0[2][K], y1[2][K];
                 #pragma unroll
                 for (int pt = 0; pt < 2; ++pt)
@@ -805,7 +811,8 @@ wq_status launch_zline_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, i
         a.qoff = (wq_host_qlo(a.i2b, Pl->dir[2].E, Pl->p) - Pl->cq_b) & ~(int64_t)1;
         a.lines = lines;
         a.n_items = n_lines;
-        a.bounds = nullptr;
+        a.bounds = BND && Pl->zbounds_dev && lines == Pl->zlines_dev + Pl->zlines_uni.size() + Pl->zlines_int.size() &&
+                           n_lines == (int64_t)Pl->zlines_bnd.size() ? Pl->zbounds_dev : nullptr;
         a.val = val;
         a.col = col;
         a.val_base = val_base;
@@ -838,6 +845,7 @@ wq_status launch_zline_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, i
         cudaFuncSetAttribute(k_zline<P, BND, PU, CU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int64_t grid = z_num_sms(Pl->device);
         if (grid > n_lines) grid = n_lines;
+        if (a.bounds && grid != Pl->zbounds_n) a.bounds = nullptr;
         k_zline<P, BND, PU, CU><<<(unsigned)grid, CF::NT, smem, s>>>(m, a, un);
         wq_count_launches(1);
         return wq_cuda_status(cudaGetLastError(), "z-line assembly kernel");
