@@ -344,6 +344,7 @@ wq_status wq_plan_destroy(wq_plan P) {
     if (P->zlines_dev) cudaFree(P->zlines_dev);
     if (P->lines_dev) cudaFree(P->lines_dev);
     if (P->ctrl_dev) cudaFree(P->ctrl_dev);
+    if (P->dnet) cudaFree(P->dnet);
     if (P->stage_val) cudaFree(P->stage_val);
     delete P;
     return WQ_OK;

@@ -12,6 +12,8 @@
 //   stage A contracts k_3, stage B contracts k_2, stage C contracts k_1 per
 //   point -- O(p) FMAs per component per point instead of the O(p^d) of the
 //   direct sum.
+#include <cstdlib>
+#include <type_traits>
 #include "wq_internal.cuh"
 
 namespace {
@@ -31,6 +33,7 @@ struct CoefArgs {
     int ncomp_s, ncomp;
     int need_s, need_m;
     Flags *flags;
+    const double *dnet;  // z layout: derivative control nets [k][m][c] (k_dnet)
     // z layout of the stiffness components (wq_internal.cuh): [comp][q_1][q_2][q_3 - cq_b]
     int zlayout;
     double *coefz;
@@ -254,7 +257,29 @@ __global__ void __launch_bounds__(NTC) k_coef(CoefArgs a) {
 //   stage A contracts k_2 (plane):   A0 = N2 . Q^1, A1 = M2 . Q^2, A2 = N2 . Q^3   (threads over k_1, k_3)
 //   stage B contracts k_1:           X0 = M1 . A0,  X1 = N1 . A1,  X2 = N1 . A2
 //   stage C contracts k_3 per point: J[:,0] = N3 . X0, J[:,1] = N3 . X1, J[:,2] = M3 . X2
-constexpr int TQF = 32, TQM = 8;
+constexpr int TQF = 32;
+
+// derivative control nets (d = 3): Q^m_k = (P_k - P_{k - e_m}) p / (xi_{k_m + p} - xi_{k_m}) for k_m >= 1,
+// else 0; [k][m][c], one thread per control point.  Same expressions as the inline differences of
+// k_coef (bit-identical), computed once per build instead of (p+1) times per grid tile.
+__global__ void k_dnet(const double *__restrict__ P, double *__restrict__ Q, DirView v0, DirView v1, DirView v2,
+                       int p, int64_t ntot) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= ntot) return;
+    const int64_t n0 = v0.n, n1 = v1.n;
+    const int64_t k0 = k % n0, k1 = (k / n0) % n1, k2 = k / (n0 * n1);
+    const double s0 = k0 >= 1 ? dscale(v0, p, k0) : 0.0;
+    const double s1 = k1 >= 1 ? dscale(v1, p, k1) : 0.0;
+    const double s2 = k2 >= 1 ? dscale(v2, p, k2) : 0.0;
+    #pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double cur = P[k * 3 + c];
+        Q[k * 9 + 0 + c] = k0 >= 1 ? (cur - P[(k - 1) * 3 + c]) * s0 : 0.0;
+        Q[k * 9 + 3 + c] = k1 >= 1 ? (cur - P[(k - n0) * 3 + c]) * s1 : 0.0;
+        Q[k * 9 + 6 + c] = k2 >= 1 ? (cur - P[(k - n0 * n1) * 3 + c]) * s2 : 0.0;
+    }
+}
+template <int TQM>
 __global__ void __launch_bounds__(TQF * TQM) k_coefz(CoefArgs a) {
     extern __shared__ __align__(16) double sm[];
     const int p = a.p;
@@ -275,29 +300,23 @@ __global__ void __launch_bounds__(TQF * TQM) k_coefz(CoefArgs a) {
     const double *P = a.ctrl;
     const int64_t n0 = v0.n, n1 = v1.n;
     {
-        // stage A: contract k_2 with the plane's basis; threads over (k_3, k_1), k_1 fastest
+        // stage A: contract k_2 with the plane's basis; threads over (k_3, k_1), k_1 fastest;
+        // derivative nets from k_dnet
         const double *nt = Ntab(v1, p, q1p), *mt = Mtab(v1, p, q1p);
         const int64_t e1 = v1.span[q1p];
+        const double *Q = a.dnet;
         for (int t = tid; t < KF * KM; t += blockDim.x) {
             const int cf = t / KM, cm = t % KM;
             const int64_t k0 = kma + cm, k2 = kfa + cf;
-            double A0[3] = {0, 0, 0}, A1[3] = {0, 0, 0}, A2[3] = {0, 0, 0}, prev[3] = {0, 0, 0};
-            const double s0 = k0 >= 1 ? dscale(v0, p, k0) : 0.0;
-            const double s2 = k2 >= 1 ? dscale(v2, p, k2) : 0.0;
+            double A0[3] = {0, 0, 0}, A1[3] = {0, 0, 0}, A2[3] = {0, 0, 0};
             for (int r = 0; r <= p; ++r) {
-                const int64_t k1 = e1 + r;
-                const int64_t k = k0 + n0 * (k1 + n1 * k2);
-                const double nv = nt[2 * r];
-                const double s1 = r >= 1 ? dscale(v1, p, k1) : 0.0;
+                const int64_t k = k0 + n0 * (e1 + r + n1 * k2);
+                const double nv = nt[2 * r], mv = r >= 1 ? mt[r - 1] : 0.0;
                 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const double cur = __ldg(P + k * 3 + c);
-                    const double d0 = k0 >= 1 ? (cur - __ldg(P + (k - 1) * 3 + c)) * s0 : 0.0;
-                    const double d2 = k2 >= 1 ? (cur - __ldg(P + (k - n0 * n1) * 3 + c)) * s2 : 0.0;
-                    A0[c] = fma(nv, d0, A0[c]);
-                    A2[c] = fma(nv, d2, A2[c]);
-                    if (r >= 1) A1[c] = fma(mt[r - 1], (cur - prev[c]) * s1, A1[c]);
-                    prev[c] = cur;
+                    A0[c] = fma(nv, __ldg(Q + k * 9 + 0 + c), A0[c]);
+                    A2[c] = fma(nv, __ldg(Q + k * 9 + 6 + c), A2[c]);
+                    if (r >= 1) A1[c] = fma(mv, __ldg(Q + k * 9 + 3 + c), A1[c]);
                 }
             }
             #pragma unroll
@@ -387,6 +406,7 @@ __global__ void __launch_bounds__(TQF * TQM) k_coefz(CoefArgs a) {
 
 wq_status launch_coef(wq_plan_s *P, const double *ctrl, cudaStream_t s) {
     CoefArgs a;
+    a.dnet = nullptr;
     for (int l = 0; l < 3; ++l) a.v[l] = P->dir[l];
     a.d = P->d;
     a.p = P->p;
@@ -408,11 +428,32 @@ wq_status launch_coef(wq_plan_s *P, const double *ctrl, cudaStream_t s) {
     a.zcs = P->zcs;
     const int K1M = TQ1 + P->p + 1, K2M = TQ2 + P->p + 1;
     if (P->d == 3 && P->zlayout) {
-        const size_t sm = (size_t)(9 * (TQM + P->p + 1) * (TQF + P->p + 1) + TQM * 9 * (TQF + P->p + 1)) * sizeof(double);
-        static bool setz = false;
-        if (!setz) { cudaFuncSetAttribute(k_coefz, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024); setz = true; }
-        dim3 g((unsigned)((a.nq_loc_d + TQF - 1) / TQF), (unsigned)((P->dir[0].nq + TQM - 1) / TQM), (unsigned)P->dir[1].nq);
-        k_coefz<<<g, TQF * TQM, sm, s>>>(a);
+        const int64_t ntot = P->dir[0].n * P->dir[1].n * P->dir[2].n;
+        if (P->dnet_bytes < sizeof(double) * 9 * (size_t)ntot) {
+            if (P->dnet) cudaFree(P->dnet);
+            P->dnet_bytes = sizeof(double) * 9 * (size_t)ntot;
+            if (cudaMalloc((void **)&P->dnet, P->dnet_bytes) != cudaSuccess) {
+                P->dnet = nullptr;
+                P->dnet_bytes = 0;
+                wq_set_error("derivative control-net allocation failed");
+                return WQ_ENOMEM;
+            }
+        }
+        k_dnet<<<(unsigned)((ntot + 255) / 256), 256, 0, s>>>(ctrl, P->dnet, P->dir[0], P->dir[1], P->dir[2], P->p, ntot);
+        wq_count_launches(1);
+        a.dnet = P->dnet;
+        const int tqm = getenv("WQ_COEF_TQM") ? atoi(getenv("WQ_COEF_TQM")) : 16;  // tile height (tuning experiments)
+        auto run = [&](auto TT) {
+            constexpr int TQM = decltype(TT)::value;
+            const size_t sm = (size_t)(9 * (TQM + P->p + 1) * (TQF + P->p + 1) + TQM * 9 * (TQF + P->p + 1)) * sizeof(double);
+            cudaFuncSetAttribute(k_coefz<TQM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            dim3 g((unsigned)((a.nq_loc_d + TQF - 1) / TQF), (unsigned)((P->dir[0].nq + TQM - 1) / TQM), (unsigned)P->dir[1].nq);
+            k_coefz<TQM><<<g, TQF * TQM, sm, s>>>(a);
+        };
+        if (tqm == 4) run(std::integral_constant<int, 4>{});
+        else if (tqm == 16) run(std::integral_constant<int, 16>{});
+        else if (tqm == 2) run(std::integral_constant<int, 2>{});
+        else run(std::integral_constant<int, 8>{});
     } else if (P->d == 3) {
         size_t sm = (size_t)(9 * K2M * K1M + TQ2 * 9 * K1M) * sizeof(double);
         static bool set = false;

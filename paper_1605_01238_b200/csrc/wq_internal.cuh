@@ -62,6 +62,8 @@ struct wq_plan_s {
     void *arena;                   // one allocation for all small tables
     size_t arena_bytes;
     double *ctrl_dev;              // device control-net staging (wq_form_host)
+    double *dnet;                  // z layout: derivative control nets [N_DOF][3][3] (k_dnet)
+    size_t dnet_bytes;
     size_t ctrl_bytes;
     // form_host staging
     double *stage_val; int32_t *stage_col; int64_t *stage_rp; size_t stage_bytes;
