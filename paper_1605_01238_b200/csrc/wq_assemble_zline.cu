@@ -155,6 +155,8 @@ struct ZArgs {
     int32_t *col;
     int64_t val_base;
     unsigned long long *prof;  // debug builds (-DWQ_ZL_PROF): per (block, warp) [total, wait1, wait2] cycles
+    int dbg;                   // debug builds: ablation mask (WQ_ZL_DBG): 1 no consumer stores, 2 no consumer
+                               // fast-path arithmetic, 4 no producer stage A/B arithmetic
 };
 
 // debug builds: per-warp wait accounting (tools/prof_zline.py); compiled out of the product build
@@ -165,8 +167,10 @@ struct ZArgs {
 #endif
 #ifdef WQ_ZL_PROF
 #define ZPROF 1
+#define ZDBG(bit) (a.dbg & (bit))
 #else
 #define ZPROF 0
+#define ZDBG(bit) false
 #endif
 __device__ __forceinline__ void zwait(uint64_t *b, unsigned par, unsigned long long &acc) {
     if (ZPROF) {
@@ -310,8 +314,12 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 const ZItem I = z_item(a, item_of(is_k));
                 ik = is_k; iq0 = I.ql0; iq1 = I.ql1;
             }
-            mbar_arrive_tx(&pfull[wp * NB + b], BOX_BYTES);
-            tma_load_4d(wbase + b * BOXD, &tm, &pfull[wp * NB + b], (int)a.qoff + 2 * is_tau, iq1, iq0, 0);
+            if (ZDBG(8)) {
+                mbar_arrive(&pfull[wp * NB + b]);  // debug ablation: no box load
+            } else {
+                mbar_arrive_tx(&pfull[wp * NB + b], BOX_BYTES);
+                tma_load_4d(wbase + b * BOXD, &tm, &pfull[wp * NB + b], (int)a.qoff + 2 * is_tau, iq1, iq0, 0);
+            }
             is_T += NWP;
             is_tau += NWP;
             while (is_tau >= NTASK) { is_tau -= NTASK; ++is_k; }
@@ -401,7 +409,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 for (int pt = 0; pt < 2; ++pt)
                     #pragma unroll
                     for (int t = 0; t < K; ++t) { y0[pt][t] = 0.0; y1[pt][t] = 0.0; }
-                if (fv) {
+                if (fv && !ZDBG(4)) {
                     // components: a2 = 1 chain C_2m, a2 = 0 chain C_0m and C_1m (C_00 C_01 C_02 C_11 C_12 C_22)
                     const int ka = m == 0 ? 2 : (m == 1 ? 4 : 5);
                     const int kb = m == 0 ? 0 : (m == 1 ? 1 : 2);
@@ -475,7 +483,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 for (int pt = 0; pt < 2; ++pt)
                     #pragma unroll
                     for (int t = 0; t < K; ++t) g[x][pt][t] = 0.0;
-            if (fl) {
+            if (fl && !ZDBG(4)) {
                 const int t0 = fc;
                 const double *Ya = Y + CF::yoff(ybx0) + t0 * 2;
                 const double *Yb = Y + CF::yoff(ybx1) + t0 * 2;
@@ -635,7 +643,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             // rules are the uniform ones (the others go through the generic path)
             const int rlo = CU ? 2 * P : P + 1, rhi = CU ? (int)v2.n - 1 - 2 * P : (int)v2.n - P - 2;
             const bool interior = nr == NR && i2b + r0 >= rlo && i2b + r0 + NR - 1 <= rhi;
-            if (interior) {
+            if (interior && !ZDBG(2)) {
                 const int slot0 = slot_of(qlo2[r0]);
                 constexpr int UW = 2 * (NR - 1) + 2 * P + 1;
                 #pragma unroll
@@ -671,7 +679,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                         }
                     }
                 }
-            } else {
+            } else if (!interior && !ZDBG(16)) {
                 #pragma unroll
                 for (int k = 0; k < NR; ++k) {
                     if (k >= nr) break;
@@ -724,7 +732,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             const int nc = BND ? nc01 : K * K;
             #pragma unroll
             for (int k = 0; k < NR; ++k) {
-                if (k >= nr) break;
+                if (k >= nr || ZDBG(1)) break;
                 const int r = r0 + k;
                 const int ni2 = jlen2[r];
                 const int64_t ro = pref2[r] * L01 + (int64_t)ni2 * A - a.val_base;
@@ -817,6 +825,7 @@ wq_status launch_zline_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, i
         a.col = col;
         a.val_base = val_base;
         a.prof = nullptr;
+        a.dbg = getenv("WQ_ZL_DBG") ? atoi(getenv("WQ_ZL_DBG")) : 0;
         if (ZPROF && getenv("WQ_ZL_PROF")) {  // debug: per-warp wait accounting, read back with wq_debug_zprof
             if (!g_zprof) cudaMalloc(&g_zprof, sizeof(unsigned long long) * 148 * 32 * 3 * 3);
             const int slot = BND ? 2 : (PU ? 0 : 1);

@@ -55,13 +55,24 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, unsigned bytes) {
 }
 // try_wait with a suspend-time hint: the waiting warp sleeps in hardware (up to ~0.1 ms) until the
 // phase completes instead of re-issuing the test
+#ifndef WQ_MBAR_HINT
+#define WQ_MBAR_HINT 100000
+#endif
 __device__ __forceinline__ bool mbar_try(uint64_t *b, unsigned parity) {
     unsigned ok;
+#if WQ_MBAR_HINT > 0
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
         : "=r"(ok)
-        : "r"(smem_u32(b)), "r"(parity), "r"(100000u)
+        : "r"(smem_u32(b)), "r"(parity), "r"((unsigned)WQ_MBAR_HINT)
         : "memory");
+#else
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+#endif
     return ok != 0;
 }
 // wait until the phase with the given parity has completed
