@@ -175,7 +175,7 @@ __global__ void k_gauss(int n, double *gl) {
         double dP = n == 1 ? 1.0 : n * (x * P1 - P0) / (x * x - 1.0);
         double dx = P1 / dP;
         x -= dx;
-        if (fabs(dx) < 1e-17) break;
+        if (fabs(dx) <= 1e-15 * fabs(x)) break;  // FP64 accurate; the dd Newton steps below finish
     }
     dd X = dd_make(x), Pn, dPn;
     for (int it = 0; it < 3; ++it) {  // dd Newton
