@@ -46,14 +46,21 @@ using namespace wqdev;
 namespace {
 
 struct ZPar {
-    int nr, rw, nts, nb;  // rows per consumer batch, warps per SM sub-partition, task slots, box buffers per producer
+    // rows per consumer batch, producer / consumer warps per SM sub-partition (sub-partitions 0, 1
+    // produce, 2, 3 consume), task slots, box buffers per producer, t_1 columns per chunk
+    int nr, rwp, rwc, nts, nb, t0c;
 };
+// p >= 5: the columns (t_1, t_2) of a line are done in chunks of t0c values of t_1 (one launch per
+// chunk; stage A/B work splits without redundancy, only the coefficient boxes are re-read), which
+// keeps the G ring (4 t0c (2p+1) doubles per point) and the registers within the SM
 __host__ __device__ constexpr ZPar z_par(int p, bool bnd) {
     switch (p) {
-    case 2: return bnd ? ZPar{4, 3, 12, 1} : ZPar{4, 3, 16, 2};
-    case 3: return bnd ? ZPar{3, 2, 12, 1} : ZPar{3, 2, 16, 2};
-    case 4: return bnd ? ZPar{2, 2, 12, 1} : ZPar{2, 2, 16, 2};
-    default: return {0, 0, 0, 0};
+    case 2: return bnd ? ZPar{4, 3, 3, 12, 1, 5} : ZPar{4, 3, 3, 16, 2, 5};
+    case 3: return bnd ? ZPar{3, 2, 2, 12, 1, 7} : ZPar{3, 2, 2, 16, 2, 7};
+    case 4: return bnd ? ZPar{2, 2, 2, 12, 1, 9} : ZPar{2, 2, 2, 16, 2, 9};
+    case 5: return bnd ? ZPar{1, 1, 2, 16, 1, 6} : ZPar{1, 2, 2, 16, 1, 6};
+    case 6: return bnd ? ZPar{1, 1, 2, 14, 1, 7} : ZPar{1, 2, 2, 14, 1, 7};
+    default: return {0, 0, 0, 0, 0, 0};
     }
 }
 
@@ -65,12 +72,14 @@ struct ZCfg {
     static constexpr int QI = 2 * P + 1;
     static constexpr int QB = 3 * P + 1;  // max #Q of a row
     static constexpr int NP = P + 1;
-    static constexpr int COLS = K * K;
+    static constexpr int T0C = ENABLED ? W.t0c : K;   // t_1 values per column chunk
+    static constexpr int NCH = (K + T0C - 1) / T0C;   // chunks (launches per line class)
+    static constexpr int COLS = T0C * K;              // columns (t0 local, t1) of a chunk, t0 fastest
     static constexpr int CPL = (COLS + 31) / 32;  // columns (t0, t1) per consumer lane
     static constexpr int NR = ENABLED ? W.nr : 1;
-    static constexpr int RW = ENABLED ? W.rw : 1;
-    static constexpr int NWC = 2 * RW, NWP = 2 * RW;
-    static constexpr int NT = 128 * RW;
+    static constexpr int RWP = ENABLED ? W.rwp : 1, RWC = ENABLED ? W.rwc : 1;
+    static constexpr int NWC = 2 * RWC, NWP = 2 * RWP;
+    static constexpr int NT = 128 * (RWP > RWC ? RWP : RWC);
     static constexpr int NTS = ENABLED ? W.nts : 2;
     static constexpr int NB = ENABLED ? W.nb : 1;
     static constexpr int RING = 2 * NTS;
@@ -80,12 +89,14 @@ struct ZCfg {
     static constexpr int NPP = (NP + 1) & ~1;        // table row length (r pairs)
     // Y blocks (m*2 + a2) of QX*K*2 doubles, 128-B aligned block stride plus a per-block shift that
     // spreads the stage-B lanes (g, t0) over distinct bank groups
-    static constexpr int YB = (QX * K * 2 + 4 + 15) / 16 * 16;
+    static constexpr int YB = (QX * T0C * 2 + 4 + 15) / 16 * 16;
     __host__ __device__ static constexpr int yoff(int bi) { return bi * YB + (bi == 1 || bi == 3 ? 2 : (bi >= 4 ? 4 : 0)); }
     static constexpr int YTOT = 6 * YB;
-    static constexpr int BOXD = BND ? (6 * QX * QX * 2 + 15) / 16 * 16
-                                    : ((6 * QX * QX * 2 > YTOT ? 6 * QX * QX * 2 : YTOT) + 15) / 16 * 16;
-    static constexpr int YD = BND ? YTOT : 0;
+    // Y over the consumed box when stage A is one pass over interior fibres, else its own buffer
+    static constexpr bool YSEP = BND || NPASS > 1;
+    static constexpr int BOXD = YSEP ? (6 * QX * QX * 2 + 15) / 16 * 16
+                                     : ((6 * QX * QX * 2 > YTOT ? 6 * QX * QX * 2 : YTOT) + 15) / 16 * 16;
+    static constexpr int YD = YSEP ? YTOT : 0;
     static constexpr int TABD = (4 * QX * NPP + 8 * QX + QX + 1) & ~1;  // T0, T1, W0, W1, offsets (ints); 16-B multiple
     static constexpr int W2D = NR * QB * 4;                  // doubles per consumer weight buffer
     __host__ __device__ static constexpr size_t al(size_t x) { return (x + 127) & ~(size_t)127; }
@@ -101,7 +112,7 @@ struct ZCfg {
     __host__ __device__ static constexpr size_t d2_bytes(int64_t n2l, int64_t nq2l) {
         return al(8 * (size_t)(n2l + 1) + 16 * (size_t)n2l + 4 * (size_t)nq2l);
     }
-    static constexpr bool FITS = ENABLED && (BND || NF <= 32) && 3 * K <= 32 && NT <= 1024 &&
+    static constexpr bool FITS = ENABLED && 3 * T0C <= 32 && NT <= 1024 &&
                                  SMEM + d2_bytes(64, 2 * 64 + 2 * P + 1) <= 227 * 1024;
 };
 
@@ -186,7 +197,7 @@ __device__ __forceinline__ void zwait(uint64_t *b, unsigned par, unsigned long l
 // weights w(c) on its points c = 0..2p, and the basis values at its points depend only on whether
 // the point is a span midpoint (c even) or a knot (c odd), Remark 1).  Verified against the
 // device-computed rules of every interior row before use (z_fetch_uniform).
-#define WQ_ZPMAX 4
+#define WQ_ZPMAX 6
 struct __align__(16) ZUni {
     double w[3][2 * WQ_ZPMAX + 1][4];  // [dir][c][f], f = a + 2b
     double b[3][2][WQ_ZPMAX + 1][2];   // [dir][c & 1][r][value, derivative] of functions span..span+p
@@ -215,7 +226,7 @@ __device__ __forceinline__ ZItem z_item(const ZArgs &a, int64_t it) {
 
 // PU: the line's producer tables from the uniform rules (lines with i0, i1 in [2p, n-1-2p]);
 // CU: rows i2 in [2p, n2-1-2p] take the uniform rules in the consumer
-template <int P, bool BND, bool PU, bool CU>
+template <int P, bool BND, bool PU, bool CU, int CH>
 __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
     k_zline(const __grid_constant__ CUtensorMap tm, ZArgs a, const __grid_constant__ ZUni u) {
     using CF = ZCfg<P, BND>;
@@ -223,6 +234,8 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
     constexpr int K = CF::K, QI = CF::QI, NP = CF::NP, COLS = CF::COLS, CPL = CF::CPL;
     constexpr int NR = CF::NR, NWC = CF::NWC, NWP = CF::NWP, NTS = CF::NTS, RING = CF::RING, NB = CF::NB;
     constexpr int NF = CF::NF, BOXD = CF::BOXD, NPP = CF::NPP;
+    constexpr int T0C = CF::T0C, T0A = CH * T0C, T0N = K - T0A < T0C ? K - T0A : T0C;  // this chunk's t_1 range
+    constexpr bool YSEP = CF::YSEP;
     constexpr int BS = wq_bstride(P);
     extern __shared__ __align__(128) unsigned char smb[];
     uint64_t *pfull = (uint64_t *)(smb + CF::O_BAR);  // [NWP][NB]
@@ -292,11 +305,12 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
     // roles: WQ_ZL_MIXED: warps 0..NWP-1 producers (one per SM sub-partition and row), the rest
     // consumers; else by sub-partition (warp % 4 in {0, 1} producers)
     const bool is_prod = ZMIXED ? warp < NWP : smsp < 2;
+    if (!ZMIXED && (is_prod ? wrow >= CF::RWP : wrow >= CF::RWC)) return;  // idle warp (RWP != RWC)
     if (is_prod) {
         // ============================================================ producer warp
         const int wp = ZMIXED ? warp : wrow * 2 + smsp;
         double *wbase = Boxes + wp * (NB * BOXD + CF::YD);
-        double *Ybuf = wbase + NB * BOXD;  // BND only
+        double *Ybuf = wbase + NB * BOXD;  // YSEP only
         double *tab = Tabs + wp * CF::TABD;
         // line tables: T0[sel][c0][NPP], T1[sel][c1][NPP] (sel 0: derivative, 1: value; r padded to
         // NPP so that (r, r+1) pairs load as one 16-B word), W0t / W1t [c][f] (f = a + 2b)
@@ -333,8 +347,8 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
         int64_t cur_item = -1;
         // stage B lanes (g, t0): g = 0, 1 -> b2 = 0, a2 = g (chains m = 0 and m = 1 summed in the lane);
         // g = 2 -> b2 = 1 (chain m = 2, both a2).  Input blocks x = 0, 1 of Y and their tables:
-        const int fg = lane / K, fc = lane % K;
-        const bool fl = lane < 3 * K;
+        const int fg = lane / T0C, fc = lane % T0C;
+        const bool fl = lane < 3 * T0C && fc < T0N;
         const int ybx0 = fg == 0 ? 0 : (fg == 1 ? 1 : 4), ybx1 = fg == 0 ? 2 : (fg == 1 ? 3 : 5);  // Y blocks m*2+a2
         const int tsel1 = fg == 2 ? 1 : 0;  // table of block x = 1: B1' for m = 1, B1 for m = 2
         // PU: this lane's selections of the uniform tables (stage A: family b0 = [m == 0], weights of
@@ -396,7 +410,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             const double *bx = wbase + b * BOXD;  // [comp][c0][c1][pt]
             // ---------------- stage A: fibre (m, c1), both points, chains a2 = 0 (y0), 1 (y1)
             // Y: block m*2+a2 at CF::yoff, [c1][t0][pt] inside; interior: over the consumed box
-            double *Y = BND ? Ybuf : wbase + b * BOXD;
+            double *Y = YSEP ? Ybuf : wbase + b * BOXD;
             #pragma unroll
             for (int pass = 0; pass < CF::NPASS; ++pass) {
                 // boundary lines: the 3 #Q_1 fibres of this line packed densely (one pass when #Q_1 <= 10)
@@ -404,11 +418,11 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 const int f = lane + 32 * pass;
                 const int m = BND ? f / cq1 : f / QX, c1 = BND ? f % cq1 : f % QX;
                 const bool fv = BND ? f < 3 * cq1 : f < NF;
-                double y0[2][K], y1[2][K];
+                double y0[2][T0C], y1[2][T0C];
                 #pragma unroll
                 for (int pt = 0; pt < 2; ++pt)
                     #pragma unroll
-                    for (int t = 0; t < K; ++t) { y0[pt][t] = 0.0; y1[pt][t] = 0.0; }
+                    for (int t = 0; t < T0C; ++t) { y0[pt][t] = 0.0; y1[pt][t] = 0.0; }
                 if (fv && !ZDBG(4)) {
                     // components: a2 = 1 chain C_2m, a2 = 0 chain C_0m and C_1m (C_00 C_01 C_02 C_11 C_12 C_22)
                     const int ka = m == 0 ? 2 : (m == 1 ? 4 : 5);
@@ -435,11 +449,13 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                             for (int h = 0; h < 2; ++h) {
                                 const int r = 2 * rr + h;
                                 if (r > P) continue;
+                                const int t = o0 + r - T0A;  // compile time: t_1 in this chunk?
+                                if (t < 0 || t >= T0N) continue;
                                 const double bv = PU ? b0s[c0 & 1][r] : (h ? bp.y : bp.x);
-                                y1[0][o0 + r] = fma(bv, h1a, y1[0][o0 + r]);
-                                y1[1][o0 + r] = fma(bv, h1b, y1[1][o0 + r]);
-                                y0[0][o0 + r] = fma(bv, h0a, y0[0][o0 + r]);
-                                y0[1][o0 + r] = fma(bv, h0b, y0[1][o0 + r]);
+                                y1[0][t] = fma(bv, h1a, y1[0][t]);
+                                y1[1][t] = fma(bv, h1b, y1[1][t]);
+                                y0[0][t] = fma(bv, h0a, y0[0][t]);
+                                y0[1][t] = fma(bv, h0b, y0[1][t]);
                             }
                         }
                     };
@@ -458,19 +474,19 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                         });
                     }
                 }
-                if (!BND) __syncwarp();  // every lane has read the box: Y may overwrite it
+                if (!YSEP) __syncwarp();  // every lane has read the box: Y may overwrite it
                 if (fv) {
-                    double *Y0 = Y + CF::yoff(m * 2 + 0) + c1 * K * 2;
-                    double *Y1 = Y + CF::yoff(m * 2 + 1) + c1 * K * 2;
+                    double *Y0 = Y + CF::yoff(m * 2 + 0) + c1 * T0C * 2;
+                    double *Y1 = Y + CF::yoff(m * 2 + 1) + c1 * T0C * 2;
                     #pragma unroll
-                    for (int t = 0; t < K; ++t) {
+                    for (int t = 0; t < T0C; ++t) {
                         *(double2 *)(Y0 + t * 2) = make_double2(y0[0][t], y0[1][t]);
                         *(double2 *)(Y1 + t * 2) = make_double2(y1[0][t], y1[1][t]);
                     }
                 }
             }
             __syncwarp();
-            if constexpr (BND) {
+            if constexpr (YSEP) {
                 // the box is consumed (Y has its own buffer): start the next task's box load now
                 fence_async_smem();
                 if (lane == 0) issue(b);
@@ -486,12 +502,12 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             if (fl && !ZDBG(4)) {
                 const int t0 = fc;
                 const double *Ya = Y + CF::yoff(ybx0) + t0 * 2;
-                const double *Yb = Y + CF::yoff(ybx1) + t0 * 2;
+                const double *Yb = Y + CF::yoff(ybx1) + t0 * 2;  // t0: this lane's t_1 within the chunk
                 const double *Ta = T1 + QX * NPP, *Tb = T1 + tsel1 * QX * NPP;
                 auto point1 = [&](int c1, auto O) {
                     constexpr int o1 = decltype(O)::value;
-                    const double2 ya = *(const double2 *)(Ya + c1 * K * 2);
-                    const double2 yb = *(const double2 *)(Yb + c1 * K * 2);
+                    const double2 ya = *(const double2 *)(Ya + c1 * T0C * 2);
+                    const double2 yb = *(const double2 *)(Yb + c1 * T0C * 2);
                     #pragma unroll
                     for (int rr = 0; rr < NPP / 2; ++rr) {
                         const double2 pa = PU ? make_double2(0.0, 0.0) : *(const double2 *)(Ta + c1 * NPP + 2 * rr);
@@ -539,17 +555,17 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 for (int pt = 0; pt < 2; ++pt) {
                     double2 *Gd = Gs + ((slot_t * 2 + pt) * 2 + b2) * COLS + t0;
                     #pragma unroll
-                    for (int t = 0; t < K; ++t) {
+                    for (int t = 0; t < K; ++t) {  // t = t_2; column t0 + T0C t
                         const double v = fma(g[1][pt][t], sum1, g[0][pt][t]);
-                        const double o = __shfl_down_sync(0xffffffffu, v, K);
-                        if (fl && fg != 1) Gd[K * t] = make_double2(v, fg == 0 ? o : g[1][pt][t]);
+                        const double o = __shfl_down_sync(0xffffffffu, v, T0C);
+                        if (fl && fg != 1) Gd[T0C * t] = make_double2(v, fg == 0 ? o : g[1][pt][t]);
                     }
                 }
             }
             if (lane < 2 * NP) B2r[(slot_t * 2 + b2pt) * NP + b2r] = b2v;
             mbar_arrive(&gfull[slot_t]);
             // the buffer is free again (all lanes done with Y): prefetch the task after next into it
-            if constexpr (!BND) {
+            if constexpr (!YSEP) {
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) issue(b);
@@ -568,8 +584,8 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
     for (int j = 0; j < CPL; ++j) {
         colx[j] = lane + 32 * j;
         colr[j] = colx[j] < COLS ? colx[j] : COLS - 1;  // clamped column for shared-memory reads
-        t0c[j] = colx[j] % K;
-        t1c[j] = colx[j] / K;
+        t0c[j] = T0A + colx[j] % T0C;  // global t_1 of the column
+        t1c[j] = colx[j] / T0C;
     }
     double *W2b = W2all + cw * 2 * CF::W2D;  // [2][NR][mq2][4]
     const int mq2 = v2.maxq;
@@ -595,7 +611,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
         int el[CPL], colb[CPL];
         #pragma unroll
         for (int j = 0; j < CPL; ++j) {
-            live[j] = colx[j] < COLS && t0c[j] < I.ni0 && t1c[j] < I.ni1;
+            live[j] = colx[j] < COLS && colx[j] % T0C < T0N && t0c[j] < I.ni0 && t1c[j] < I.ni1;
             el[j] = t0c[j] + I.ni0 * t1c[j];
             colb[j] = (I.jl0 + t0c[j]) + n0 * (I.jl1 + t1c[j]);
         }
@@ -793,6 +809,14 @@ PFN_cuTensorMapEncodeTiled_v12000 z_encode_fn() {
 
 unsigned long long *g_zprof = nullptr;
 
+template <int N, class F>
+void hunroll(F &&f) {  // host-side compile-time loop
+    if constexpr (N > 0) {
+        hunroll<N - 1>(f);
+        f(std::integral_constant<int, N - 1>{});
+    }
+}
+
 int z_num_sms(int dev) {
     int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -851,13 +875,20 @@ wq_status launch_zline_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, i
             wq_set_error("z-line kernel: direction-2 tables exceed shared memory");
             return WQ_EINVAL;
         }
-        cudaFuncSetAttribute(k_zline<P, BND, PU, CU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int64_t grid = z_num_sms(Pl->device);
         if (grid > n_lines) grid = n_lines;
         if (a.bounds && grid != Pl->zbounds_n) a.bounds = nullptr;
-        k_zline<P, BND, PU, CU><<<(unsigned)grid, CF::NT, smem, s>>>(m, a, un);
-        wq_count_launches(1);
-        return wq_cuda_status(cudaGetLastError(), "z-line assembly kernel");
+        // one launch per column chunk of t_1
+        wq_status st = WQ_OK;
+        hunroll<CF::NCH>([&](auto CC) {
+            constexpr int CH = decltype(CC)::value;
+            if (st != WQ_OK) return;
+            cudaFuncSetAttribute(k_zline<P, BND, PU, CU, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_zline<P, BND, PU, CU, CH><<<(unsigned)grid, CF::NT, smem, s>>>(m, a, un);
+            wq_count_launches(1);
+            st = wq_cuda_status(cudaGetLastError(), "z-line assembly kernel");
+        });
+        return st;
     }
 }
 
@@ -867,6 +898,8 @@ bool fits_z(int p, int64_t n2l, int64_t nq2l) {
     case 2: return ZCfg<2, BND>::FITS && ZCfg<2, BND>::SMEM + ZCfg<2, BND>::d2_bytes(n2l, nq2l) <= 227 * 1024;
     case 3: return ZCfg<3, BND>::FITS && ZCfg<3, BND>::SMEM + ZCfg<3, BND>::d2_bytes(n2l, nq2l) <= 227 * 1024;
     case 4: return ZCfg<4, BND>::FITS && ZCfg<4, BND>::SMEM + ZCfg<4, BND>::d2_bytes(n2l, nq2l) <= 227 * 1024;
+    case 5: return ZCfg<5, BND>::FITS && ZCfg<5, BND>::SMEM + ZCfg<5, BND>::d2_bytes(n2l, nq2l) <= 227 * 1024;
+    case 6: return ZCfg<6, BND>::FITS && ZCfg<6, BND>::SMEM + ZCfg<6, BND>::d2_bytes(n2l, nq2l) <= 227 * 1024;
     }
     return false;
 }
@@ -914,7 +947,9 @@ bool z_fetch_uniform(wq_plan_s *P, cudaStream_t s, ZUni &U, bool &types_ok) {
             ZFAIL("copy");
         const bool ok = p == 2 ? z_types_match<2>(qlo, qlen, jlo, span, v.n)
                       : p == 3 ? z_types_match<3>(qlo, qlen, jlo, span, v.n)
-                               : z_types_match<4>(qlo, qlen, jlo, span, v.n);
+                      : p == 4 ? z_types_match<4>(qlo, qlen, jlo, span, v.n)
+                      : p == 5 ? z_types_match<5>(qlo, qlen, jlo, span, v.n)
+                               : z_types_match<6>(qlo, qlen, jlo, span, v.n);
         if (!ok) ZFAIL("dir %d: row staircase types do not match", l);
     }
     types_ok = true;
@@ -989,14 +1024,18 @@ wq_status launch_assemble_zline(wq_plan_s *P, int cls, const int32_t *lines, int
     ZUni U;
     memcpy(&U, P->zuni_buf, sizeof(U));
     const bool cu = P->zuni_state == 1;
-    const bool bnd = cls == 2, pu = cls == 0 && cu;
+    // PU keeps each stage-A lane's tables in registers: one fibre per lane (a single stage-A pass)
+    const bool one_pass = P->p == 2 ? ZCfg<2, false>::NPASS == 1 : P->p == 3 ? ZCfg<3, false>::NPASS == 1
+                        : P->p == 4 ? ZCfg<4, false>::NPASS == 1 : P->p == 5 ? ZCfg<5, false>::NPASS == 1
+                                                                  : ZCfg<6, false>::NPASS == 1;
+    const bool bnd = cls == 2, pu = cls == 0 && cu && one_pass;
     switch (P->p * 8 + (bnd ? 4 : 0) + (pu ? 2 : 0) + (cu ? 1 : 0)) {
 #define WQ_ZL(PP, B, PUU, CUU) \
     case PP * 8 + (B ? 4 : 0) + (PUU ? 2 : 0) + (CUU ? 1 : 0): \
         return launch_zline_p<PP, B, PUU, CUU>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, U, s);
 #define WQ_ZLP(PP) WQ_ZL(PP, false, false, false) WQ_ZL(PP, false, false, true) WQ_ZL(PP, false, true, true) \
                    WQ_ZL(PP, true, false, false) WQ_ZL(PP, true, false, true)
-        WQ_ZLP(2) WQ_ZLP(3) WQ_ZLP(4)
+        WQ_ZLP(2) WQ_ZLP(3) WQ_ZLP(4) WQ_ZLP(5) WQ_ZLP(6)
 #undef WQ_ZLP
 #undef WQ_ZL
     }

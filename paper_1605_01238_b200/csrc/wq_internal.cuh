@@ -88,7 +88,7 @@ struct wq_plan_s {
     int32_t *zbounds_dev;          // cost-balanced chunks of the boundary lines for zbounds_n CTAs
     int64_t zbounds_n;
     int zuni_state;
-    double zuni_buf[3 * 9 * 4 + 3 * 2 * 5 * 2];
+    double zuni_buf[3 * 13 * 4 + 3 * 2 * 7 * 2];
 };
 
 // host helpers
