@@ -1025,9 +1025,8 @@ wq_status launch_assemble_zline(wq_plan_s *P, int cls, const int32_t *lines, int
     memcpy(&U, P->zuni_buf, sizeof(U));
     const bool cu = P->zuni_state == 1;
     // PU keeps each stage-A lane's tables in registers: one fibre per lane (a single stage-A pass)
-    const bool one_pass = P->p == 2 ? ZCfg<2, false>::NPASS == 1 : P->p == 3 ? ZCfg<3, false>::NPASS == 1
-                        : P->p == 4 ? ZCfg<4, false>::NPASS == 1 : P->p == 5 ? ZCfg<5, false>::NPASS == 1
-                                                                  : ZCfg<6, false>::NPASS == 1;
+    const bool one_pass = P->p <= 4;  // ZCfg<p, false>::NPASS == 1 (3 (2p+1) <= 32)
+    static_assert(ZCfg<4, false>::NPASS == 1 && ZCfg<5, false>::NPASS > 1, "single-pass degrees");
     const bool bnd = cls == 2, pu = cls == 0 && cu && one_pass;
     switch (P->p * 8 + (bnd ? 4 : 0) + (pu ? 2 : 0) + (cu ? 1 : 0)) {
 #define WQ_ZL(PP, B, PUU, CUU) \
@@ -1035,7 +1034,10 @@ wq_status launch_assemble_zline(wq_plan_s *P, int cls, const int32_t *lines, int
         return launch_zline_p<PP, B, PUU, CUU>(P, lines, n_lines, pl_lo, pl_hi, val, col, val_base, U, s);
 #define WQ_ZLP(PP) WQ_ZL(PP, false, false, false) WQ_ZL(PP, false, false, true) WQ_ZL(PP, false, true, true) \
                    WQ_ZL(PP, true, false, false) WQ_ZL(PP, true, false, true)
-        WQ_ZLP(2) WQ_ZLP(3) WQ_ZLP(4) WQ_ZLP(5) WQ_ZLP(6)
+#define WQ_ZLQ(PP) WQ_ZL(PP, false, false, false) WQ_ZL(PP, false, false, true) \
+                   WQ_ZL(PP, true, false, false) WQ_ZL(PP, true, false, true)
+        WQ_ZLP(2) WQ_ZLP(3) WQ_ZLP(4) WQ_ZLQ(5) WQ_ZLQ(6)
+#undef WQ_ZLQ
 #undef WQ_ZLP
 #undef WQ_ZL
     }
