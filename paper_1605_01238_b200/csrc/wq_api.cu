@@ -181,7 +181,18 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     std::vector<size_t> offs;
     auto take = [&](size_t n) { size_t o = bytes; bytes = align_up(bytes + n); offs.push_back(o); return o; };
     struct Off { size_t knots, pts, span, qlo, qlen, jlo, jlen, pref, B, W; } O[3];
+    // directions with bitwise-identical knot vectors share one set of rules tables (the rules are a
+    // pure function of the knots and p): dir_src[l] = first such direction
+    for (int l = 0; l < 3; ++l) P->dir_src[l] = l;
+    for (int l = 1; l < d; ++l)
+        for (int q = 0; q < l; ++q)
+            if (P->dir_src[q] == q && desc->n_knots[q] == desc->n_knots[l] &&
+                memcmp(desc->knots[q], desc->knots[l], sizeof(double) * (size_t)desc->n_knots[l]) == 0) {
+                P->dir_src[l] = q;
+                break;
+            }
     for (int l = 0; l < d; ++l) {
+        if (P->dir_src[l] != l) continue;
         DirView &v = P->dir[l];
         O[l].knots = take(sizeof(double) * v.nk);
         O[l].pts = take(sizeof(double) * v.nq);
@@ -205,6 +216,12 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     char *A = (char *)arena;
     for (int l = 0; l < d; ++l) {
         DirView &v = P->dir[l];
+        if (P->dir_src[l] != l) {  // alias: the source direction's tables
+            const DirView &u = P->dir[P->dir_src[l]];
+            v.knots = u.knots; v.pts = u.pts; v.span = u.span; v.qlo = u.qlo; v.qlen = u.qlen;
+            v.jlo = u.jlo; v.jlen = u.jlen; v.pref = u.pref; v.B = u.B; v.W = u.W;
+            continue;
+        }
         v.knots = (const double *)(A + O[l].knots);
         v.pts = (double *)(A + O[l].pts);
         v.span = (int32_t *)(A + O[l].span);

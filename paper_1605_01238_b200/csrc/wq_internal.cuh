@@ -46,6 +46,7 @@ struct wq_plan_s {
     int64_t n_dof_total, nnz_total, row_begin, n_rows_local, nnz_local;
     int64_t L[3];                  // sum_i #I_{l,i}
     DirView dir[3];
+    int dir_src[3];                // direction whose rules tables dir[l] shares (identical knots), or l
     // coefficient sub-grid: q_d in [cq_b, cq_e)
     int64_t cq_b, cq_e, coef_points;
     int64_t c0off;                 // d = 3: point q_1 is stored at column q_1 + 1 (c0off = 1), so that

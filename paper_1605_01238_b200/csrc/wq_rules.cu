@@ -396,18 +396,22 @@ __global__ void __launch_bounds__(64) k_weights(DirArgs a, const double *__restr
 }  // namespace
 
 wq_status launch_rules(wq_plan_s *P, cudaStream_t s) {
+    // one set of rules per distinct knot vector (aliased directions share the tables)
     DirArgs a;
-    for (int l = 0; l < 3; ++l) a.v[l] = P->dir[l];
+    int nd = 0;
+    for (int l = 0; l < P->d; ++l)
+        if (P->dir_src[l] == l) a.v[nd++] = P->dir[l];
+    for (int l = nd; l < 3; ++l) a.v[l] = P->dir[l];
     a.p = P->p;
-    a.d = P->d;
+    a.d = nd;
     int64_t maxnq = 0, maxn = 0;
     for (int l = 0; l < P->d; ++l) {
         maxnq = P->dir[l].nq > maxnq ? P->dir[l].nq : maxnq;
         maxn = P->dir[l].n > maxn ? P->dir[l].n : maxn;
     }
-    dim3 g1((unsigned)((maxnq + 127) / 128), P->d);
+    dim3 g1((unsigned)((maxnq + 127) / 128), nd);
     k_grid<<<g1, 128, 0, s>>>(a);
-    dim3 g2((unsigned)((maxn + 1 + 127) / 128), P->d);
+    dim3 g2((unsigned)((maxn + 1 + 127) / 128), nd);
     k_ranges<<<g2, 128, 0, s>>>(a);
     k_gauss<<<1, 32, 0, s>>>(P->p + 1, P->gl);
     k_basis<<<g1, 128, 0, s>>>(a);
@@ -419,7 +423,7 @@ wq_status launch_rules(wq_plan_s *P, cudaStream_t s) {
         cudaFuncSetAttribute(k_weights, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = 1;
     }
-    dim3 g3((unsigned)maxn, P->d);
+    dim3 g3((unsigned)maxn, nd);
     k_weights<<<g3, 64, L.bytes, s>>>(a, P->gl, P->flags, qmax);
     wq_count_launches(5);
     return wq_cuda_status(cudaGetLastError(), "rules kernels");
