@@ -18,9 +18,11 @@ from wqinputs import baseline_config  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--p", type=int, default=4)
 ap.add_argument("--config", default="C4")
+ap.add_argument("--slab", default="0,-1", help="planes [b,e) of the slowest index (one rank of a multi-GPU run)")
 a = ap.parse_args()
 cfg = baseline_config(a.config, a.p)
-plan = wq.Plan(cfg.p, cfg.knots(), need_mass=False, need_stiffness=True)
+plan = wq.Plan(cfg.p, cfg.knots(), slab=tuple(int(x) for x in a.slab.split(",")), need_mass=False,
+               need_stiffness=True)
 ctrl = torch.from_numpy(cfg.ctrl()).cuda()
 rp, col, val = plan.alloc_csr()
 for _ in range(2):
