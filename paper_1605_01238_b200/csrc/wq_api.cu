@@ -85,7 +85,7 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     if (!desc->n_knots || !desc->knots) return fail(WQ_EINVAL, "knots are NULL");
     if (!desc->need_mass && !desc->need_stiffness) return fail(WQ_EINVAL, "need_mass or need_stiffness required");
     wq_plan_s *P = new wq_plan_s();
-    memset(P, 0, sizeof(*P));
+    // value-initialised: POD members zero, vectors empty (no memset over the std::vector members)
     P->d = d;
     P->p = p;
     P->device = desc->device;
