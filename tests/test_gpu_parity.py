@@ -349,3 +349,30 @@ def test_zline_column_chunks(p, E, knots):
     ptr, oc, ov, kappa, scale = o.rows(STIFFNESS, rows)
     gptr, gc, gv = gather_rows_device(rp, col, val, rows)
     compare_rows(rows, gptr, gc, gv, ptr, oc, ov, kappa, scale)
+
+
+@pytest.mark.parametrize("p,E", [(2, 7), (3, 8), (4, 9), (6, 10)])
+def test_zline_graded_knots(p, E):
+    """Non-uniform (graded) knots: the z-line kernel runs with every row's own rules (no uniform
+    tables, reading R16 inapplicable); every row against the oracle."""
+    ks, ctrl = make_case(3, p, E, "grid", 0.08, knots="graded", seed=3)
+    rp, col, val, info = run_full(ks, ctrl, p, STIFFNESS, wq.WQ_KERNEL_ZLINE)
+    o = Oracle(p, ks, ctrl)
+    orp, ocol = o.pattern()
+    assert np.array_equal(rp.cpu().numpy(), orp) and np.array_equal(col.cpu().numpy(), ocol)
+    rows = np.arange(o.ndof)
+    ptr, oc, ov, kappa, scale = o.rows(STIFFNESS, rows)
+    compare_rows(rows, ptr, col.cpu().numpy(), val.cpu().numpy(), ptr, oc, ov, kappa, scale)
+
+
+def test_zline_uniform_rules_switch(monkeypatch):
+    """Reading R16: the uniform-rules tables change values only at the FP64 rounding level of the
+    knots (well inside the R6 tolerance); indices identical."""
+    p, E = 4, 14
+    ks, ctrl = make_case(3, p, E, "annulus", 0.05)
+    _, c1, v1, _ = run_full(ks, ctrl, p, STIFFNESS, wq.WQ_KERNEL_ZLINE)
+    monkeypatch.setenv("WQ_ZLINE_NO_UNIFORM", "1")
+    _, c2, v2, _ = run_full(ks, ctrl, p, STIFFNESS, wq.WQ_KERNEL_ZLINE)
+    assert np.array_equal(c1.cpu().numpy(), c2.cpu().numpy())
+    a, b = v1.cpu().numpy(), v2.cpu().numpy()
+    assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
