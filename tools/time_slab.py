@@ -15,6 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--p", type=int, default=4)
 ap.add_argument("--config", default="C4")
 ap.add_argument("--world", default="1,2,4,8")
+ap.add_argument("--layout", type=int, default=0, help="coefficient layout: 0 library choice (z-line), 1 standard")
 a = ap.parse_args()
 cfg = baseline_config(a.config, a.p)
 ctrl = torch.from_numpy(cfg.ctrl()).cuda()
@@ -23,7 +24,8 @@ for w in [int(x) for x in a.world.split(",")]:
     cuts = slab_cuts(cfg.n_el + cfg.p, cfg.p, w)
     worst = 0.0
     for rank in sorted({0, w // 2, w - 1}):
-        plan = wq.Plan(cfg.p, cfg.knots(), slab=(cuts[rank], cuts[rank + 1]), need_mass=False, need_stiffness=True)
+        plan = wq.Plan(cfg.p, cfg.knots(), slab=(cuts[rank], cuts[rank + 1]), need_mass=False, need_stiffness=True,
+                       coef_layout=a.layout)
         rp, col, val = plan.alloc_csr()
         plan.setup(ctrl)
         wq.wq_pattern(plan.h, 0, rp, None)
