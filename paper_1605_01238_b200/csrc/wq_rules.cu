@@ -309,30 +309,44 @@ __global__ void __launch_bounds__(64) k_weights(DirArgs a, const double *__restr
         for (int q = 0; q < nqi; ++q) mx = fmax(mx, fabs(Mb[r * QM + q].hi));
         if (mx == 0.0) mx = 1.0;
         scb[c] = dd_make(mx);
-        for (int q = 0; q < nqi; ++q) Ab[c * QM + q] = dd_div(Mb[r * QM + q], dd_make(mx));
+        const dd rmx = dd_div(dd_make(1.0), dd_make(mx));  // one division per equation, then products
+        for (int q = 0; q < nqi; ++q) Ab[c * QM + q] = dd_mul(Mb[r * QM + q], rmx);
     }
     __syncwarp();
     // Householder QR of A (nqi x m); lane 0 forms the reflector, lanes update columns
     __shared__ int zero_pivot[2];
     if (lane == 0) zero_pivot[b] = 0;
     __syncwarp();
+    // warp sum of per-lane dd partials (lanes hold the terms q = k + lane, k + lane + 32, ..)
+    auto warp_sum = [&](dd x) {
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            dd y{__shfl_xor_sync(0xffffffffu, x.hi, o), __shfl_xor_sync(0xffffffffu, x.lo, o)};
+            x = dd_add(x, y);
+        }
+        return x;
+    };
     for (int k = 0; k < m && ok; ++k) {
         dd *vk = Vb + k * QM;
-        if (lane == 0) {
-            dd nrm = dd_make(0.0);
-            for (int q = k; q < nqi; ++q) nrm = dd_add(nrm, dd_mul(Ab[k * QM + q], Ab[k * QM + q]));
-            nrm = dd_sqrt(nrm);
-            if (nrm.hi == 0.0) {
-                zero_pivot[b] = 1;
-            } else {
-                dd x0 = Ab[k * QM + k];
-                dd alpha = x0.hi >= 0.0 ? dd_neg(nrm) : nrm;
-                for (int q = k; q < nqi; ++q) vk[q] = Ab[k * QM + q];
-                vk[k] = dd_sub(vk[k], alpha);
-                dd vn = dd_make(0.0);
-                for (int q = k; q < nqi; ++q) vn = dd_add(vn, dd_mul(vk[q], vk[q]));
-                vn = dd_sqrt(vn);
-                for (int q = k; q < nqi; ++q) vk[q] = dd_div(vk[q], vn);
+        dd part = dd_make(0.0);
+        for (int q = k + lane; q < nqi; q += 32) part = dd_add(part, dd_mul(Ab[k * QM + q], Ab[k * QM + q]));
+        const dd nrm = dd_sqrt(warp_sum(part));
+        if (nrm.hi == 0.0) {
+            if (lane == 0) zero_pivot[b] = 1;
+        } else {
+            const dd x0 = Ab[k * QM + k];
+            const dd alpha = x0.hi >= 0.0 ? dd_neg(nrm) : nrm;
+            // v = (a_k - alpha e_k) / |a_k - alpha e_k|
+            dd vpart = dd_make(0.0);
+            for (int q = k + lane; q < nqi; q += 32) {
+                const dd vq = q == k ? dd_sub(Ab[k * QM + q], alpha) : Ab[k * QM + q];
+                vk[q] = vq;
+                vpart = dd_add(vpart, dd_mul(vq, vq));
+            }
+            const dd rvn = dd_div(dd_make(1.0), dd_sqrt(warp_sum(vpart)));
+            for (int q = k + lane; q < nqi; q += 32) vk[q] = dd_mul(vk[q], rvn);
+            __syncwarp();
+            if (lane == 0) {
                 Ab[k * QM + k] = alpha;  // R(k,k)
                 for (int q = k + 1; q < nqi; ++q) Ab[k * QM + q] = dd_make(0.0);
             }
