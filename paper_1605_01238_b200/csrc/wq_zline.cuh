@@ -66,8 +66,8 @@ struct ZPar {
 // keeps the G ring (4 t0c (2p+1) doubles per point) and the registers within the SM
 __host__ __device__ constexpr ZPar z_par(int p, bool bnd) {
     switch (p) {
-    case 2: return bnd ? ZPar{4, 3, 3, 16, 1, 5} : ZPar{4, 3, 3, 16, 2, 5};
-    case 3: return bnd ? ZPar{3, 2, 2, 16, 1, 7} : ZPar{3, 2, 2, 16, 2, 7};
+    case 2: return bnd ? ZPar{4, 3, 3, 32, 1, 5} : ZPar{4, 3, 3, 32, 2, 5};
+    case 3: return bnd ? ZPar{3, 3, 3, 16, 1, 7} : ZPar{3, 3, 3, 32, 2, 7};
     case 4: return bnd ? ZPar{2, 2, 2, 16, 1, 9} : ZPar{2, 2, 2, 16, 2, 9};
     case 5: return bnd ? ZPar{1, 1, 2, 16, 1, 6} : ZPar{1, 2, 2, 16, 1, 6};
     case 6: return bnd ? ZPar{1, 1, 2, 16, 1, 7} : ZPar{1, 2, 2, 16, 1, 7};
