@@ -58,20 +58,21 @@ namespace {
 
 struct ZPar {
     // rows per consumer batch, producer / consumer warps per SM sub-partition (sub-partitions 0, 1
-    // produce, 2, 3 consume), task slots, box buffers per producer, t_1 columns per chunk
-    int nr, rwp, rwc, nts, nb, t0c;
+    // produce, 2, 3 consume), task slots, box buffers per producer, t_1 columns per chunk, consumer
+    // batches as one stream over the CTA's items (1) or restarting at warp 0 on every item (0)
+    int nr, rwp, rwc, nts, nb, t0c, rot;
 };
 // p >= 5: the columns (t_1, t_2) of a line are done in chunks of t0c values of t_1 (one launch per
 // chunk; stage A/B work splits without redundancy, only the coefficient boxes are re-read), which
 // keeps the G ring (4 t0c (2p+1) doubles per point) and the registers within the SM
 __host__ __device__ constexpr ZPar z_par(int p, bool bnd) {
     switch (p) {
-    case 2: return bnd ? ZPar{4, 3, 3, 32, 1, 5} : ZPar{4, 3, 3, 32, 2, 5};
+    case 2: return bnd ? ZPar{4, 3, 3, 32, 1, 5, 1} : ZPar{4, 3, 3, 32, 2, 5, 1};
     case 3: return bnd ? ZPar{3, 3, 3, 16, 1, 7} : ZPar{3, 3, 3, 32, 2, 7};
     case 4: return bnd ? ZPar{2, 2, 2, 16, 1, 9} : ZPar{2, 2, 2, 16, 2, 9};
     case 5: return bnd ? ZPar{1, 1, 2, 16, 1, 6} : ZPar{1, 2, 2, 16, 1, 6};
     case 6: return bnd ? ZPar{1, 1, 2, 16, 1, 7} : ZPar{1, 2, 2, 16, 1, 7};
-    default: return {0, 0, 0, 0, 0, 0};
+    default: return {0, 0, 0, 0, 0, 0, 0};
     }
 }
 
@@ -93,6 +94,7 @@ struct ZCfg {
     static constexpr int NT = 128 * (RWP > RWC ? RWP : RWC);
     static constexpr int NTS = ENABLED ? W.nts : 2;
     static constexpr int NB = ENABLED ? W.nb : 1;
+    static constexpr bool ROT = W.rot != 0;
     static constexpr int RING = 2 * NTS;
     static constexpr int QX = BND ? QB : QI;         // box / table extent in directions 0, 1
     static constexpr int NF = 3 * QX;                // stage-A fibres (m, c1)
@@ -611,10 +613,27 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                      "l"(v2.W + (int64_t)(i2b + r0) * mq2 * 4), "r"(bytes), "r"(smem_u32(&wfull[cw * 2 + buf]))
                      : "memory");
     };
-    const int my_first = cw * NR;
+    // ROT: the batches of the CTA's items form one round-robin stream over the consumer warps (batch
+    // b of item k is stream position k nb + b): the warp after the one that took a line's last batch
+    // takes the next line's first, so the extra batch of a ragged line and the generic (non-uniform)
+    // rows at the line ends rotate over the warps instead of always landing on warp 0 (measured: p = 2
+    // 2.00 -> 1.74 ms at C4; p = 3 slower, 3.25 -> 3.39 ms; p = 4 unchanged: 52 batches per line)
+    const int nbl = (n2l + NR - 1) / NR;
+    auto first_row = [&](int64_t k) {
+        return (int)((cw + NWC - (CF::ROT ? (int)((k * nbl) % NWC) : 0)) % NWC) * NR;
+    };
+    // first row of the first item >= k in which this warp has a batch (-1: none left)
+    auto next_first = [&](int64_t k) {
+        for (int64_t k2 = k; k2 < my_items && k2 < k + NWC; ++k2)
+            if (first_row(k2) < n2l) return first_row(k2);
+        return -1;
+    };
     int wbuf = 0;
     unsigned wuse[2] = {0, 0};
-    if (lane == 0 && my_first < n2l && my_items > 0) w2_issue(my_first, 0);
+    if (lane == 0) {
+        const int f0 = next_first(0);
+        if (f0 >= 0) w2_issue(f0, 0);
+    }
     uint32_t got = 0, rel = 0, Tbase = 0;  // tasks waited for / released, first task of the item
     for (int64_t ik_ = 0; ik_ < my_items; ++ik_) {
         const ZItem I = z_item(a, item_of(ik_));
@@ -629,7 +648,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
         const int nc01 = I.ni0 * I.ni1;
         const int64_t A = v1.pref[I.i1] * a.L0 + (int64_t)I.ni1 * v0.pref[I.i0];
         const int64_t L01 = a.L0 * a.L1;
-        for (int r0 = cw * NR; r0 < n2l; r0 += NWC * NR) {
+        for (int r0 = first_row(ik_); r0 < n2l; r0 += NWC * NR) {
             const int nr = n2l - r0 < NR ? n2l - r0 : NR;
             const int rl = r0 + nr - 1;
             const uint32_t t_hi = Tbase + (uint32_t)((qlo2[rl] + qlen2[rl] - 1) / 2);
@@ -640,7 +659,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             if (lane == 0) {
                 int nxt = r0 + NWC * NR;
                 bool more = true;
-                if (nxt >= n2l) { nxt = my_first; more = ik_ + 1 < my_items; }
+                if (nxt >= n2l) { nxt = next_first(ik_ + 1); more = nxt >= 0; }
                 if (more) w2_issue(nxt, wbuf ^ 1);
             }
             wbuf ^= 1;
