@@ -279,10 +279,13 @@ __global__ void k_dnet(const double *__restrict__ P, double *__restrict__ Q, Dir
         Q[k * 9 + 6 + c] = k2 >= 1 ? (cur - P[(k - n0 * n1) * 3 + c]) * s2 : 0.0;
     }
 }
-template <int TQM>
+// PP > 0: the degree as a compile-time constant (p <= 6), so that the r loops unroll and each thread
+// issues all of its derivative-net loads of stage A before the first FMA (the kernel is bound by
+// their L2 latency); PP = 0: any degree
+template <int TQM, int PP>
 __global__ void __launch_bounds__(TQF * TQM) k_coefz(CoefArgs a) {
     extern __shared__ __align__(16) double sm[];
-    const int p = a.p;
+    const int p = PP > 0 ? PP : a.p;
     const DirView &v0 = a.v[0], &v1 = a.v[1], &v2 = a.v[2];
     const int64_t q1p = blockIdx.z;  // plane (direction 2)
     const int64_t qfa = (int64_t)blockIdx.x * TQF, qma = (int64_t)blockIdx.y * TQM;  // q_3 local, q_1
@@ -309,6 +312,7 @@ __global__ void __launch_bounds__(TQF * TQM) k_coefz(CoefArgs a) {
             const int cf = t / KM, cm = t % KM;
             const int64_t k0 = kma + cm, k2 = kfa + cf;
             double A0[3] = {0, 0, 0}, A1[3] = {0, 0, 0}, A2[3] = {0, 0, 0};
+            #pragma unroll
             for (int r = 0; r <= p; ++r) {
                 const int64_t k = k0 + n0 * (e1 + r + n1 * k2);
                 const double nv = nt[2 * r], mv = r >= 1 ? mt[r - 1] : 0.0;
@@ -335,6 +339,7 @@ __global__ void __launch_bounds__(TQF * TQM) k_coefz(CoefArgs a) {
         const double *nt = Ntab(v0, p, q0), *mt = Mtab(v0, p, q0);
         const int cms = (int)(v0.span[q0] - kma);
         double X0[3] = {0, 0, 0}, X1[3] = {0, 0, 0}, X2[3] = {0, 0, 0};
+        #pragma unroll
         for (int r = 0; r <= p; ++r) {
             const double nv = nt[2 * r], mv = r < p ? mt[r] : 0.0;
             #pragma unroll
@@ -364,6 +369,7 @@ __global__ void __launch_bounds__(TQF * TQM) k_coefz(CoefArgs a) {
         #pragma unroll
         for (int m = 0; m < 3; ++m) J[c][m] = 0.0;
     const double *X = Xsm + (tm * 3) * 3 * KFM;
+    #pragma unroll
     for (int r = 0; r <= p; ++r) {
         const double nv = nt[2 * r], mv = r < p ? mt[r] : 0.0;
         #pragma unroll
@@ -443,17 +449,26 @@ wq_status launch_coef(wq_plan_s *P, const double *ctrl, cudaStream_t s) {
         wq_count_launches(1);
         a.dnet = P->dnet;
         const int tqm = getenv("WQ_COEF_TQM") ? atoi(getenv("WQ_COEF_TQM")) : 16;  // tile height (tuning experiments)
-        auto run = [&](auto TT) {
-            constexpr int TQM = decltype(TT)::value;
+        auto run = [&](auto TT, auto PPc) {
+            constexpr int TQM = decltype(TT)::value, PP = decltype(PPc)::value;
             const size_t sm = (size_t)(9 * (TQM + P->p + 1) * (TQF + P->p + 1) + TQM * 9 * (TQF + P->p + 1)) * sizeof(double);
-            cudaFuncSetAttribute(k_coefz<TQM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(k_coefz<TQM, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
             dim3 g((unsigned)((a.nq_loc_d + TQF - 1) / TQF), (unsigned)((P->dir[0].nq + TQM - 1) / TQM), (unsigned)P->dir[1].nq);
-            k_coefz<TQM><<<g, TQF * TQM, sm, s>>>(a);
+            k_coefz<TQM, PP><<<g, TQF * TQM, sm, s>>>(a);
         };
-        if (tqm == 4) run(std::integral_constant<int, 4>{});
-        else if (tqm == 16) run(std::integral_constant<int, 16>{});
-        else if (tqm == 2) run(std::integral_constant<int, 2>{});
-        else run(std::integral_constant<int, 8>{});
+        auto run_p = [&](auto TT) {
+            switch (P->p) {
+            case 2: run(TT, std::integral_constant<int, 2>{}); break;
+            case 3: run(TT, std::integral_constant<int, 3>{}); break;
+            case 4: run(TT, std::integral_constant<int, 4>{}); break;
+            case 5: run(TT, std::integral_constant<int, 5>{}); break;
+            case 6: run(TT, std::integral_constant<int, 6>{}); break;
+            default: run(TT, std::integral_constant<int, 0>{}); break;
+            }
+        };
+        if (tqm == 4) run_p(std::integral_constant<int, 4>{});
+        else if (tqm == 16) run_p(std::integral_constant<int, 16>{});
+        else run_p(std::integral_constant<int, 8>{});
     } else if (P->d == 3) {
         size_t sm = (size_t)(9 * K2M * K1M + TQ2 * 9 * K1M) * sizeof(double);
         static bool set = false;
