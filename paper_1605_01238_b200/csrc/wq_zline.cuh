@@ -95,6 +95,9 @@ struct ZCfg {
     static constexpr int NTS = ENABLED ? W.nts : 2;
     static constexpr int NB = ENABLED ? W.nb : 1;
     static constexpr bool ROT = W.rot != 0;
+    // boundary lines: three staircase groups instead of 2P+3 row types (ZTy::group; the full set of
+    // unrolled staircases overflows the instruction cache: 40 % no-instruction stalls at p = 4)
+    static constexpr bool ZMERGE = BND && NCH == 1;
     static constexpr int RING = 2 * NTS;
     static constexpr int QX = BND ? QB : QI;         // box / table extent in directions 0, 1
     static constexpr int NF = 3 * QX;                // stage-A fibres (m, c1)
@@ -155,6 +158,14 @@ struct ZTy {
         if (i >= n - 1 - P) return (int)(n - 1 - i) + P + 2;
         return 0;
     }
+    // Staircase groups (boundary-line kernel): every left type is a prefix of the longest left type
+    // P+1 (the extra points get zero weights), and right type i' equals the longest right type 2P+2
+    // on points shifted by 2 sh, sh = P - i', with every offset raised by sh:
+    //   off(2P+2, c + 2 sh) = off(t, c) + sh.
+    // So three staircases (interior, left P+1, right 2P+2) serve all 2P+3 types: the box and tables
+    // start 2 sh points earlier (zero weights there) and the results are written sh slots lower.
+    __host__ __device__ static constexpr int group(int t) { return t == 0 ? 0 : (t <= P + 1 ? P + 1 : 2 * P + 2); }
+    __host__ __device__ static constexpr int shift(int t) { return t <= P + 1 ? 0 : 2 * P + 2 - t; }
 };
 // f(integral_constant<t>) for the runtime row type t in [0, 2P+2]
 template <int P, int T = 0, class F>
@@ -324,6 +335,11 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
         const int wp = ZMIXED ? warp : wrow * 2 + smsp;
         double *wbase = Boxes + wp * (NB * BOXD + CF::YD);
         double *Ybuf = wbase + NB * BOXD;  // YSEP only
+        if constexpr (CF::ZMERGE) {
+            // group staircases read Y rows beyond the row's points (times zero tables): keep them finite
+            for (int x = lane; x < CF::YD; x += 32) Ybuf[x] = 0.0;
+            __syncwarp();
+        }
         double *tab = Tabs + wp * CF::TABD;
         // line tables: T0[sel][c0][NPP], T1[sel][c1][NPP] (sel 0: derivative, 1: value; r padded to
         // NPP so that (r, r+1) pairs load as one 16-B word), W0t / W1t [c][f] (f = a + 2b)
@@ -340,6 +356,10 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             if (is_k != ik) {
                 const ZItem I = z_item(a, item_of(is_k));
                 ik = is_k; iq0 = I.ql0; iq1 = I.ql1;
+                if (CF::ZMERGE) {
+                    iq0 -= 2 * ZTy<P>::shift(ZTy<P>::type(I.i0, a.v[0].n));
+                    iq1 -= 2 * ZTy<P>::shift(ZTy<P>::type(I.i1, a.v[1].n));
+                }
             }
             if (ZDBG(8)) {
                 mbar_arrive(&pfull[wp * NB + b]);  // debug ablation: no box load
@@ -384,7 +404,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             w1u0 = u.w[1][c1][m == 1 ? 2 : 0];
             w1u1 = u.w[1][c1][m == 1 ? 3 : 1];
         }
-        int cq0 = QI, cq1 = QI, ty0 = 0, ty1 = 0;
+        int cq0 = QI, cq1 = QI, ty0 = 0, ty1 = 0, sh0 = 0, sh1 = 0;
         int use = 0;
         for (int64_t T = wp; T < n_tasks; T += NWP, ++use) {
             const int b = NB == 2 ? (use & 1) : 0;
@@ -401,16 +421,23 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     cq0 = I.nq0; cq1 = I.nq1;
                     ty0 = ZTy<P>::type(I.i0, v0.n);
                     ty1 = ZTy<P>::type(I.i1, v1.n);
+                    if (CF::ZMERGE) {
+                        sh0 = ZTy<P>::shift(ty0); sh1 = ZTy<P>::shift(ty1);
+                        ty0 = ZTy<P>::group(ty0); ty1 = ZTy<P>::group(ty1);
+                        cq0 += 2 * sh0; cq1 += 2 * sh1;
+                    }
                 }
+                // tables over the box's points c (the row's points start at c = 2 sh)
+                const int64_t tq0 = I.ql0 - 2 * sh0, tq1 = I.ql1 - 2 * sh1;
                 for (int x = lane; x < QX * NPP; x += 32) {
                     const int c = x / NPP, r = x % NPP;
-                    const double2 b0 = c < cq0 && r < NP ? __ldg((const double2 *)(v0.B + (int64_t)(I.ql0 + c) * BS) + r) : make_double2(0.0, 0.0);
-                    const double2 b1 = c < cq1 && r < NP ? __ldg((const double2 *)(v1.B + (int64_t)(I.ql1 + c) * BS) + r) : make_double2(0.0, 0.0);
+                    const double2 b0 = c < cq0 && r < NP ? __ldg((const double2 *)(v0.B + (tq0 + c) * BS) + r) : make_double2(0.0, 0.0);
+                    const double2 b1 = c < cq1 && r < NP ? __ldg((const double2 *)(v1.B + (tq1 + c) * BS) + r) : make_double2(0.0, 0.0);
                     T0[x] = b0.y; T0[QX * NPP + x] = b0.x; T1[x] = b1.y; T1[QX * NPP + x] = b1.x;
                 }
                 for (int x = lane; x < 4 * QX; x += 32) {
-                    W0t[x] = x / 4 < cq0 ? __ldg(v0.W + (int64_t)I.i0 * v0.maxq * 4 + x) : 0.0;
-                    W1t[x] = x / 4 < cq1 ? __ldg(v1.W + (int64_t)I.i1 * v1.maxq * 4 + x) : 0.0;
+                    W0t[x] = x / 4 >= 2 * sh0 && x / 4 < cq0 ? __ldg(v0.W + (int64_t)I.i0 * v0.maxq * 4 + x - 8 * sh0) : 0.0;
+                    W1t[x] = x / 4 >= 2 * sh1 && x / 4 < cq1 ? __ldg(v1.W + (int64_t)I.i1 * v1.maxq * 4 + x - 8 * sh1) : 0.0;
                 }
                 __syncwarp();
             }
@@ -424,7 +451,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             // ---------------- stage A: fibre (m, c1), both points, chains a2 = 0 (y0), 1 (y1)
             // Y: block m*2+a2 at CF::yoff, [c1][t0][pt] inside; interior: over the consumed box
             double *Y = YSEP ? Ybuf : wbase + b * BOXD;
-            #pragma unroll
+            #pragma unroll(CF::ZMERGE ? 1 : CF::NPASS)
             for (int pass = 0; pass < CF::NPASS; ++pass) {
                 // boundary lines: the 3 #Q_1 fibres of this line packed densely (one pass when #Q_1 <= 10)
                 if (BND && 32 * pass >= 3 * cq1) break;
@@ -472,7 +499,24 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                             }
                         }
                     };
-                    if constexpr (BND) {
+                    if constexpr (CF::ZMERGE) {
+                        // the group staircases as one unrolled interior staircase over a range of
+                        // its points plus a rolled loop over the flat part (ZTy::group): left
+                        // [0]*(P+1) + interior points 1..2P; right interior points 0..2P-2 + [P]*(P+2)
+                        const int base = ty0 == P + 1 ? P : 0, clo = ty0 == P + 1 ? 1 : 0,
+                                  chi = ty0 == 2 * P + 2 ? 2 * P - 2 : 2 * P;
+                        unroll<QI>([&](auto C0) {
+                            constexpr int c0 = decltype(C0)::value;
+                            if (c0 >= clo && c0 <= chi) plane(base + c0, std::integral_constant<int, (c0 + 1) / 2>{});
+                        });
+                        if (ty0 == P + 1) {
+                            #pragma unroll 1
+                            for (int c0 = 0; c0 <= P; ++c0) plane(c0, std::integral_constant<int, 0>{});
+                        } else if (ty0 == 2 * P + 2) {
+                            #pragma unroll 1
+                            for (int c0 = 2 * P - 1; c0 <= 3 * P; ++c0) plane(c0, std::integral_constant<int, P>{});
+                        }
+                    } else if constexpr (BND) {
                         zdispatch<P>(ty0, [&](auto TT) {
                             constexpr int t = decltype(TT)::value;
                             unroll<ZTy<P>::nq(t)>([&](auto C0) {
@@ -493,8 +537,13 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     double *Y1 = Y + CF::yoff(m * 2 + 1) + c1 * T0C * 2;
                     #pragma unroll
                     for (int t = 0; t < T0C; ++t) {
-                        *(double2 *)(Y0 + t * 2) = make_double2(y0[0][t], y0[1][t]);
-                        *(double2 *)(Y1 + t * 2) = make_double2(y1[0][t], y1[1][t]);
+                        // ZMERGE: slot t of the group staircase is slot t - sh0 of the row (slots at
+                        // and above #I_0 - sh0... are dead columns, never read as live)
+                        const int td = CF::ZMERGE ? t - sh0 : t;
+                        if (td >= 0) {
+                            *(double2 *)(Y0 + td * 2) = make_double2(y0[0][t], y0[1][t]);
+                            *(double2 *)(Y1 + td * 2) = make_double2(y1[0][t], y1[1][t]);
+                        }
                     }
                 }
             }
@@ -538,7 +587,21 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                         }
                     }
                 };
-                if constexpr (BND) {
+                if constexpr (CF::ZMERGE) {
+                    const int base = ty1 == P + 1 ? P : 0, clo = ty1 == P + 1 ? 1 : 0,
+                              chi = ty1 == 2 * P + 2 ? 2 * P - 2 : 2 * P;
+                    unroll<QI>([&](auto C1) {
+                        constexpr int c1 = decltype(C1)::value;
+                        if (c1 >= clo && c1 <= chi) point1(base + c1, std::integral_constant<int, (c1 + 1) / 2>{});
+                    });
+                    if (ty1 == P + 1) {
+                        #pragma unroll 1
+                        for (int c1 = 0; c1 <= P; ++c1) point1(c1, std::integral_constant<int, 0>{});
+                    } else if (ty1 == 2 * P + 2) {
+                        #pragma unroll 1
+                        for (int c1 = 2 * P - 1; c1 <= 3 * P; ++c1) point1(c1, std::integral_constant<int, P>{});
+                    }
+                } else if constexpr (BND) {
                     zdispatch<P>(ty1, [&](auto TT) {
                         constexpr int t = decltype(TT)::value;
                         unroll<ZTy<P>::nq(t)>([&](auto C1) {
@@ -571,7 +634,8 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     for (int t = 0; t < K; ++t) {  // t = t_2; column t0 + T0C t
                         const double v = fma(g[1][pt][t], sum1, g[0][pt][t]);
                         const double o = __shfl_down_sync(0xffffffffu, v, T0C);
-                        if (fl && fg != 1) Gd[T0C * t] = make_double2(v, fg == 0 ? o : g[1][pt][t]);
+                        const int td = CF::ZMERGE ? t - sh1 : t;  // slot of the row (see ZTy::shift)
+                        if (fl && fg != 1 && td >= 0) Gd[T0C * td] = make_double2(v, fg == 0 ? o : g[1][pt][t]);
                     }
                 }
             }
