@@ -97,7 +97,7 @@ struct ZCfg {
     static constexpr bool ROT = W.rot != 0;
     // boundary lines: three staircase groups instead of 2P+3 row types (ZTy::group; the full set of
     // unrolled staircases overflows the instruction cache: 40 % no-instruction stalls at p = 4)
-    static constexpr bool ZMERGE = BND && NCH == 1;
+    static constexpr bool ZMERGE = BND && NCH == 1 && P >= 3;
     static constexpr int RING = 2 * NTS;
     static constexpr int QX = BND ? QB : QI;         // box / table extent in directions 0, 1
     static constexpr int NF = 3 * QX;                // stage-A fibres (m, c1)
