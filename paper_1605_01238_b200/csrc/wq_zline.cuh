@@ -67,9 +67,9 @@ struct ZPar {
 // keeps the G ring (4 t0c (2p+1) doubles per point) and the registers within the SM
 __host__ __device__ constexpr ZPar z_par(int p, bool bnd) {
     switch (p) {
-    case 2: return bnd ? ZPar{4, 3, 3, 32, 1, 5, 1} : ZPar{4, 3, 3, 32, 2, 5, 1};
-    case 3: return bnd ? ZPar{3, 3, 3, 16, 1, 7} : ZPar{3, 3, 3, 32, 2, 7};
-    case 4: return bnd ? ZPar{2, 2, 2, 16, 1, 9} : ZPar{2, 2, 2, 16, 2, 9};
+    case 2: return bnd ? ZPar{2, 3, 3, 32, 1, 5, 1} : ZPar{4, 3, 3, 32, 2, 5, 1};
+    case 3: return bnd ? ZPar{1, 3, 3, 16, 1, 7} : ZPar{1, 3, 3, 32, 2, 7};
+    case 4: return bnd ? ZPar{1, 2, 2, 16, 1, 9} : ZPar{1, 2, 2, 16, 2, 9};
     case 5: return bnd ? ZPar{1, 1, 2, 16, 1, 6} : ZPar{1, 2, 2, 16, 1, 6};
     case 6: return bnd ? ZPar{1, 1, 2, 16, 1, 7} : ZPar{1, 2, 2, 16, 1, 7};
     default: return {0, 0, 0, 0, 0, 0, 0};
@@ -97,7 +97,10 @@ struct ZCfg {
     static constexpr bool ROT = W.rot != 0;
     // boundary lines: three staircase groups instead of 2P+3 row types (ZTy::group; the full set of
     // unrolled staircases overflows the instruction cache: 40 % no-instruction stalls at p = 4)
-    static constexpr bool ZMERGE = BND && NCH == 1 && P >= 3;
+    // ZMA: direction 0 (stage A) - only without column chunks (the shift moves slots across chunks);
+    // ZMB: direction 1 (stage B)
+    static constexpr bool ZMA = BND && NCH == 1 && P >= 3;
+    static constexpr bool ZMB = BND && P >= 3;
     static constexpr int RING = 2 * NTS;
     static constexpr int QX = BND ? QB : QI;         // box / table extent in directions 0, 1
     static constexpr int NF = 3 * QX;                // stage-A fibres (m, c1)
@@ -335,7 +338,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
         const int wp = ZMIXED ? warp : wrow * 2 + smsp;
         double *wbase = Boxes + wp * (NB * BOXD + CF::YD);
         double *Ybuf = wbase + NB * BOXD;  // YSEP only
-        if constexpr (CF::ZMERGE) {
+        if constexpr (CF::ZMB) {
             // group staircases read Y rows beyond the row's points (times zero tables): keep them finite
             for (int x = lane; x < CF::YD; x += 32) Ybuf[x] = 0.0;
             __syncwarp();
@@ -356,10 +359,8 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             if (is_k != ik) {
                 const ZItem I = z_item(a, item_of(is_k));
                 ik = is_k; iq0 = I.ql0; iq1 = I.ql1;
-                if (CF::ZMERGE) {
-                    iq0 -= 2 * ZTy<P>::shift(ZTy<P>::type(I.i0, a.v[0].n));
-                    iq1 -= 2 * ZTy<P>::shift(ZTy<P>::type(I.i1, a.v[1].n));
-                }
+                if (CF::ZMA) iq0 -= 2 * ZTy<P>::shift(ZTy<P>::type(I.i0, a.v[0].n));
+                if (CF::ZMB) iq1 -= 2 * ZTy<P>::shift(ZTy<P>::type(I.i1, a.v[1].n));
             }
             if (ZDBG(8)) {
                 mbar_arrive(&pfull[wp * NB + b]);  // debug ablation: no box load
@@ -421,10 +422,15 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     cq0 = I.nq0; cq1 = I.nq1;
                     ty0 = ZTy<P>::type(I.i0, v0.n);
                     ty1 = ZTy<P>::type(I.i1, v1.n);
-                    if (CF::ZMERGE) {
-                        sh0 = ZTy<P>::shift(ty0); sh1 = ZTy<P>::shift(ty1);
-                        ty0 = ZTy<P>::group(ty0); ty1 = ZTy<P>::group(ty1);
-                        cq0 += 2 * sh0; cq1 += 2 * sh1;
+                    if (CF::ZMA) {
+                        sh0 = ZTy<P>::shift(ty0);
+                        ty0 = ZTy<P>::group(ty0);
+                        cq0 += 2 * sh0;
+                    }
+                    if (CF::ZMB) {
+                        sh1 = ZTy<P>::shift(ty1);
+                        ty1 = ZTy<P>::group(ty1);
+                        cq1 += 2 * sh1;
                     }
                 }
                 // tables over the box's points c (the row's points start at c = 2 sh)
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             // ---------------- stage A: fibre (m, c1), both points, chains a2 = 0 (y0), 1 (y1)
             // Y: block m*2+a2 at CF::yoff, [c1][t0][pt] inside; interior: over the consumed box
             double *Y = YSEP ? Ybuf : wbase + b * BOXD;
-            #pragma unroll(CF::ZMERGE ? 1 : CF::NPASS)
+            #pragma unroll(CF::ZMB ? 1 : CF::NPASS)
             for (int pass = 0; pass < CF::NPASS; ++pass) {
                 // boundary lines: the 3 #Q_1 fibres of this line packed densely (one pass when #Q_1 <= 10)
                 if (BND && 32 * pass >= 3 * cq1) break;
@@ -499,7 +505,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                             }
                         }
                     };
-                    if constexpr (CF::ZMERGE) {
+                    if constexpr (CF::ZMA) {
                         // the group staircases as one unrolled interior staircase over a range of
                         // its points plus a rolled loop over the flat part (ZTy::group): left
                         // [0]*(P+1) + interior points 1..2P; right interior points 0..2P-2 + [P]*(P+2)
@@ -537,9 +543,9 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     double *Y1 = Y + CF::yoff(m * 2 + 1) + c1 * T0C * 2;
                     #pragma unroll
                     for (int t = 0; t < T0C; ++t) {
-                        // ZMERGE: slot t of the group staircase is slot t - sh0 of the row (slots at
+                        // ZMA: slot t of the group staircase is slot t - sh0 of the row (slots at
                         // and above #I_0 - sh0... are dead columns, never read as live)
-                        const int td = CF::ZMERGE ? t - sh0 : t;
+                        const int td = CF::ZMA ? t - sh0 : t;
                         if (td >= 0) {
                             *(double2 *)(Y0 + td * 2) = make_double2(y0[0][t], y0[1][t]);
                             *(double2 *)(Y1 + td * 2) = make_double2(y1[0][t], y1[1][t]);
@@ -587,7 +593,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                         }
                     }
                 };
-                if constexpr (CF::ZMERGE) {
+                if constexpr (CF::ZMB) {
                     const int base = ty1 == P + 1 ? P : 0, clo = ty1 == P + 1 ? 1 : 0,
                               chi = ty1 == 2 * P + 2 ? 2 * P - 2 : 2 * P;
                     unroll<QI>([&](auto C1) {
@@ -634,7 +640,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                     for (int t = 0; t < K; ++t) {  // t = t_2; column t0 + T0C t
                         const double v = fma(g[1][pt][t], sum1, g[0][pt][t]);
                         const double o = __shfl_down_sync(0xffffffffu, v, T0C);
-                        const int td = CF::ZMERGE ? t - sh1 : t;  // slot of the row (see ZTy::shift)
+                        const int td = CF::ZMB ? t - sh1 : t;  // slot of the row (see ZTy::shift)
                         if (fl && fg != 1 && td >= 0) Gd[T0C * td] = make_double2(v, fg == 0 ? o : g[1][pt][t]);
                     }
                 }
