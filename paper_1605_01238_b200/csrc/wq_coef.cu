@@ -303,32 +303,25 @@ __global__ void __launch_bounds__(TQF * TQM) k_coefz(CoefArgs a) {
     const double *P = a.ctrl;
     const int64_t n0 = v0.n, n1 = v1.n;
     {
-        // stage A: contract k_2 with the plane's basis; threads over (k_3, k_1), k_1 fastest;
-        // derivative nets from k_dnet
+        // stage A: contract k_2 with the plane's basis.  Threads over (k_3, e) with e = (k_1 - kma)*9 +
+        // 3*variant + comp: for fixed (k_2, k_3) the derivative-net entries of the tile's k_1 range are
+        // one contiguous run, so consecutive threads load consecutive doubles (coalesced); every
+        // entry is an independent sum over k_2 (variants 0, 2 with N2, variant 1 with M2)
         const double *nt = Ntab(v1, p, q1p), *mt = Mtab(v1, p, q1p);
         const int64_t e1 = v1.span[q1p];
         const double *Q = a.dnet;
-        for (int t = tid; t < KF * KM; t += blockDim.x) {
-            const int cf = t / KM, cm = t % KM;
-            const int64_t k0 = kma + cm, k2 = kfa + cf;
-            double A0[3] = {0, 0, 0}, A1[3] = {0, 0, 0}, A2[3] = {0, 0, 0};
+        const int KE = KM * 9;
+        for (int t = tid; t < KF * KE; t += blockDim.x) {
+            const int cf = t / KE, e = t % KE;
+            const int cm = e / 9, vc = e % 9, var = vc / 3;
+            const double *Qe = Q + (kma + n0 * (e1 + n1 * (kfa + cf))) * 9 + e;
+            double acc = 0.0;
             #pragma unroll
             for (int r = 0; r <= p; ++r) {
-                const int64_t k = k0 + n0 * (e1 + r + n1 * k2);
-                const double nv = nt[2 * r], mv = r >= 1 ? mt[r - 1] : 0.0;
-                #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    A0[c] = fma(nv, __ldg(Q + k * 9 + 0 + c), A0[c]);
-                    A2[c] = fma(nv, __ldg(Q + k * 9 + 6 + c), A2[c]);
-                    if (r >= 1) A1[c] = fma(mv, __ldg(Q + k * 9 + 3 + c), A1[c]);
-                }
+                const double w = var == 1 ? (r >= 1 ? mt[r - 1] : 0.0) : nt[2 * r];
+                if (var != 1 || r >= 1) acc = fma(w, __ldg(Qe + r * n0 * 9), acc);
             }
-            #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                Asm[((0 * 3 + c) * KFM + cf) * KMM + cm] = A0[c];
-                Asm[((1 * 3 + c) * KFM + cf) * KMM + cm] = A1[c];
-                Asm[((2 * 3 + c) * KFM + cf) * KMM + cm] = A2[c];
-            }
+            Asm[(vc * KFM + cf) * KMM + cm] = acc;
         }
     }
     __syncthreads();
