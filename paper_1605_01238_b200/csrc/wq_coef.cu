@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(TQF * TQM) k_coefz(CoefArgs a) {
     const int KF = (int)(kfe - kfa), KM = (int)(kme - kma);
     const int KFM = TQF + p + 1, KMM = TQM + p + 1;
     double *Asm = sm;                      // [3 variants][3 comps][KFM][KMM]  (k_1 fastest)
-    double *Xsm = sm + 9 * KMM * KFM;      // [TQM][3 variants][3 comps][KFM]
+    double *Xsm = sm;                      // [TQM][3 variants][3 comps][KFM], over Asm once stage B has read it
     const int tid = threadIdx.x;
     const double *P = a.ctrl;
     const int64_t n0 = v0.n, n1 = v1.n;
@@ -325,8 +325,15 @@ __global__ void __launch_bounds__(TQF * TQM) k_coefz(CoefArgs a) {
         }
     }
     __syncthreads();
-    // stage B: contract k_1 for each q_1 point of the tile
-    for (int t = tid; t < ntm * KF; t += blockDim.x) {
+    // stage B: contract k_1 for each q_1 point of the tile.  A thread's (at most XIT) items are held in
+    // registers until every thread has read Asm, then X is written over it (smem per CTA = max of
+    // the two arrays instead of their sum: one more CTA per SM)
+    constexpr int XIT = 2;  // ceil((TQF + p + 1) / TQF) items per thread for p < TQF
+    double Xr[XIT][9];
+    #pragma unroll
+    for (int it = 0; it < XIT; ++it) {
+        const int t = tid + it * (int)blockDim.x;
+        if (t >= ntm * KF) break;
         const int tm = t / KF, cf = t % KF;
         const int64_t q0 = qma + tm;
         const double *nt = Ntab(v0, p, q0), *mt = Mtab(v0, p, q0);
@@ -343,11 +350,16 @@ __global__ void __launch_bounds__(TQF * TQM) k_coefz(CoefArgs a) {
             }
         }
         #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            Xsm[((tm * 3 + 0) * 3 + c) * KFM + cf] = X0[c];
-            Xsm[((tm * 3 + 1) * 3 + c) * KFM + cf] = X1[c];
-            Xsm[((tm * 3 + 2) * 3 + c) * KFM + cf] = X2[c];
-        }
+        for (int c = 0; c < 3; ++c) { Xr[it][c] = X0[c]; Xr[it][3 + c] = X1[c]; Xr[it][6 + c] = X2[c]; }
+    }
+    __syncthreads();
+    #pragma unroll
+    for (int it = 0; it < XIT; ++it) {
+        const int t = tid + it * (int)blockDim.x;
+        if (t >= ntm * KF) break;
+        const int tm = t / KF, cf = t % KF;
+        #pragma unroll
+        for (int vc = 0; vc < 9; ++vc) Xsm[(tm * 9 + vc) * KFM + cf] = Xr[it][vc];
     }
     __syncthreads();
     // stage C: one thread per point (q_3 fastest)
@@ -444,7 +456,8 @@ wq_status launch_coef(wq_plan_s *P, const double *ctrl, cudaStream_t s) {
         const int tqm = getenv("WQ_COEF_TQM") ? atoi(getenv("WQ_COEF_TQM")) : 16;  // tile height (tuning experiments)
         auto run = [&](auto TT, auto PPc) {
             constexpr int TQM = decltype(TT)::value, PP = decltype(PPc)::value;
-            const size_t sm = (size_t)(9 * (TQM + P->p + 1) * (TQF + P->p + 1) + TQM * 9 * (TQF + P->p + 1)) * sizeof(double);
+            const size_t na = (size_t)9 * (TQM + P->p + 1) * (TQF + P->p + 1), nx = (size_t)TQM * 9 * (TQF + P->p + 1);
+            const size_t sm = (na > nx ? na : nx) * sizeof(double);
             cudaFuncSetAttribute(k_coefz<TQM, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
             dim3 g((unsigned)((a.nq_loc_d + TQF - 1) / TQF), (unsigned)((P->dir[0].nq + TQM - 1) / TQM), (unsigned)P->dir[1].nq);
             k_coefz<TQM, PP><<<g, TQF * TQM, sm, s>>>(a);
