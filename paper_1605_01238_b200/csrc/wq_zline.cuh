@@ -101,7 +101,10 @@ struct ZCfg {
     // ZMB: direction 1 (stage B)
     static constexpr bool ZMA = BND && NCH == 1 && P >= 3;
     static constexpr bool ZMB = BND && P >= 3;
-    static constexpr int RING = 2 * NTS;
+    // points per producer task: 4 at p = 2 (interior boxes), the two point pairs on the two half-warps
+    // (15 stage-A fibres and 15 stage-B lanes per pair), else 2
+    static constexpr int PTS = P == 2 && !BND ? 4 : 2;
+    static constexpr int RING = PTS * NTS;
     static constexpr int QX = BND ? QB : QI;         // box / table extent in directions 0, 1
     static constexpr int NF = 3 * QX;                // stage-A fibres (m, c1)
     static constexpr int NPASS = (NF + 31) / 32;
@@ -113,8 +116,8 @@ struct ZCfg {
     static constexpr int YTOT = 6 * YB;
     // Y over the consumed box when stage A is one pass over interior fibres, else its own buffer
     static constexpr bool YSEP = BND || NPASS > 1;
-    static constexpr int BOXD = YSEP ? (6 * QX * QX * 2 + 15) / 16 * 16
-                                     : ((6 * QX * QX * 2 > YTOT ? 6 * QX * QX * 2 : YTOT) + 15) / 16 * 16;
+    static constexpr int BOXD = YSEP ? (6 * QX * QX * PTS + 15) / 16 * 16
+                                     : ((6 * QX * QX * PTS > YTOT * (PTS / 2) ? 6 * QX * QX * PTS : YTOT * (PTS / 2)) + 15) / 16 * 16;
     static constexpr int YD = YSEP ? YTOT : 0;
     static constexpr int TABD = (4 * QX * NPP + 8 * QX + QX + 1) & ~1;  // T0, T1, W0, W1, offsets (ints); 16-B multiple
     static constexpr int W2D = NR * QB * 4;                  // doubles per consumer weight buffer
@@ -292,7 +295,9 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
     for (int x = tid; x <= n2l; x += blockDim.x) pref2[x] = v2.pref[i2b + x] - v2.pref[a.slab_b];
     for (int x = tid; x < nq2l; x += blockDim.x) span2[x] = v2.span[cqb + x];
     // tasks: local points (2 tau, 2 tau + 1); the slab's first point is local 0
-    const int NTASK = (q_end + 1) / 2;
+    constexpr int PTS = CF::PTS;
+    static_assert(PTS == 2 || (3 * QX <= 16 && 3 * CF::T0C <= 16 && !CF::YSEP), "4-point tasks");
+    const int NTASK = (q_end + PTS - 1) / PTS;
     // items of this CTA: round-robin (neighbouring lines run concurrently and share their coefficient
     // boxes in L2), or a contiguous chunk (boundary lines, sorted by row type: one code path per CTA)
     // boundary lines: chunks of ZCH consecutive lines (same row types, sorted on the host) dealt
@@ -348,7 +353,9 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
         // NPP so that (r, r+1) pairs load as one 16-B word), W0t / W1t [c][f] (f = a + 2b)
         double *T0 = tab, *T1 = T0 + 2 * QX * NPP;
         double *W0t = T1 + 2 * QX * NPP, *W1t = W0t + 4 * QX;
-        constexpr unsigned BOX_BYTES = 6 * QX * QX * 2 * 8;
+        constexpr unsigned BOX_BYTES = 6 * QX * QX * PTS * 8;
+        // PTS = 4: half-warp hp works on point pair hp of the task, sub-lane sl
+        const int hp = PTS == 4 ? lane >> 4 : 0, sl = PTS == 4 ? lane & 15 : lane;
         // task T = k * NTASK + tau of this warp (T = wp, wp + NWP, ...): item k, point pair tau; the
         // issue stream (TMA of the coefficient boxes) runs NB tasks ahead of the compute stream
         int64_t ik = -1, is_k = wp / NTASK, is_T = wp;
@@ -366,7 +373,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 mbar_arrive(&pfull[wp * NB + b]);  // debug ablation: no box load
             } else {
                 mbar_arrive_tx(&pfull[wp * NB + b], BOX_BYTES);
-                tma_load_4d(wbase + b * BOXD, &tm, &pfull[wp * NB + b], (int)a.qoff + 2 * is_tau, iq1, iq0, 0);
+                tma_load_4d(wbase + b * BOXD, &tm, &pfull[wp * NB + b], (int)a.qoff + PTS * is_tau, iq1, iq0, 0);
             }
             is_T += NWP;
             is_tau += NWP;
@@ -381,15 +388,15 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
         int64_t cur_item = -1;
         // stage B lanes (g, t0): g = 0, 1 -> b2 = 0, a2 = g (chains m = 0 and m = 1 summed in the lane);
         // g = 2 -> b2 = 1 (chain m = 2, both a2).  Input blocks x = 0, 1 of Y and their tables:
-        const int fg = lane / T0C, fc = lane % T0C;
-        const bool fl = lane < 3 * T0C && fc < T0N;
+        const int fg = sl / T0C, fc = sl % T0C;
+        const bool fl = sl < 3 * T0C && fc < T0N;
         const int ybx0 = fg == 0 ? 0 : (fg == 1 ? 1 : 4), ybx1 = fg == 0 ? 2 : (fg == 1 ? 3 : 5);  // Y blocks m*2+a2
         const int tsel1 = fg == 2 ? 1 : 0;  // table of block x = 1: B1' for m = 1, B1 for m = 2
         // PU: this lane's selections of the uniform tables (stage A: family b0 = [m == 0], weights of
         // its c1; stage B: table of block x = 1)
         double b0s[2][NP], w0s[QI][2], b1x[2][NP], w1u0 = 0.0, w1u1 = 0.0;
         if constexpr (PU) {
-            const int m = lane / QX < 3 ? lane / QX : 2, c1 = lane % QX;
+            const int m = sl / QX < 3 ? sl / QX : 2, c1 = sl % QX;
             #pragma unroll
             for (int par = 0; par < 2; ++par)
                 #pragma unroll
@@ -450,18 +457,18 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             // direction-2 basis pairs of the task's points (published with G)
             double2 b2v = make_double2(0.0, 0.0);
             const int b2pt = lane / NP, b2r = lane % NP;
-            const int b2q = 2 * tau + b2pt;
-            if (lane < 2 * NP && b2q < q_end) b2v = __ldg((const double2 *)(v2.B + (int64_t)(cqb + b2q) * BS) + b2r);
+            const int b2q = PTS * tau + b2pt;
+            if (lane < PTS * NP && b2q < q_end) b2v = __ldg((const double2 *)(v2.B + (int64_t)(cqb + b2q) * BS) + b2r);
             zwait(&pfull[wp * NB + b], (NB == 2 ? use >> 1 : use) & 1, wt1);
             const double *bx = wbase + b * BOXD;  // [comp][c0][c1][pt]
             // ---------------- stage A: fibre (m, c1), both points, chains a2 = 0 (y0), 1 (y1)
             // Y: block m*2+a2 at CF::yoff, [c1][t0][pt] inside; interior: over the consumed box
-            double *Y = YSEP ? Ybuf : wbase + b * BOXD;
+            double *Y = YSEP ? Ybuf : wbase + b * BOXD + hp * CF::YTOT;
             #pragma unroll(CF::ZMB ? 1 : CF::NPASS)
             for (int pass = 0; pass < CF::NPASS; ++pass) {
                 // boundary lines: the 3 #Q_1 fibres of this line packed densely (one pass when #Q_1 <= 10)
                 if (BND && 32 * pass >= 3 * cq1) break;
-                const int f = lane + 32 * pass;
+                const int f = sl + 32 * pass;
                 const int m = BND ? f / cq1 : f / QX, c1 = BND ? f % cq1 : f % QX;
                 const bool fv = BND ? f < 3 * cq1 : f < NF;
                 double y0[2][T0C], y1[2][T0C];
@@ -483,9 +490,9 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                         const double2 w0p = PU ? make_double2(w0s[c0 % QI][0], w0s[c0 % QI][1])
                                                : *(const double2 *)(W0t + c0 * 4 + w0o);  // w0^(0,b0), w0^(1,b0)
                         const double s1 = w0p.x * w1p.x, s2 = w0p.y * w1p.x, s3 = w0p.x * w1p.y;
-                        const double2 ca = *(const double2 *)(bx + ((ka * QX + c0) * QX + c1) * 2);
-                        const double2 cb = *(const double2 *)(bx + ((kb * QX + c0) * QX + c1) * 2);
-                        const double2 cc = *(const double2 *)(bx + ((kc * QX + c0) * QX + c1) * 2);
+                        const double2 ca = *(const double2 *)(bx + ((ka * QX + c0) * QX + c1) * PTS + 2 * hp);
+                        const double2 cb = *(const double2 *)(bx + ((kb * QX + c0) * QX + c1) * PTS + 2 * hp);
+                        const double2 cc = *(const double2 *)(bx + ((kc * QX + c0) * QX + c1) * PTS + 2 * hp);
                         const double h1a = s1 * ca.x, h1b = s1 * ca.y;                                // l = 2
                         const double h0a = fma(s2, cb.x, s3 * cc.x), h0b = fma(s2, cb.y, s3 * cc.y);  // l = 0, 1
                         #pragma unroll
@@ -635,17 +642,17 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 const int b2 = fg == 2 ? 1 : 0;
                 #pragma unroll
                 for (int pt = 0; pt < 2; ++pt) {
-                    double2 *Gd = Gs + ((slot_t * 2 + pt) * 2 + b2) * COLS + t0;
+                    double2 *Gd = Gs + ((slot_t * PTS + 2 * hp + pt) * 2 + b2) * COLS + t0;
                     #pragma unroll
                     for (int t = 0; t < K; ++t) {  // t = t_2; column t0 + T0C t
                         const double v = fma(g[1][pt][t], sum1, g[0][pt][t]);
-                        const double o = __shfl_down_sync(0xffffffffu, v, T0C);
+                        const double o = __shfl_down_sync(0xffffffffu, v, T0C, PTS == 4 ? 16 : 32);
                         const int td = CF::ZMB ? t - sh1 : t;  // slot of the row (see ZTy::shift)
                         if (fl && fg != 1 && td >= 0) Gd[T0C * td] = make_double2(v, fg == 0 ? o : g[1][pt][t]);
                     }
                 }
             }
-            if (lane < 2 * NP) B2r[(slot_t * 2 + b2pt) * NP + b2r] = b2v;
+            if (lane < PTS * NP) B2r[(slot_t * PTS + b2pt) * NP + b2r] = b2v;
             mbar_arrive(&gfull[slot_t]);
             // the buffer is free again (all lanes done with Y): prefetch the task after next into it
             if constexpr (!YSEP) {
@@ -721,8 +728,8 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
         for (int r0 = first_row(ik_); r0 < n2l; r0 += NWC * NR) {
             const int nr = n2l - r0 < NR ? n2l - r0 : NR;
             const int rl = r0 + nr - 1;
-            const uint32_t t_hi = Tbase + (uint32_t)((qlo2[rl] + qlen2[rl] - 1) / 2);
-            const uint32_t t_lo = Tbase + (uint32_t)(qlo2[r0] / 2);
+            const uint32_t t_hi = Tbase + (uint32_t)((qlo2[rl] + qlen2[rl] - 1) / PTS);
+            const uint32_t t_lo = Tbase + (uint32_t)(qlo2[r0] / PTS);
             zwait(&wfull[cw * 2 + wbuf], wuse[wbuf] & 1, wt2);
             ++wuse[wbuf];
             const double2 *W2w = (const double2 *)(W2b + wbuf * CF::W2D);  // [row][c][2] double2, row stride mq2
@@ -754,7 +761,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                 for (int j = 0; j < CPL; ++j)
                     #pragma unroll
                     for (int t = 0; t < K; ++t) acc[k][j][t] = 0.0;
-            auto slot_of = [&](int q) { return (int)((Tbase * 2 + (uint32_t)q) % RING); };
+            auto slot_of = [&](int q) { return (int)((Tbase * PTS + (uint32_t)q) % RING); };
             // fast path: a full batch of rows with the interior staircase; with CU only rows whose
             // rules are the uniform ones (the others go through the generic path)
             const int rlo = CU ? 2 * P : P + 1, rhi = CU ? (int)v2.n - 1 - 2 * P : (int)v2.n - P - 2;
@@ -836,7 +843,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             {
                 const int nb = r0 + NWC * NR;
                 const int low = nb < n2l ? qlo2[nb] : q_end;
-                const uint32_t t_rel = Tbase + (uint32_t)(low / 2);
+                const uint32_t t_rel = Tbase + (uint32_t)(low / PTS);
                 __syncwarp();
                 while (rel < t_rel && rel < got) {
                     if (lane == 0) mbar_arrive_relaxed(&gempty[rel % NTS]);
@@ -961,7 +968,7 @@ wq_status launch_zline_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, i
         const int64_t nq0 = Pl->dir[0].nq, nq1 = Pl->dir[1].nq;
         cuuint64_t dims[4] = {(cuuint64_t)Pl->zld, (cuuint64_t)nq1, (cuuint64_t)nq0, 6};
         cuuint64_t strides[3] = {(cuuint64_t)Pl->zld * 8, (cuuint64_t)Pl->zld * nq1 * 8, (cuuint64_t)Pl->zcs * 8};
-        cuuint32_t box[4] = {2, (cuuint32_t)CF::QX, (cuuint32_t)CF::QX, 6};
+        cuuint32_t box[4] = {(cuuint32_t)CF::PTS, (cuuint32_t)CF::QX, (cuuint32_t)CF::QX, 6};
         cuuint32_t es[4] = {1, 1, 1, 1};
         if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void *)Pl->coefz, dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
