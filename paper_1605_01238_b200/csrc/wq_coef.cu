@@ -283,7 +283,7 @@ __global__ void k_dnet(const double *__restrict__ P, double *__restrict__ Q, Dir
 // issues all of its derivative-net loads of stage A before the first FMA (the kernel is bound by
 // their L2 latency); PP = 0: any degree
 template <int TQM, int PP>
-__global__ void __launch_bounds__(TQF * TQM) k_coefz(CoefArgs a) {
+__global__ void __launch_bounds__(TQF * TQM, TQM == 16 ? 3 : 1) k_coefz(CoefArgs a) {
     extern __shared__ __align__(16) double sm[];
     const int p = PP > 0 ? PP : a.p;
     const DirView &v0 = a.v[0], &v1 = a.v[1], &v2 = a.v[2];
