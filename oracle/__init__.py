@@ -59,6 +59,8 @@ def _load():
             lib.orc_row_nnz.restype = C.c_int64
             lib.orc_rows.argtypes = [P, C.c_int, C.c_int64] + [C.c_void_p] * 6
             lib.orc_pattern.argtypes = [P, C.c_void_p, C.c_void_p]
+            lib.orc_pattern_rows.argtypes = [P, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
+            lib.orc_set_coefficients.argtypes = [P, C.c_void_p, C.c_void_p]
             lib.orc_sgq_dense.argtypes = [P, C.c_int, C.c_void_p]
             lib.orc_check_knots.argtypes = [C.c_int, C.c_int64, dp]
             lib.orc_num_points.argtypes = [C.c_int, C.c_int64]
@@ -120,7 +122,7 @@ def gauss(n):
 class Oracle:
     """One WQ problem: d knot vectors of degree p plus an optional control net."""
 
-    def __init__(self, p: int, knots, ctrl=None):
+    def __init__(self, p: int, knots, ctrl=None, kappa=None, gamma=None):
         self._lib = _load()
         self.p = int(p)
         self.knots = [np.ascontiguousarray(k, dtype=np.float64) for k in knots]
@@ -136,6 +138,10 @@ class Oracle:
             self._lib.orc_destroy(self._h)
             self._h = None
             raise OracleError(st, msg)
+        self._kappa = None if kappa is None else np.ascontiguousarray(kappa, dtype=np.float64).reshape(-1)
+        self._gamma = None if gamma is None else np.ascontiguousarray(gamma, dtype=np.float64).reshape(-1)
+        if self._kappa is not None or self._gamma is not None:
+            self._lib.orc_set_coefficients(self._h, _vp(self._kappa), _vp(self._gamma))
         self.n = [int(self._lib.orc_info(self._h, l, 0)) for l in range(self.d)]
         self.nq = [int(self._lib.orc_info(self._h, l, 1)) for l in range(self.d)]
         self.maxq = [int(self._lib.orc_info(self._h, l, 2)) for l in range(self.d)]
@@ -197,6 +203,14 @@ class Oracle:
         self._lib.orc_pattern(self._h, _vp(rp), None)
         col = np.empty(int(rp[-1]), np.int32)
         self._lib.orc_pattern(self._h, _vp(rp), _vp(col))
+        return rp, col
+
+    def pattern_rows(self, r_lo: int, r_hi: int):
+        """Pattern of rows [r_lo, r_hi) (global row_ptr offsets, columns), by definition."""
+        rp = np.empty(r_hi - r_lo + 1, np.int64)
+        self._lib.orc_pattern_rows(self._h, int(r_lo), int(r_hi), _vp(rp), None)
+        col = np.empty(int(rp[-1] - rp[0]), np.int32)
+        self._lib.orc_pattern_rows(self._h, int(r_lo), int(r_hi), _vp(rp), _vp(col))
         return rp, col
 
     def sgq_dense(self, matrix: int) -> np.ndarray:

@@ -216,6 +216,8 @@ typedef struct {
     qr *I4[3];              /* [n][2p+1][4] exact integrals, family order (0,0),(1,0),(0,1),(1,1) */
     double *w[3];           /* [n][4][maxq] weights (FP64), zero padded                         */
     double *ctrl;           /* [N_DOF][d] control points                                       */
+    double *kappa, *gamma;  /* [N_DOF] spline coefficients of the scalar PDE coefficients or NULL
+                               (= 1): -div(kappa grad u) + gamma u, reading R17 */
     int64_t ndof;
     int status;
     char msg[256];
@@ -293,6 +295,8 @@ void orc_destroy(orc_ctx *c)
     if (!c) return;
     for (int l = 0; l < c->d; ++l) ctx_free_dir(c, l);
     free(c->ctrl);
+    free(c->kappa);
+    free(c->gamma);
     free(c);
 }
 
@@ -515,6 +519,24 @@ orc_ctx *orc_create(int d, int p, const int64_t *nk, const double *const *knots,
     return c;
 }
 
+/* scalar PDE coefficient nets (reading R17): [N_DOF] each, or NULL (= 1)   */
+int orc_set_coefficients(orc_ctx *c, const double *kappa, const double *gamma)
+{
+    if (!c) return ORC_EINVAL;
+    free(c->kappa);
+    free(c->gamma);
+    c->kappa = c->gamma = NULL;
+    if (kappa) {
+        c->kappa = (double *)malloc(sizeof(double) * (size_t)c->ndof);
+        memcpy(c->kappa, kappa, sizeof(double) * (size_t)c->ndof);
+    }
+    if (gamma) {
+        c->gamma = (double *)malloc(sizeof(double) * (size_t)c->ndof);
+        memcpy(c->gamma, gamma, sizeof(double) * (size_t)c->ndof);
+    }
+    return ORC_OK;
+}
+
 /* ------------------------------------------------------------------------ */
 /* exports of the univariate objects */
 int64_t orc_info(orc_ctx *c, int l, int what)
@@ -554,12 +576,18 @@ int orc_export_dir(orc_ctx *c, int l, double *pts, int64_t *qlo, int64_t *qlen, 
  * basis rows (values V[l][k], derivatives D[l][k], active range lo..hi).
  * J_{a,l} = dF_a/dzeta_l (Eq. mass2/stiff); returns det J and
  * fills c = |det J| and C = |det J| J^{-1} J^{-T} = adj(J) adj(J)^T / |det J|
- * (Eq. coef_stiff, reading R7), C row-major d x d.                */
+ * (Eq. coef_stiff, reading R7), C row-major d x d.  With scalar PDE
+ * coefficients ("Non-constant coefficients could be included as well";
+ * P:508-509 "the factor c incorporates the coefficient of the equation";
+ * reading R17) kappa(zeta) = sum_k kappa_k B_k(zeta) and gamma likewise, by
+ * the same direct sum over the active control points: c = gamma |det J|,
+ * C = kappa |det J| J^{-1} J^{-T}.                                          */
 static ld coef_point(const orc_ctx *c, const ld *const *V, const ld *const *D,
                      const int64_t *lo, const int64_t *hi, ld *cm, ld *C)
 {
     int d = c->d;
     ld J[3][3] = {{0}};
+    ld kap = 0, gam = 0;
     int64_t n0 = c->n[0], n1 = d > 1 ? c->n[1] : 1;
     int64_t lo1 = d > 1 ? lo[1] : 0, hi1 = d > 1 ? hi[1] : 0;
     int64_t lo2 = d > 2 ? lo[2] : 0, hi2 = d > 2 ? hi[2] : 0;
@@ -574,6 +602,10 @@ static ld coef_point(const orc_ctx *c, const ld *const *V, const ld *const *D,
                     if (f == 0) continue;
                     for (int a = 0; a < d; ++a) J[a][m] += (ld)c->ctrl[k * d + a] * f;
                 }
+                ld bv = 1;
+                for (int l = 0; l < d; ++l) bv *= V[l][kk[l]];
+                if (c->kappa) kap += (ld)c->kappa[k] * bv;
+                if (c->gamma) gam += (ld)c->gamma[k] * bv;
             }
     ld det, adj[3][3];
     if (d == 1) {
@@ -596,12 +628,14 @@ static ld coef_point(const orc_ctx *c, const ld *const *V, const ld *const *D,
         det = J[0][0] * adj[0][0] + J[0][1] * adj[1][0] + J[0][2] * adj[2][0];
     }
     ld ad = det < 0 ? -det : det;
-    *cm = ad;
+    if (!c->kappa) kap = 1;
+    if (!c->gamma) gam = 1;
+    *cm = gam * ad;
     for (int l = 0; l < d; ++l)
         for (int m = 0; m < d; ++m) {
             ld s = 0;
             for (int k = 0; k < d; ++k) s += adj[l][k] * adj[m][k];
-            C[l * d + m] = ad > 0 ? s / ad : 0;
+            C[l * d + m] = ad > 0 ? kap * s / ad : 0;
         }
     return det;
 }
@@ -790,11 +824,45 @@ int orc_pattern(orc_ctx *c, int64_t *row_ptr, int32_t *col)
     return ORC_OK;
 }
 
+/* Pattern of the rows [r_lo, r_hi) by the same definition, for streaming
+ * comparisons of full-size index arrays: row_ptr[0 .. r_hi-r_lo] are GLOBAL
+ * offsets (the nnz of all earlier rows summed row by row), col the columns
+ * of the range.                                                             */
+int orc_pattern_rows(orc_ctx *c, int64_t r_lo, int64_t r_hi, int64_t *row_ptr, int32_t *col)
+{
+    int d = c->d;
+    if (r_lo < 0 || r_hi > c->ndof || r_lo > r_hi) return ORC_EINVAL;
+    int64_t off = 0;
+    for (int64_t r = 0; r < r_lo; ++r) off += orc_row_nnz(c, r);
+    for (int64_t r = r_lo; r < r_hi; ++r) {
+        row_ptr[r - r_lo] = off;
+        off += orc_row_nnz(c, r);
+    }
+    row_ptr[r_hi - r_lo] = off;
+    if (!col) return ORC_OK;
+    const int64_t base = row_ptr[0];
+#pragma omp parallel for schedule(static)
+    for (int64_t r = r_lo; r < r_hi; ++r) {
+        int64_t i[3] = {0, 0, 0};
+        decompose(c, r, i);
+        int64_t ni[3] = {1, 1, 1}, j0[3] = {0, 0, 0};
+        for (int l = 0; l < d; ++l) { ni[l] = c->jlen[l][i[l]]; j0[l] = c->jlo[l][i[l]]; }
+        int64_t o = row_ptr[r - r_lo] - base;
+        for (int64_t t2 = 0; t2 < ni[2]; ++t2)
+            for (int64_t t1 = 0; t1 < ni[1]; ++t1)
+                for (int64_t t0 = 0; t0 < ni[0]; ++t0)
+                    col[o++] = (int32_t)((j0[0] + t0) + c->n[0] * ((d > 1 ? j0[1] + t1 : 0) +
+                                                                  (d > 1 ? c->n[1] : 1) * (d > 2 ? j0[2] + t2 : 0)));
+    }
+    return ORC_OK;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Element-loop standard Gauss quadrature (SGQ), p+1 points per direction per
  * element, dense N_DOF x N_DOF output (small problems only).  The paper's
- * comparison method; used here ONLY to self-check the WQ rows on
- * affine maps, where WQ is exact.                        */
+ * comparison method; used to self-check the WQ rows on affine
+ * maps, where WQ is exact, and as the oracle of the GPU
+ * SGQ baseline (wq_assemble_sgq).                                           */
 int orc_sgq_dense(orc_ctx *c, int matrix, double *A)
 {
     if (!c->ctrl) return ORC_EINVAL;
