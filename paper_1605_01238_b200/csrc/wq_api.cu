@@ -10,6 +10,8 @@
 #include <atomic>
 #include <vector>
 #include <algorithm>
+#include <mutex>
+#include <set>
 #include "wq_internal.cuh"
 
 namespace {
@@ -53,6 +55,26 @@ wq_status wq_cuda_status(cudaError_t e, const char *what) {
     return WQ_ECUDA;
 }
 
+cudaError_t wq_smem_attr(const void *func, size_t bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;  // (function, device) pairs already raised to 227 KB
+    int dev = 0;
+    cudaError_t ce = cudaGetDevice(&dev);
+    if (ce != cudaSuccess) return ce;
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count({func, dev})) return cudaSuccess;
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    ce = cudaFuncGetAttributes(&fa, func);
+    if (ce != cudaSuccess) return ce;
+    const int avail = optin - (int)fa.sharedSizeBytes;
+    if ((size_t)avail < bytes) return cudaErrorInvalidValue;
+    ce = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, avail);
+    if (ce == cudaSuccess) done.insert({func, dev});
+    return ce;
+}
+
 extern "C" {
 
 const char *wq_status_string(wq_status s) {
@@ -75,6 +97,59 @@ const char *wq_version(void) { return "libwq sm_100a " __DATE__ " " __TIME__; }
 
 uint64_t wq_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+static int64_t rows_per_plane(const wq_plan_s *P) {
+    int64_t r = 1;
+    for (int l = 0; l < P->d - 1; ++l) r *= P->dir[l].n;
+    return r;
+}
+
+// Upload a host net of `count` doubles into *dst (allocated on first use).
+static wq_status upload(double **dst, const double *src, size_t count) {
+    if (!*dst && cudaMalloc((void **)dst, sizeof(double) * count) != cudaSuccess) {
+        *dst = nullptr;
+        return fail(WQ_ENOMEM, "control/coefficient net allocation failed");
+    }
+    return wq_cuda_status(cudaMemcpy(*dst, src, sizeof(double) * count, cudaMemcpyHostToDevice), "net upload");
+}
+
+// Verdict of the device-side latched flags after a synchronous build.
+static wq_status flags_verdict(wq_plan_s *P) {
+    Flags f;
+    cudaError_t ce = cudaMemcpy(&f, P->flags, sizeof(Flags), cudaMemcpyDeviceToHost);
+    if (ce != cudaSuccess) return wq_cuda_status(ce, "flag readback");
+    if (f.weights_bad) {
+        int code = f.weights_bad - 1;
+        int row = code / 12, rem = code % 12, dir = rem / 4, fam = rem % 4;
+        char buf[200];
+        snprintf(buf, sizeof buf, "weight system failed (Eq. exact, residual > 1e-13): dir %d row %d family (%d,%d)", dir,
+                 row, fam & 1, fam >> 1);
+        return fail(WQ_ESINGULAR, buf);
+    }
+    if (f.det_zero || (f.det_pos && f.det_neg))
+        return fail(WQ_EGEOMETRY, f.det_zero ? "det J = 0 at a grid point" : "det J changes sign on the grid");
+    return WQ_OK;
+}
+
+// Synchronous part of plan creation: rules (ESINGULAR), coefficient field if a control net was
+// given (EGEOMETRY), and the one-time z-line preparation (reading R16).
+static wq_status create_build(wq_plan_s *P) {
+    cudaStream_t s;
+    cudaError_t ce = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    if (ce != cudaSuccess) return wq_cuda_status(ce, "plan stream");
+    wq_status st = launch_rules(P, s);
+    if (!st) st = wq_cuda_status(cudaStreamSynchronize(s), "rules");
+    if (!st) st = flags_verdict(P);
+    if (!st && P->ctrl_dev) {
+        st = launch_coef(P, P->ctrl_dev, P->kappa_dev, P->gamma_dev, s);
+        if (!st) st = wq_cuda_status(cudaStreamSynchronize(s), "coefficient field");
+        if (!st) st = flags_verdict(P);
+        if (!st) P->has_coef = 1;
+    }
+    cudaStreamDestroy(s);
+    if (!st && P->zline_ok) st = zline_prepare(P);
+    return st;
+}
+
 wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     if (!out) return fail(WQ_EINVAL, "out is NULL");
     *out = nullptr;
@@ -84,41 +159,51 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     if (p < 1 || p > WQ_MAX_DEGREE) return fail(p < 1 ? WQ_EKNOTS : WQ_EINVAL, "p must be in [1, WQ_MAX_DEGREE]");
     if (!desc->n_knots || !desc->knots) return fail(WQ_EINVAL, "knots are NULL");
     if (!desc->need_mass && !desc->need_stiffness) return fail(WQ_EINVAL, "need_mass or need_stiffness required");
+    if (desc->bpts != WQ_BPTS_INTERIOR && desc->bpts != WQ_BPTS_ENDPOINTS) return fail(WQ_EINVAL, "bad bpts");
+    if ((desc->kappa || desc->gamma) && !desc->ctrl) return fail(WQ_EINVAL, "kappa/gamma given without a control net");
+    // ---- validate knots (P:463-478)
+    int64_t nk_[3], E_[3];
+    for (int l = 0; l < d; ++l) {
+        int64_t nk = desc->n_knots[l];
+        const double *xi = desc->knots[l];
+        if (!xi) return fail(WQ_EINVAL, "knot vector is NULL");
+        int64_t E = nk - 2 * (int64_t)p - 1;
+        if (E < 1) return fail(WQ_EKNOTS, "dir " + std::to_string(l) + ": too few knots");
+        for (int64_t k = 0; k < nk; ++k)
+            if (!std::isfinite(xi[k])) return fail(WQ_EKNOTS, "dir " + std::to_string(l) + ": non-finite knot");
+        for (int k = 1; k <= p; ++k)
+            if (xi[k] != xi[0] || xi[nk - 1 - k] != xi[nk - 1])
+                return fail(WQ_EKNOTS, "dir " + std::to_string(l) + ": knot vector is not open");
+        for (int64_t k = p; k < nk - p - 1; ++k)
+            if (!(xi[k] < xi[k + 1]))
+                return fail(WQ_EKNOTS, "dir " + std::to_string(l) + ": repeated or decreasing interior knot at " +
+                                           std::to_string(k));
+        nk_[l] = nk;
+        E_[l] = E;
+    }
+    if (desc->bpts == WQ_BPTS_ENDPOINTS) {
+        // SPEC's reading of Remark 1: the p+1 boundary-span points include the span's knots, so only
+        // p-1 new points lie strictly inside span 0; row 0 (supp B_0 = span 0, open) then has
+        // #Q_0 = p-1 < #I_0 = p+1 (and row 1 #Q_1 = p+1 < p+2): Eq. numb_nodes fails.
+        return fail(WQ_ESINGULAR, "WQ_BPTS_ENDPOINTS: dir 0 row 0 has #Q = " + std::to_string(p - 1) + " < #I = " +
+                                      std::to_string(p + 1) + " (Eq. numb_nodes, P:640-642; reading R1)");
+    }
     wq_plan_s *P = new wq_plan_s();
-    // value-initialised: POD members zero, vectors empty (no memset over the std::vector members)
+    // value-initialised: POD members zero, vectors empty
     P->d = d;
     P->p = p;
     P->device = desc->device;
     P->need_mass = desc->need_mass ? 1 : 0;
     P->need_stiff = desc->need_stiffness ? 1 : 0;
-    // ---- validate knots (P:463-478)
     for (int l = 0; l < d; ++l) {
-        int64_t nk = desc->n_knots[l];
-        const double *xi = desc->knots[l];
-        if (!xi) { delete P; return fail(WQ_EINVAL, "knot vector is NULL"); }
-        int64_t E = nk - 2 * (int64_t)p - 1;
-        if (E < 1) { delete P; return fail(WQ_EKNOTS, "dir " + std::to_string(l) + ": too few knots"); }
-        for (int64_t k = 0; k < nk; ++k)
-            if (!std::isfinite(xi[k])) { delete P; return fail(WQ_EKNOTS, "dir " + std::to_string(l) + ": non-finite knot"); }
-        for (int k = 1; k <= p; ++k)
-            if (xi[k] != xi[0] || xi[nk - 1 - k] != xi[nk - 1]) {
-                delete P;
-                return fail(WQ_EKNOTS, "dir " + std::to_string(l) + ": knot vector is not open");
-            }
-        for (int64_t k = p; k < nk - p - 1; ++k)
-            if (!(xi[k] < xi[k + 1])) {
-                delete P;
-                return fail(WQ_EKNOTS, "dir " + std::to_string(l) + ": repeated or decreasing interior knot at " +
-                                           std::to_string(k));
-            }
         DirView &v = P->dir[l];
-        v.nk = nk;
-        v.n = nk - p - 1;
-        v.E = E;
-        v.nq = host_nq(E, p);
+        v.nk = nk_[l];
+        v.n = nk_[l] - p - 1;
+        v.E = E_[l];
+        v.nq = host_nq(v.E, p);
         int64_t mq = 0;
         for (int64_t i = 0; i < v.n; ++i) {
-            int64_t q = host_qhi(i, E, p) - host_qlo(i, E, p) + 1;
+            int64_t q = host_qhi(i, v.E, p) - host_qlo(i, v.E, p) + 1;
             if (q < wq_ni(i, p, v.n)) { delete P; return fail(WQ_ESINGULAR, "#Q < #I (Eq. numb_nodes)"); }
             mq = q > mq ? q : mq;
         }
@@ -143,43 +228,52 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     if (b < 0 || e > nd || b >= e) { delete P; return fail(WQ_EINVAL, "bad slab range"); }
     P->slab_b = b;
     P->slab_e = e;
-    int64_t rows_per_plane = 1, L_per_plane = 1;
-    for (int l = 0; l < ld; ++l) { rows_per_plane *= P->dir[l].n; L_per_plane *= P->L[l]; }
-    P->row_begin = b * rows_per_plane;
-    P->n_rows_local = (e - b) * rows_per_plane;
+    int64_t L_per_plane = 1;
+    for (int l = 0; l < ld; ++l) L_per_plane *= P->L[l];
+    P->row_begin = b * rows_per_plane(P);
+    P->n_rows_local = (e - b) * rows_per_plane(P);
     P->nnz_local = (host_pref(e, p, nd) - host_pref(b, p, nd)) * L_per_plane;
-    // coefficient sub-grid along direction d
+    // coefficient sub-grid along direction d (points of the owned rows' Q sets)
     P->cq_b = host_qlo(b, P->dir[ld].E, p);
     P->cq_e = host_qhi(e - 1, P->dir[ld].E, p) + 1;
-    int64_t cp = P->cq_e - P->cq_b;
+    const int64_t nql = P->cq_e - P->cq_b;
+    int64_t cp = nql;
     for (int l = 0; l < ld; ++l) cp *= P->dir[l].nq;
     P->coef_points = cp;
-    P->c0off = d == 3 ? 1 : 0;
-    P->cld1 = d == 3 ? (P->dir[0].nq + 2) / 2 * 2 : P->dir[0].nq;
-    P->cstride = d == 3 ? cp / P->dir[0].nq * P->cld1 : cp;
     P->ncomp_s = P->need_stiff ? d * (d + 1) / 2 : 0;
     P->ncomp = P->ncomp_s + P->need_mass;
-    // z layout for the stiffness components when the z-line kernel applies (wq.h coef_layout)
+    P->comp_mass = P->ncomp_s;
+    // control planes k_d that the sub-grid's points see: spans of cq_b .. cq_e-1 (+p), and one
+    // more below for the derivative differences
+    P->k3b = 0;
+    P->k3e = P->dir[ld].n;
+    if (d == 3) {
+        P->zld = (nql + 1) / 2 * 2;
+        P->zcs = P->dir[0].nq * P->dir[1].nq * P->zld;
+        P->cview.cs = P->zcs;
+        P->cview.s1 = P->dir[1].nq * P->zld;
+        P->cview.s2 = P->zld;
+        P->cview.s3 = 1;
+    } else {
+        P->nld1 = d == 2 ? P->dir[0].nq : 1;
+        P->zcs = cp;
+        P->cview.cs = cp;
+        P->cview.s1 = 1;
+        P->cview.s2 = d == 2 ? P->nld1 : 0;
+        P->cview.s3 = 0;
+    }
     {
         int64_t nn[3];
         int32_t mq[3];
         for (int l = 0; l < 3; ++l) { nn[l] = P->dir[l].n; mq[l] = P->dir[l].maxq; }
-        P->zlayout = d == 3 && P->need_stiff && desc->coef_layout == 0 &&
-                     zline_supported_p(d, p, nn, mq, e - b, P->cq_e - P->cq_b);
-    }
-    P->ncomp_std = P->zlayout ? P->need_mass : P->ncomp;
-    P->comp_mass = P->zlayout ? 0 : P->ncomp_s;
-    if (P->zlayout) {
-        P->zld = (P->cq_e - P->cq_b + 1) / 2 * 2;
-        P->zcs = P->dir[0].nq * P->dir[1].nq * P->zld;
+        P->zline_ok = d == 3 && P->need_stiff && zline_supported_p(d, p, nn, mq, e - b, nql);
     }
 
     // ---- device allocations
     cudaError_t ce = cudaSetDevice(P->device);
     if (ce != cudaSuccess) { delete P; return wq_cuda_status(ce, "cudaSetDevice"); }
     size_t bytes = 0;
-    std::vector<size_t> offs;
-    auto take = [&](size_t n) { size_t o = bytes; bytes = align_up(bytes + n); offs.push_back(o); return o; };
+    auto take = [&](size_t n) { size_t o = bytes; bytes = align_up(bytes + n); return o; };
     struct Off { size_t knots, pts, span, qlo, qlen, jlo, jlen, pref, B, W; } O[3];
     // directions with bitwise-identical knot vectors share one set of rules tables (the rules are a
     // pure function of the knots and p): dir_src[l] = first such direction
@@ -237,26 +331,17 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     }
     P->gl = (double *)(A + o_gl);
     P->flags = (Flags *)(A + o_fl);
-    size_t cbytes = sizeof(double) * (size_t)P->ncomp_std * (size_t)P->cstride;
-    if (cbytes > 0) {
-        ce = cudaMalloc((void **)&P->coef, cbytes);
-        if (ce != cudaSuccess) {
-            P->coef = nullptr;
-            wq_plan_destroy(P);
-            return fail(WQ_ENOMEM, "coefficient field allocation failed (" + std::to_string(cbytes) + " bytes)");
-        }
+    size_t cbytes = sizeof(double) * (size_t)P->ncomp * (size_t)P->zcs;
+    ce = cudaMalloc((void **)&P->coef, cbytes);
+    if (ce != cudaSuccess) {
+        P->coef = nullptr;
+        wq_plan_destroy(P);
+        return fail(WQ_ENOMEM, "coefficient field allocation failed (" + std::to_string(cbytes) + " bytes)");
     }
-    if (P->zlayout) {
-        const size_t zb = sizeof(double) * 6 * (size_t)P->zcs;
-        ce = cudaMalloc((void **)&P->coefz, zb);
-        if (ce != cudaSuccess) {
-            P->coefz = nullptr;
-            wq_plan_destroy(P);
-            return fail(WQ_ENOMEM, "z-layout coefficient field allocation failed (" + std::to_string(zb) + " bytes)");
-        }
-        cudaMemset(P->coefz, 0, zb);  // row padding stays zero
-        cbytes += zb;
-        // lines (i1, i2) of the z-line kernel: interior in directions 1 and 2 first, then the rest
+    cudaMemset(P->coef, 0, cbytes);  // z-layout row padding stays zero
+    P->cview.base = P->coef;
+    if (P->zline_ok) {
+        // lines (i1, i2) of the z-line kernel: uniform-rule lines, other interior lines, boundary lines
         const int64_t n0 = P->dir[0].n, n1 = P->dir[1].n;
         auto interz = [&](int l, int64_t i) {
             const int64_t E = P->dir[l].E, n = P->dir[l].n;
@@ -324,30 +409,35 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
         }
         cbytes += zl;
     }
-    // row lines of the slab, split for the line kernel (interior in directions 2 and 3) vs the rest
-    P->lines_dev = nullptr;
-    size_t lbytes = 0;
-    if (d == 3) {
-        const int64_t n2 = P->dir[1].n;
-        auto inter = [&](int l, int64_t i) {
-            const int64_t E = P->dir[l].E, n = P->dir[l].n;
-            return i >= p + 1 && i <= n - p - 2 && host_qhi(i, E, p) - host_qlo(i, E, p) + 1 == 2 * p + 1;
-        };
-        for (int64_t i3 = P->slab_b; i3 < P->slab_e; ++i3)
-            for (int64_t i2 = 0; i2 < n2; ++i2) {
-                const int32_t line = (int32_t)(i2 + n2 * (i3 - P->slab_b));
-                (inter(1, i2) && inter(2, i3) ? P->lines_int : P->lines_bnd).push_back(line);
-            }
-        lbytes = sizeof(int32_t) * (P->lines_int.size() + P->lines_bnd.size());
-        ce = cudaMalloc((void **)&P->lines_dev, lbytes > 0 ? lbytes : 4);
-        if (ce != cudaSuccess) { P->lines_dev = nullptr; wq_plan_destroy(P); return fail(WQ_ENOMEM, "line lists"); }
-        if (!P->lines_int.empty())
-            cudaMemcpy(P->lines_dev, P->lines_int.data(), sizeof(int32_t) * P->lines_int.size(), cudaMemcpyHostToDevice);
-        if (!P->lines_bnd.empty())
-            cudaMemcpy(P->lines_dev + P->lines_int.size(), P->lines_bnd.data(), sizeof(int32_t) * P->lines_bnd.size(),
-                       cudaMemcpyHostToDevice);
+    // ---- control net and coefficient nets (copied; the plan owns the device copies)
+    wq_status st = WQ_OK;
+    if (desc->ctrl) {
+        st = upload(&P->ctrl_dev, desc->ctrl, (size_t)N * d);
+        P->ctrl_bytes = sizeof(double) * (size_t)N * d;
+        if (!st && desc->kappa) st = upload(&P->kappa_dev, desc->kappa, (size_t)N);
+        if (!st && desc->gamma) st = upload(&P->gamma_dev, desc->gamma, (size_t)N);
+        cbytes += sizeof(double) * (size_t)N * (d + (desc->kappa ? 1 : 0) + (desc->gamma ? 1 : 0));
     }
-    P->workspace_bytes = (int64_t)(bytes + cbytes + lbytes);
+    // ---- which kernel WQ_KERNEL_AUTO runs
+    if (!st) {
+        P->kernel_auto[0] = !P->need_mass ? 0
+                          : d < 3 ? WQ_KERNEL_DIRECT
+                          : zhp_supported(P, WQ_MASS) ? WQ_KERNEL_ZHP
+                          : tile_supported(P, WQ_MASS) ? WQ_KERNEL_TILE : WQ_KERNEL_DIRECT;
+        st = create_build(P);
+        P->kernel_auto[1] = !P->need_stiff ? 0
+                          : d < 3 ? WQ_KERNEL_DIRECT
+                          : P->zline_ok ? WQ_KERNEL_ZLINE
+                          : zhp_supported(P, WQ_STIFFNESS) ? WQ_KERNEL_ZHP
+                          : tile_supported(P, WQ_STIFFNESS) ? WQ_KERNEL_TILE : WQ_KERNEL_DIRECT;
+    }
+    if (st) {
+        const std::string msg = g_err;
+        wq_plan_destroy(P);
+        g_err = msg;
+        return st;
+    }
+    P->workspace_bytes = (int64_t)(bytes + cbytes);
     *out = P;
     return WQ_OK;
 }
@@ -357,10 +447,10 @@ wq_status wq_plan_destroy(wq_plan P) {
     cudaSetDevice(P->device);
     if (P->arena) cudaFree(P->arena);
     if (P->coef) cudaFree(P->coef);
-    if (P->coefz) cudaFree(P->coefz);
     if (P->zlines_dev) cudaFree(P->zlines_dev);
-    if (P->lines_dev) cudaFree(P->lines_dev);
     if (P->ctrl_dev) cudaFree(P->ctrl_dev);
+    if (P->kappa_dev) cudaFree(P->kappa_dev);
+    if (P->gamma_dev) cudaFree(P->gamma_dev);
     if (P->dnet) cudaFree(P->dnet);
     if (P->stage_val) cudaFree(P->stage_val);
     delete P;
@@ -381,6 +471,9 @@ wq_status wq_plan_info(wq_plan P, wq_plan_info_t *info) {
     }
     info->coef_points = P->coef_points;
     info->workspace_bytes = P->workspace_bytes;
+    info->kernel[0] = P->kernel_auto[0];
+    info->kernel[1] = P->kernel_auto[1];
+    info->uniform_rules = P->zuni_state == 1 ? 1 : 0;
     return WQ_OK;
 }
 
@@ -392,12 +485,14 @@ wq_status wq_build_rules(wq_plan P, void *stream) {
     return launch_rules(P, S(stream));
 }
 
-wq_status wq_build_coef(wq_plan P, const double *d_ctrl, void *stream) {
+wq_status wq_build_coef(wq_plan P, const double *d_ctrl, const double *d_kappa, const double *d_gamma, void *stream) {
     if (!P || !d_ctrl) return fail(WQ_EINVAL, "NULL argument");
     cudaSetDevice(P->device);
     cudaError_t ce = cudaMemsetAsync(&P->flags->det_pos, 0, 3 * sizeof(int), S(stream));
     if (ce != cudaSuccess) return wq_cuda_status(ce, "flag reset");
-    return launch_coef(P, d_ctrl, S(stream));
+    wq_status st = launch_coef(P, d_ctrl, d_kappa, d_gamma, S(stream));
+    if (!st) P->has_coef = 1;
+    return st;
 }
 
 wq_status wq_pattern(wq_plan P, int64_t nnz_base, int64_t *d_row_ptr, int32_t *d_col, void *stream) {
@@ -407,20 +502,16 @@ wq_status wq_pattern(wq_plan P, int64_t nnz_base, int64_t *d_row_ptr, int32_t *d
     return launch_pattern(P, nnz_base, d_row_ptr, d_col, 0, P->n_rows_local, S(stream));
 }
 
-static int64_t rows_per_plane(const wq_plan_s *P) {
-    int64_t r = 1;
-    for (int l = 0; l < P->d - 1; ++l) r *= P->dir[l].n;
-    return r;
-}
-
 static wq_status assemble_range(wq_plan_s *P, int matrix, wq_kernel kernel, double *val, int32_t *col,
                                 int64_t pl_lo, int64_t pl_hi, int64_t val_base, cudaStream_t s) {
     if (matrix == WQ_MASS && !P->need_mass) return fail(WQ_EINVAL, "plan was created without need_mass");
     if (matrix == WQ_STIFFNESS && !P->need_stiff) return fail(WQ_EINVAL, "plan was created without need_stiffness");
-    if (matrix == WQ_STIFFNESS && P->zlayout) {
-        if (kernel != WQ_KERNEL_AUTO && kernel != WQ_KERNEL_ZLINE)
-            return fail(WQ_EINVAL, "plan holds the stiffness coefficients in the z layout: only WQ_KERNEL_ZLINE applies "
-                                   "(create the plan with coef_layout = 1 for the other kernels)");
+    if (!P->has_coef) return fail(WQ_EINVAL, "no coefficient field: pass desc.ctrl or call wq_build_coef first");
+    if (kernel == WQ_KERNEL_AUTO) kernel = (wq_kernel)P->kernel_auto[matrix];
+    switch (kernel) {
+    case WQ_KERNEL_ZLINE: {
+        if (matrix != WQ_STIFFNESS || !P->zline_ok)
+            return fail(WQ_EINVAL, "z-line kernel not available for this plan (stiffness, d = 3, 2 <= p <= 6)");
         const int64_t nu = (int64_t)P->zlines_uni.size(), ni = (int64_t)P->zlines_int.size(),
                       nb = (int64_t)P->zlines_bnd.size();
         wq_status st = launch_assemble_zline(P, 0, P->zlines_dev, nu, pl_lo, pl_hi, val, col, val_base, s);
@@ -428,35 +519,17 @@ static wq_status assemble_range(wq_plan_s *P, int matrix, wq_kernel kernel, doub
         if (!st) st = launch_assemble_zline(P, 2, P->zlines_dev + nu + ni, nb, pl_lo, pl_hi, val, col, val_base, s);
         return st;
     }
-    if (kernel == WQ_KERNEL_ZLINE) return fail(WQ_EINVAL, "z-line kernel not available for this plan (matrix, d, p, layout)");
-    const bool tile = tile_supported(P, matrix);
-    const bool ws = ws_supported(P, matrix);
-    const bool line = line_supported(P, matrix, false) && (line_supported(P, matrix, true) || tile);
-    if (kernel == WQ_KERNEL_LINE && !line) return fail(WQ_EINVAL, "line kernel not available for this (d, p, matrix)");
-    if (kernel == WQ_KERNEL_LINE || (kernel == WQ_KERNEL_AUTO && line)) {
-        // interior lines of the plane range by the line kernel, the others by the tile kernel
-        const int64_t n2 = P->dir[1].n, lo = pl_lo * n2, hi = pl_hi * n2;
-        auto sub = [&](const std::vector<int32_t> &v, int64_t &first, int64_t &count) {
-            first = std::lower_bound(v.begin(), v.end(), (int32_t)lo) - v.begin();
-            count = (std::lower_bound(v.begin(), v.end(), (int32_t)hi) - v.begin()) - first;
-        };
-        int64_t fi, ni, fb, nb;
-        sub(P->lines_int, fi, ni);
-        sub(P->lines_bnd, fb, nb);
-        wq_status st = launch_assemble_line(P, matrix, false, P->lines_dev + fi, ni, val, col, val_base, s);
-        const int32_t *lb = P->lines_dev + P->lines_int.size() + fb;
-        if (!st && nb > 0 && !getenv("WQ_LINE_ONLY"))
-            st = line_supported(P, matrix, true) ? launch_assemble_line(P, matrix, true, lb, nb, val, col, val_base, s)
-                                                 : launch_assemble_tile_list(P, matrix, lb, nb, val, col, val_base, s);
-        return st;
-    }
-    if (kernel == WQ_KERNEL_TILE && !tile) return fail(WQ_EINVAL, "tile kernel not available for this (d, p)");
-    if (kernel == WQ_KERNEL_WS && !ws) return fail(WQ_EINVAL, "warp-specialised kernel not available for this (d, p)");
-    if (kernel == WQ_KERNEL_DIRECT || (kernel == WQ_KERNEL_AUTO && !tile))
+    case WQ_KERNEL_ZHP:
+        if (!zhp_supported(P, matrix)) return fail(WQ_EINVAL, "ZHP kernel not available for this plan (d = 3)");
+        return launch_assemble_zhp(P, matrix, pl_lo, pl_hi, val, col, val_base, s);
+    case WQ_KERNEL_TILE:
+        if (!tile_supported(P, matrix)) return fail(WQ_EINVAL, "tile kernel not available for this (d, p)");
+        return launch_assemble_tile(P, matrix, val, col, pl_lo, pl_hi, val_base, s);
+    case WQ_KERNEL_DIRECT:
         return launch_assemble_direct(P, matrix, val, col, pl_lo, pl_hi, val_base, s);
-    if (kernel == WQ_KERNEL_WS)
-        return launch_assemble_ws(P, matrix, val, col, pl_lo, pl_hi, val_base, s);
-    return launch_assemble_tile(P, matrix, val, col, pl_lo, pl_hi, val_base, s);
+    default:
+        return fail(WQ_EINVAL, "unknown kernel");
+    }
 }
 
 wq_status wq_assemble_ex(wq_plan P, wq_matrix matrix, wq_kernel kernel, double *d_val, int32_t *d_col, void *stream) {
@@ -470,38 +543,42 @@ wq_status wq_assemble(wq_plan P, wq_matrix matrix, double *d_val, int32_t *d_col
     return wq_assemble_ex(P, matrix, WQ_KERNEL_AUTO, d_val, d_col, stream);
 }
 
+wq_status wq_assemble_sgq(wq_plan P, wq_matrix matrix, const double *d_ctrl, const double *d_kappa,
+                          const double *d_gamma, double *d_val, int32_t *d_col, void *stream) {
+    if (!P || !d_val || !d_ctrl) return fail(WQ_EINVAL, "NULL argument");
+    if (matrix != WQ_MASS && matrix != WQ_STIFFNESS) return fail(WQ_EINVAL, "bad matrix");
+    cudaSetDevice(P->device);
+    return launch_assemble_sgq(P, matrix, d_ctrl, d_kappa, d_gamma, d_val, d_col, S(stream));
+}
+
 wq_status wq_check(wq_plan P, void *stream) {
     if (!P) return fail(WQ_EINVAL, "NULL plan");
     cudaSetDevice(P->device);
     cudaError_t ce = cudaStreamSynchronize(S(stream));
     if (ce != cudaSuccess) return wq_cuda_status(ce, "stream synchronize");
-    Flags f;
-    ce = cudaMemcpy(&f, P->flags, sizeof(Flags), cudaMemcpyDeviceToHost);
-    if (ce != cudaSuccess) return wq_cuda_status(ce, "flag readback");
-    if (f.weights_bad) {
-        int code = f.weights_bad - 1;
-        int row = code / 12, rem = code % 12, dir = rem / 4, fam = rem % 4;
-        char buf[160];
-        snprintf(buf, sizeof buf, "weight system failed: dir %d row %d family (%d,%d)", dir, row, fam & 1, fam >> 1);
-        return fail(WQ_ESINGULAR, buf);
-    }
-    if (f.det_zero || (f.det_pos && f.det_neg))
-        return fail(WQ_EGEOMETRY, f.det_zero ? "det J = 0 at a grid point" : "det J changes sign on the grid");
-    return WQ_OK;
+    return flags_verdict(P);
 }
 
-wq_status wq_form_host(wq_plan P, wq_matrix matrix, const double *h_ctrl, int64_t nnz_base, int64_t *h_row_ptr,
-                       int32_t *h_col, double *h_val, void *stream) {
+wq_status wq_form_host(wq_plan P, wq_matrix matrix, const double *h_ctrl, const double *h_kappa, const double *h_gamma,
+                       int64_t nnz_base, int64_t *h_row_ptr, int32_t *h_col, double *h_val, void *stream) {
     if (!P || !h_ctrl || !h_row_ptr || !h_col || !h_val) return fail(WQ_EINVAL, "NULL argument");
+    if (matrix != WQ_MASS && matrix != WQ_STIFFNESS) return fail(WQ_EINVAL, "bad matrix");
     cudaSetDevice(P->device);
     cudaStream_t s = S(stream);
-    const size_t cbytes = sizeof(double) * (size_t)P->n_dof_total * P->d;
+    const size_t nctrl = (size_t)P->n_dof_total * P->d;
     cudaError_t ce;
-    if (P->ctrl_bytes < cbytes) {
+    if (P->ctrl_bytes < nctrl * sizeof(double)) {
         if (P->ctrl_dev) cudaFree(P->ctrl_dev);
-        ce = cudaMalloc((void **)&P->ctrl_dev, cbytes);
+        ce = cudaMalloc((void **)&P->ctrl_dev, nctrl * sizeof(double));
         if (ce != cudaSuccess) { P->ctrl_dev = nullptr; P->ctrl_bytes = 0; return fail(WQ_ENOMEM, "ctrl staging"); }
-        P->ctrl_bytes = cbytes;
+        P->ctrl_bytes = nctrl * sizeof(double);
+    }
+    for (double **dst : {&P->kappa_dev, &P->gamma_dev}) {
+        const double *src = dst == &P->kappa_dev ? h_kappa : h_gamma;
+        if (src && !*dst && cudaMalloc((void **)dst, sizeof(double) * (size_t)P->n_dof_total) != cudaSuccess) {
+            *dst = nullptr;
+            return fail(WQ_ENOMEM, "coefficient net staging");
+        }
     }
     // chunking by slab planes, double-buffered staging for values + columns + row_ptr
     const int64_t nplanes = P->slab_e - P->slab_b;
@@ -546,10 +623,12 @@ wq_status wq_form_host(wq_plan P, wq_matrix matrix, const double *h_ctrl, int64_
         cudaEventRecord(freed[k], cs);
     }
     wq_status st = WQ_OK;
-    ce = cudaMemcpyAsync(P->ctrl_dev, h_ctrl, cbytes, cudaMemcpyHostToDevice, s);
+    ce = cudaMemcpyAsync(P->ctrl_dev, h_ctrl, nctrl * sizeof(double), cudaMemcpyHostToDevice, s);
+    if (!ce && h_kappa) ce = cudaMemcpyAsync(P->kappa_dev, h_kappa, sizeof(double) * P->n_dof_total, cudaMemcpyHostToDevice, s);
+    if (!ce && h_gamma) ce = cudaMemcpyAsync(P->gamma_dev, h_gamma, sizeof(double) * P->n_dof_total, cudaMemcpyHostToDevice, s);
     if (ce != cudaSuccess) st = wq_cuda_status(ce, "ctrl upload");
     if (!st) st = wq_build_rules(P, s);
-    if (!st) st = wq_build_coef(P, P->ctrl_dev, s);
+    if (!st) st = wq_build_coef(P, P->ctrl_dev, h_kappa ? P->kappa_dev : nullptr, h_gamma ? P->gamma_dev : nullptr, s);
     // host-side 1D prefix of the slowest direction for chunk offsets
     const int64_t nd = P->dir[P->d - 1].n;
     int64_t Lpp = 1;
@@ -627,27 +706,21 @@ wq_status wq_export_coef(wq_plan P, double *h_out, int64_t *n_values, int32_t *n
     if (!h_out) return WQ_OK;
     cudaSetDevice(P->device);
     cudaError_t ce = cudaDeviceSynchronize();
-    // d = 3: un-pad the q_1 leading dimension (rows of nq_1 values at column offset c0off)
-    const int64_t nq1 = P->dir[0].nq, rows = P->coef_points / nq1;
-    if (P->zlayout) {
-        // stiffness components from the z layout [comp][q_1][q_2][q_3 - cq_b], then c (standard layout)
+    if (P->d == 3) {
+        // z layout [comp][q_1][q_2][q_3 - cq_b] -> documented [comp][q_3][q_2][q_1]
         const int64_t nqa = P->dir[0].nq, nqb = P->dir[1].nq, nqc = P->cq_e - P->cq_b;
-        std::vector<double> z((size_t)6 * P->zcs);
-        if (!ce) ce = cudaMemcpy(z.data(), P->coefz, sizeof(double) * z.size(), cudaMemcpyDeviceToHost);
+        std::vector<double> z((size_t)P->ncomp * P->zcs);
+        if (!ce) ce = cudaMemcpy(z.data(), P->coef, sizeof(double) * z.size(), cudaMemcpyDeviceToHost);
         if (!ce)
-            for (int k = 0; k < 6; ++k)
+            for (int k = 0; k < P->ncomp; ++k)
                 for (int64_t qc = 0; qc < nqc; ++qc)
                     for (int64_t qb = 0; qb < nqb; ++qb)
                         for (int64_t qa = 0; qa < nqa; ++qa)
                             h_out[k * P->coef_points + (qc * nqb + qb) * nqa + qa] =
                                 z[k * P->zcs + (qa * nqb + qb) * P->zld + qc];
-        if (!ce && P->need_mass)
-            ce = cudaMemcpy2D(h_out + 6 * P->coef_points, sizeof(double) * nq1, P->coef + P->c0off,
-                              sizeof(double) * P->cld1, sizeof(double) * nq1, (size_t)rows, cudaMemcpyDeviceToHost);
-    } else if (P->d < 3) {
-        if (!ce) ce = cudaMemcpy(h_out, P->coef, sizeof(double) * P->ncomp * P->coef_points, cudaMemcpyDeviceToHost);
-    } else if (!ce) ce = cudaMemcpy2D(h_out, sizeof(double) * nq1, P->coef + P->c0off, sizeof(double) * P->cld1, sizeof(double) * nq1,
-                               (size_t)(rows * P->ncomp), cudaMemcpyDeviceToHost);
+    } else if (!ce) {
+        ce = cudaMemcpy(h_out, P->coef, sizeof(double) * P->ncomp * P->coef_points, cudaMemcpyDeviceToHost);
+    }
     return wq_cuda_status(ce, "export coef");
 }
 

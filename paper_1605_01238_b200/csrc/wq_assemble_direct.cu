@@ -13,9 +13,7 @@ struct DirectArgs {
     RowGeo g;
     DirView v[3];
     int d, p, matrix;
-    const double *coef;
-    int64_t npts, nq1, nq2;  // coefficient sub-grid strides
-    int64_t c0off;
+    CoefView cv;             // coefficient field (any layout)
     int64_t cq_b;
     int comp_mass, ncomp_s;
     double *val;
@@ -81,16 +79,15 @@ __global__ void __launch_bounds__(128) k_direct(DirectArgs a) {
             const double *A1 = A + ((0 * nf + f[0]) * KM + t1) * QM;
             const double *A2 = A + ((1 * nf + f[1]) * KM + t2) * QM;
             const double *A3 = A + ((2 * nf + f[2]) * KM + t3) * QM;
-            const double *Cc = a.coef + (int64_t)comp * a.npts;
             for (int c3 = 0; c3 < nq[2]; ++c3) {
                 double s2 = 0.0;
                 for (int c2 = 0; c2 < nq[1]; ++c2) {
                     double s1 = 0.0;
-                    int64_t base;
-                    if (D == 3) base = a.c0off + (ql[0]) + a.nq1 * ((ql[1] + c2) + a.nq2 * (ql[2] + c3 - a.cq_b));
-                    else if (D == 2) base = (ql[0]) + a.nq1 * (ql[1] + c2 - a.cq_b);
-                    else base = ql[0] - a.cq_b;
-                    for (int c1 = 0; c1 < nq[0]; ++c1) s1 = fma(A1[c1], __ldg(Cc + base + c1), s1);
+                    // local coordinate along the slab direction d (the view counts it from cq_b)
+                    const double *Cc = D == 3 ? a.cv.ptr(comp, ql[0], ql[1] + c2, ql[2] + c3 - a.cq_b)
+                                     : D == 2 ? a.cv.ptr(comp, ql[0], ql[1] + c2 - a.cq_b, 0)
+                                              : a.cv.ptr(comp, ql[0] - a.cq_b, 0, 0);
+                    for (int c1 = 0; c1 < nq[0]; ++c1) s1 = fma(A1[c1], __ldg(Cc + c1 * a.cv.s1), s1);
                     s2 = fma(A2[c2], s1, s2);
                 }
                 s = fma(A3[c3], s2, s);
@@ -108,10 +105,6 @@ __global__ void __launch_bounds__(128) k_direct(DirectArgs a) {
 
 wq_status launch_assemble_direct(wq_plan_s *P, int matrix, double *val, int32_t *col, int64_t plane_lo,
                                  int64_t plane_hi, int64_t val_base, cudaStream_t s) {
-    if (matrix == WQ_STIFFNESS && P->zlayout) {
-        wq_set_error("direct kernel needs the standard coefficient layout (plan uses the z layout)");
-        return WQ_EINVAL;
-    }
     int64_t rpp = 1;
     for (int l = 0; l < P->d - 1; ++l) rpp *= P->dir[l].n;
     const int64_t row_lo = plane_lo * rpp, row_hi = plane_hi * rpp;
@@ -121,11 +114,7 @@ wq_status launch_assemble_direct(wq_plan_s *P, int matrix, double *val, int32_t 
     a.d = P->d;
     a.p = P->p;
     a.matrix = matrix;
-    a.coef = P->coef;
-    a.npts = P->cstride;
-    a.c0off = P->c0off;
-    a.nq1 = P->cld1;
-    a.nq2 = P->dir[1].nq;
+    a.cv = P->cview;
     a.cq_b = P->cq_b;
     a.ncomp_s = P->ncomp_s;
     a.comp_mass = P->comp_mass;
@@ -140,11 +129,7 @@ wq_status launch_assemble_direct(wq_plan_s *P, int matrix, double *val, int32_t 
     int KM = 2 * p + 1, QM = qmax;
     int nf = matrix == 0 ? 1 : 4;
     size_t sm = (size_t)3 * nf * KM * QM * sizeof(double);
-    static bool set = false;
-    if (!set) {
-        cudaFuncSetAttribute(k_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        set = true;
-    }
+    wq_smem_attr((const void *)k_direct, sm);
     int64_t rows = row_hi - row_lo;
     if (rows > 0) {
         k_direct<<<(unsigned)rows, 128, sm, s>>>(a);

@@ -98,10 +98,8 @@ __device__ __forceinline__ void unroll(F &&f) {
 struct TileArgs {
     RowGeo g;
     DirView v[3];
-    const double *coef;
-    int64_t nq1, nq2;  // coefficient strides
+    CoefView cv;       // coefficient field (any layout; q_1 contiguous in the fastest layout)
     int64_t cq_b;
-    int64_t npts;
     int comp_mass;
     double *val;
     int32_t *col;
@@ -154,7 +152,7 @@ __global__ void __launch_bounds__(256, 1) k_tile(TileArgs a) {
     const int t3a = chunk * T3C;
     if (t3a >= ni3) return;
     const int nt3 = ni3 - t3a < T3C ? ni3 - t3a : T3C;
-    const int64_t plane_stride = a.nq1 * a.nq2;
+    const int64_t plane_stride = a.cv.s3;
     const int *__restrict__ qlo1 = v1.qlo, *__restrict__ qlen1 = v1.qlen, *__restrict__ jlo1 = v1.jlo;
     const int *__restrict__ jlen1 = v1.jlen, *__restrict__ span1 = v1.span;
     const int mq1 = v1.maxq;
@@ -174,7 +172,7 @@ __global__ void __launch_bounds__(256, 1) k_tile(TileArgs a) {
     const bool int2 = nq2 == 2 * P + 1 && i2 >= P + 1 && i2 <= n2 - P - 2;  // interior pattern in dir 2
     const bool int3 = nq3 == 2 * P + 1 && i3 >= P + 1 && i3 <= (int)a.g.n[2] - P - 2 && CF::NCH == 1;
     // coefficient field restricted to this line
-    const double *__restrict__ Cl = a.coef + 1 + (int64_t)ql2 * a.nq1 + (int64_t)(ql3 - a.cq_b) * plane_stride;
+    const double *__restrict__ Cl = a.cv.ptr(0, 0, ql2, ql3 - a.cq_b);
 
     // CSR offset of row (0, i2, i3) relative to the first owned row; row i1 adds ni2*ni3*P1(i1)
     const int64_t line_off = a.g.offset(0, i2, i3) - a.val_base;
@@ -220,10 +218,10 @@ __global__ void __launch_bounds__(256, 1) k_tile(TileArgs a) {
                 const int ka = STIFF ? m : a.comp_mass;
                 const int kb = m == 0 ? 1 : (m == 1 ? 3 : 4);
                 const int kc = m == 0 ? 2 : (m == 1 ? 4 : 5);
-                const int64_t fo = (int64_t)c2 * a.nq1 + (qs + q1s);
-                const double *pa = Cl + (int64_t)ka * a.npts + fo;
-                const double *pb = Cl + (int64_t)kb * a.npts + fo;
-                const double *pc = Cl + (int64_t)kc * a.npts + fo;
+                const int64_t fo = (int64_t)c2 * a.cv.s2 + (int64_t)(qs + q1s) * a.cv.s1;
+                const double *pa = Cl + (int64_t)ka * a.cv.cs + fo;
+                const double *pb = Cl + (int64_t)kb * a.cv.cs + fo;
+                const double *pc = Cl + (int64_t)kc * a.cv.cs + fo;
                 const double *B3b = (const double *)B3s + b3;  // value (b3 = 0) or derivative column
                 // contribution of point c3 (coefficients ca, cb, cc) at staircase offset O (compile time)
                 auto point3 = [&](int c3, double ca, double cb, double cc, auto O) {
@@ -501,11 +499,8 @@ wq_status launch_tile_p(wq_plan_s *Pl, double *val, int32_t *col, int64_t pl_lo,
     TileArgs a;
     a.g.init(Pl);
     for (int l = 0; l < 3; ++l) a.v[l] = Pl->dir[l];
-    a.coef = Pl->coef;
-    a.nq1 = Pl->cld1;
-    a.nq2 = Pl->dir[1].nq;
+    a.cv = Pl->cview;
     a.cq_b = Pl->cq_b;
-    a.npts = Pl->cstride;
     a.comp_mass = Pl->comp_mass;
     a.val = val;
     a.col = col;
@@ -514,11 +509,7 @@ wq_status launch_tile_p(wq_plan_s *Pl, double *val, int32_t *col, int64_t pl_lo,
     a.lines = list;
     const int64_t lines = list ? n_list : Pl->dir[1].n * (pl_hi - pl_lo);
     const int64_t blocks = lines * CF::NCH;
-    static bool set = false;
-    if (!set) {
-        cudaFuncSetAttribute(k_tile<P, STIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
-        set = true;
-    }
+    wq_smem_attr((const void *)k_tile<P, STIFF>, CF::SMEM);
     if (blocks > 0) {
         k_tile<P, STIFF><<<(unsigned)blocks, CF::NT, CF::SMEM, s>>>(a);
         wq_count_launches(1);
@@ -549,7 +540,6 @@ wq_status dispatch_p(wq_plan_s *Pl, double *val, int32_t *col, int64_t lo, int64
 
 bool tile_supported(const wq_plan_s *P, int matrix) {
     if (P->d != 3 || P->p < 1 || P->p > 10) return false;
-    if (matrix == WQ_STIFFNESS && P->zlayout) return false;  // stiffness components are in the z layout
     for (int l = 0; l < 3; ++l)
         if (P->dir[l].maxq > 3 * P->p + 1) return false;  // a support holding both boundary spans
     return true;
@@ -563,15 +553,4 @@ wq_status launch_assemble_tile(wq_plan_s *P, int matrix, double *val, int32_t *c
     }
     return matrix == WQ_MASS ? dispatch_p<false>(P, val, col, plane_lo, plane_hi, val_base, s)
                              : dispatch_p<true>(P, val, col, plane_lo, plane_hi, val_base, s);
-}
-
-wq_status launch_assemble_tile_list(wq_plan_s *P, int matrix, const int32_t *lines, int64_t n_lines, double *val,
-                                    int32_t *col, int64_t val_base, cudaStream_t s) {
-    if (!tile_supported(P, matrix)) {
-        wq_set_error("tile kernel not available for this plan");
-        return WQ_EINVAL;
-    }
-    if (n_lines <= 0) return WQ_OK;
-    return matrix == WQ_MASS ? dispatch_p<false>(P, val, col, 0, 0, val_base, s, lines, n_lines)
-                             : dispatch_p<true>(P, val, col, 0, 0, val_base, s, lines, n_lines);
 }

@@ -31,10 +31,11 @@ bool z_types_match(const std::vector<int32_t> &qlo, const std::vector<int32_t> &
     }
     return true;
 }
-bool z_fetch_uniform(wq_plan_s *P, cudaStream_t s, ZUni &U, bool &types_ok) {
+bool z_fetch_uniform(wq_plan_s *P, ZUni &U, bool &types_ok, bool &cuda_ok) {
     const int p = P->p, K = 2 * p + 1, bs = wq_bstride(p);
     types_ok = false;
-    if (p > WQ_ZPMAX || cudaStreamSynchronize(s) != cudaSuccess) ZFAIL("p or stream");
+    cuda_ok = false;
+    if (p > WQ_ZPMAX) ZFAIL("p");
     memset(&U, 0, sizeof(U));
     // staircase types of every row (the boundary-line kernel unrolls them at compile time)
     for (int l = 0; l < 3; ++l) {
@@ -44,15 +45,16 @@ bool z_fetch_uniform(wq_plan_s *P, cudaStream_t s, ZUni &U, bool &types_ok) {
             cudaMemcpy(qlen.data(), v.qlen, v.n * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
             cudaMemcpy(jlo.data(), v.jlo, v.n * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
             cudaMemcpy(span.data(), v.span, v.nq * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
-            ZFAIL("copy");
+            return false;
         const bool ok = p == 2 ? z_types_match<2>(qlo, qlen, jlo, span, v.n)
                       : p == 3 ? z_types_match<3>(qlo, qlen, jlo, span, v.n)
                       : p == 4 ? z_types_match<4>(qlo, qlen, jlo, span, v.n)
                       : p == 5 ? z_types_match<5>(qlo, qlen, jlo, span, v.n)
                                : z_types_match<6>(qlo, qlen, jlo, span, v.n);
-        if (!ok) ZFAIL("dir %d: row staircase types do not match", l);
+        if (!ok) { cuda_ok = true; ZFAIL("dir %d: row staircase types do not match", l); }
     }
     types_ok = true;
+    cuda_ok = true;
     for (int l = 0; l < 3; ++l) {
         const DirView &v = P->dir[l];
         const int64_t n = v.n, nq = v.nq;
@@ -64,8 +66,10 @@ bool z_fetch_uniform(wq_plan_s *P, cudaStream_t s, ZUni &U, bool &types_ok) {
             cudaMemcpy(qlo.data(), v.qlo, n * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
             cudaMemcpy(qlen.data(), v.qlen, n * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
             cudaMemcpy(jlo.data(), v.jlo, n * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
-            cudaMemcpy(span.data(), v.span, nq * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+            cudaMemcpy(span.data(), v.span, nq * 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            cuda_ok = false;
             return false;
+        }
         const int64_t ir = n / 2;  // in [2p, n-1-2p]
         const double *Wr = W.data() + (size_t)ir * v.maxq * 4;
         double wsc[4] = {0, 0, 0, 0}, bsc[2] = {0, 0};
@@ -101,26 +105,36 @@ bool z_fetch_uniform(wq_plan_s *P, cudaStream_t s, ZUni &U, bool &types_ok) {
 }
 }  // namespace
 
+// Once per plan, after the rules have been built and synchronised (wq_plan_create): verify the row
+// staircase types the kernel compiles in, and fetch the uniform-mesh rules (reading R16).  A type
+// mismatch disables the z-line kernel for the plan (AUTO then runs another kernel); a CUDA failure
+// is WQ_ECUDA.
+wq_status zline_prepare(wq_plan_s *P) {
+    static_assert(sizeof(ZUni) <= sizeof(P->zuni_buf), "uniform table buffer");
+    ZUni U;
+    bool types_ok = false, cuda_ok = false;
+    bool ok = z_fetch_uniform(P, U, types_ok, cuda_ok);
+    if (!cuda_ok) {
+        wq_set_error("z-line preparation: device -> host copy of the rules failed");
+        return WQ_ECUDA;
+    }
+    if (!types_ok) {
+        P->zline_ok = 0;
+        return WQ_OK;
+    }
+    if (getenv("WQ_ZLINE_NO_UNIFORM")) ok = false;
+    P->zuni_state = ok ? 1 : -1;
+    if (ok) memcpy(P->zuni_buf, &U, sizeof(U));
+    return WQ_OK;
+}
+
 wq_status launch_assemble_zline(wq_plan_s *P, int cls, const int32_t *lines, int64_t n_lines, int64_t pl_lo,
                                 int64_t pl_hi, double *val, int32_t *col, int64_t val_base, cudaStream_t s) {
-    if (!P->coefz) {
-        wq_set_error("z-line kernel needs the z-layout coefficient field");
+    if (!P->zline_ok || P->zuni_state == 0) {
+        wq_set_error("z-line kernel not prepared for this plan");
         return WQ_EINVAL;
     }
     if (n_lines <= 0) return WQ_OK;
-    static_assert(sizeof(ZUni) <= sizeof(P->zuni_buf), "uniform table buffer");
-    if (P->zuni_state == 0) {
-        ZUni U;
-        bool types_ok = false;
-        bool ok = z_fetch_uniform(P, s, U, types_ok);
-        if (!types_ok) {
-            wq_set_error("z-line kernel: row staircases do not match the compiled row types");
-            return WQ_EINVAL;
-        }
-        if (getenv("WQ_ZLINE_NO_UNIFORM")) ok = false;
-        P->zuni_state = ok ? 1 : -1;
-        if (ok) memcpy(P->zuni_buf, &U, sizeof(U));
-    }
     ZUni U;
     memcpy(&U, P->zuni_buf, sizeof(U));
     const bool cu = P->zuni_state == 1;

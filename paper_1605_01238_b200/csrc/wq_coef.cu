@@ -14,6 +14,7 @@
 //   direct sum.
 #include <cstdlib>
 #include <type_traits>
+#include <algorithm>
 #include "wq_internal.cuh"
 
 namespace {
@@ -25,19 +26,19 @@ constexpr int NTC = TQ1 * TQ2;
 struct CoefArgs {
     DirView v[3];
     int d, p;
-    const double *ctrl;  // [N_DOF][d]
-    double *coef;        // [ncomp][points]
-    int64_t cq_b;        // first q_d of the sub-grid
-    int64_t nq_loc_d;    // q_d extent of the sub-grid
-    int64_t cld1, cstride, c0off;  // coefficient layout (wq_internal.cuh)
-    int ncomp_s, ncomp;
+    const double *ctrl;   // [N_DOF][d]
+    const double *kappa;  // [N_DOF] diffusion coefficient net or null (= 1), reading R17
+    const double *gamma;  // [N_DOF] reaction coefficient net or null (= 1)
+    double *coef;         // [ncomp][cs] (d = 3: z layout, d <= 2: standard; wq_internal.cuh CoefView)
+    int64_t cs;
+    int64_t cq_b;         // first q_d of the sub-grid
+    int64_t nq_loc_d;     // q_d extent of the sub-grid
+    int ncomp_s, comp_mass;
     int need_s, need_m;
     Flags *flags;
-    const double *dnet;  // z layout: derivative control nets [k][m][c] (k_dnet)
-    // z layout of the stiffness components (wq_internal.cuh): [comp][q_1][q_2][q_3 - cq_b]
-    int zlayout;
-    double *coefz;
-    int64_t zld, zcs;
+    const double *dnet;   // d = 3: derivative control nets (+ coefficient nets) [k][NE] (k_dnet)
+    int64_t k3b;          // first control plane held in dnet
+    int64_t zld;          // d = 3: z-layout row length
 };
 
 // table rows at grid point q: N = degree p (functions span..span+p, stride 2:
@@ -51,97 +52,32 @@ __device__ __forceinline__ double dscale(const DirView &v, int p, int64_t k) {
     return (double)p / (v.knots[k + p] - v.knots[k]);
 }
 
+// d <= 2 (standard layout): the control net read directly; CTA = TQ1 x TQ2 points (d = 2) or TQ1
+// points (d = 1).  The coefficient nets kappa, gamma are evaluated with the plain basis values.
 template <int D>
 __global__ void __launch_bounds__(NTC) k_coef(CoefArgs a) {
+    static_assert(D == 1 || D == 2, "d <= 2");
     extern __shared__ __align__(16) double sm[];
     const int p = a.p;
-    const DirView &v1 = a.v[0], &v2 = a.v[1], &v3 = a.v[2];
-    // d = 3: blockIdx.x = q_3 plane (consecutive CTAs write neighbouring q_3 of the z layout)
-    const int64_t q1a = (int64_t)(D == 3 ? blockIdx.y : blockIdx.x) * TQ1;
-    const int64_t q2a = D >= 2 ? (int64_t)(D == 3 ? blockIdx.z : blockIdx.y) * TQ2 : 0;
-    const int64_t q3l = D == 3 ? (int64_t)blockIdx.x : 0;  // local plane
-    const int64_t q3 = D == 3 ? a.cq_b + q3l : 0;
+    const DirView &v1 = a.v[0], &v2 = a.v[1];
+    const int64_t q1a = (int64_t)blockIdx.x * TQ1;
+    const int64_t q2a = D >= 2 ? (int64_t)blockIdx.y * TQ2 : 0;
     const int64_t q1off = D == 1 ? a.cq_b : 0;  // D == 1: direction 1 is the slab direction
     const int64_t nq1 = D == 1 ? a.nq_loc_d : v1.nq;
-    const int64_t nq2 = D >= 2 ? (D == 2 ? a.nq_loc_d : v2.nq) : 1;
+    const int64_t nq2 = D == 2 ? a.nq_loc_d : 1;
     const int64_t q2off = D == 2 ? a.cq_b : 0;  // D == 2: direction 2 is the slab direction
     const int64_t q1e = q1a + TQ1 < nq1 ? q1a + TQ1 : nq1;
     const int64_t q2e = q2a + TQ2 < nq2 ? q2a + TQ2 : nq2;
     const int nt1 = (int)(q1e - q1a), nt2 = (int)(q2e - q2a);
-    const int64_t k1a = v1.span[q1off + q1a], k1e = v1.span[q1off + q1e - 1] + p + 1;
-    const int K1 = (int)(k1e - k1a);
-    int64_t k2a = 0, k2e = 1;
-    if (D >= 2) { k2a = v2.span[q2off + q2a]; k2e = v2.span[q2off + q2e - 1] + p + 1; }
-    const int K2 = (int)(k2e - k2a);
-    const int64_t n1 = v1.n, n2 = D >= 2 ? v2.n : 1;
-    const int K1M = TQ1 + p + 1, K2M = TQ2 + p + 1;  // bounds of K1, K2 (smem sized by the actual p)
-    // smem: A[3 variants][3 comps][K2M][K1M] (D == 3), X[TQ2][3 variants][3 comps][K1M]
-    double *Asm = sm;
-    double *Xsm = sm + (D == 3 ? 9 * K2M * K1M : 0);
+    const int64_t k1a = v1.span[q1off + q1a];
+    const int64_t n1 = v1.n;
+    const int K1M = TQ1 + p + 1;
+    // smem (D == 2): X[TQ2][5 rows: 0,1 = N2.Q^1 (2 comps), 2,3 = M2.Q^2, 4 = N2.kappa, 5 = N2.gamma][K1M]
+    double *Xsm = sm;
     const int tid = threadIdx.x;
     const double *P = a.ctrl;
-
-    if (D == 3) {
-        // stage A: contract k_3.  A1 = N3 . Q^1, A2 = N3 . Q^2, A3 = M3 . Q^3
-        const double *n3 = Ntab(v3, p, q3), *m3 = Mtab(v3, p, q3);
-        const int64_t e3 = v3.span[q3];
-        for (int t = tid; t < K2 * K1; t += blockDim.x) {
-            const int c2 = t / K1, c1 = t % K1;
-            const int64_t k1 = k1a + c1, k2 = k2a + c2;
-            double A1[3] = {0, 0, 0}, A2[3] = {0, 0, 0}, A3[3] = {0, 0, 0};
-            const double s1 = k1 >= 1 ? dscale(v1, p, k1) : 0.0;
-            const double s2 = k2 >= 1 ? dscale(v2, p, k2) : 0.0;
-            double prev[3] = {0, 0, 0};
-            for (int r = 0; r <= p; ++r) {
-                const int64_t k3 = e3 + r;
-                const int64_t k = k1 + n1 * (k2 + n2 * k3);
-                const double nv = n3[2 * r];
-                const double s3 = r >= 1 ? dscale(v3, p, k3) : 0.0;
-                #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const double cur = __ldg(P + k * 3 + c);
-                    const double d1 = k1 >= 1 ? (cur - __ldg(P + (k - 1) * 3 + c)) * s1 : 0.0;
-                    const double d2 = k2 >= 1 ? (cur - __ldg(P + (k - n1) * 3 + c)) * s2 : 0.0;
-                    A1[c] = fma(nv, d1, A1[c]);
-                    A2[c] = fma(nv, d2, A2[c]);
-                    if (r >= 1) A3[c] = fma(m3[r - 1], (cur - prev[c]) * s3, A3[c]);
-                    prev[c] = cur;
-                }
-            }
-            #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                Asm[((0 * 3 + c) * K2M + c2) * K1M + c1] = A1[c];
-                Asm[((1 * 3 + c) * K2M + c2) * K1M + c1] = A2[c];
-                Asm[((2 * 3 + c) * K2M + c2) * K1M + c1] = A3[c];
-            }
-        }
-        __syncthreads();
-        // stage B: contract k_2.  X1 = N2 . A1, X2 = M2 . A2, X3 = N2 . A3
-        for (int t = tid; t < nt2 * K1; t += blockDim.x) {
-            const int t2 = t / K1, c1 = t % K1;
-            const int64_t q2 = q2a + t2;
-            const double *n2t = Ntab(v2, p, q2), *m2t = Mtab(v2, p, q2);
-            const int c2s = (int)(v2.span[q2] - k2a);
-            double X1[3] = {0, 0, 0}, X2[3] = {0, 0, 0}, X3[3] = {0, 0, 0};
-            for (int r = 0; r <= p; ++r) {
-                const double nv = n2t[2 * r], mv = r < p ? m2t[r] : 0.0;
-                #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    X1[c] = fma(nv, Asm[((0 * 3 + c) * K2M + c2s + r) * K1M + c1], X1[c]);
-                    X3[c] = fma(nv, Asm[((2 * 3 + c) * K2M + c2s + r) * K1M + c1], X3[c]);
-                    if (r < p) X2[c] = fma(mv, Asm[((1 * 3 + c) * K2M + c2s + 1 + r) * K1M + c1], X2[c]);
-                }
-            }
-            #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                Xsm[((t2 * 3 + 0) * 3 + c) * K1M + c1] = X1[c];
-                Xsm[((t2 * 3 + 1) * 3 + c) * K1M + c1] = X2[c];
-                Xsm[((t2 * 3 + 2) * 3 + c) * K1M + c1] = X3[c];
-            }
-        }
-        __syncthreads();
-    } else if (D == 2) {
-        // stage B directly on the control net: X1 = N2 . Q^1, X2 = M2 . Q^2
+    if (D == 2) {
+        const int K1 = (int)(v1.span[q1e - 1] + p + 1 - k1a);
         for (int t = tid; t < nt2 * K1; t += blockDim.x) {
             const int t2 = t / K1, c1 = t % K1;
             const int64_t q2 = q2off + q2a + t2;
@@ -149,7 +85,7 @@ __global__ void __launch_bounds__(NTC) k_coef(CoefArgs a) {
             const int64_t e2 = v2.span[q2];
             const int64_t k1 = k1a + c1;
             const double s1 = k1 >= 1 ? dscale(v1, p, k1) : 0.0;
-            double X1[2] = {0, 0}, X2[2] = {0, 0}, prev[2] = {0, 0};
+            double X1[2] = {0, 0}, X2[2] = {0, 0}, prev[2] = {0, 0}, Xk = 0.0, Xg = 0.0;
             for (int r = 0; r <= p; ++r) {
                 const int64_t k2 = e2 + r;
                 const int64_t k = k1 + n1 * k2;
@@ -162,12 +98,12 @@ __global__ void __launch_bounds__(NTC) k_coef(CoefArgs a) {
                     if (r >= 1) X2[c] = fma(m2t[r - 1], (cur - prev[c]) * s2, X2[c]);
                     prev[c] = cur;
                 }
+                if (a.kappa && k1 < n1) Xk = fma(n2t[2 * r], __ldg(a.kappa + k), Xk);
+                if (a.gamma && k1 < n1) Xg = fma(n2t[2 * r], __ldg(a.gamma + k), Xg);
             }
-            #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                Xsm[((t2 * 3 + 0) * 3 + c) * K1M + c1] = X1[c];
-                Xsm[((t2 * 3 + 1) * 3 + c) * K1M + c1] = X2[c];
-            }
+            double *X = Xsm + t2 * 6 * K1M + c1;
+            X[0 * K1M] = X1[0]; X[1 * K1M] = X1[1]; X[2 * K1M] = X2[0]; X[3 * K1M] = X2[1];
+            X[4 * K1M] = Xk; X[5 * K1M] = Xg;
         }
         __syncthreads();
     }
@@ -178,112 +114,103 @@ __global__ void __launch_bounds__(NTC) k_coef(CoefArgs a) {
     const double *n1t = Ntab(v1, p, q1off + q1), *m1t = Mtab(v1, p, q1off + q1);
     const int64_t e1 = v1.span[q1off + q1];
     const int c1s = (int)(e1 - k1a);
-    const int64_t ld1 = D == 3 ? a.cld1 : nq1;
-    const int64_t npts_plane = ld1 * (D >= 2 ? nq2 : 1);
-    const int64_t npts = a.cstride;
-    {
-        double J[3][3];
-        #pragma unroll
-        for (int c = 0; c < 3; ++c)
+    double J[2][2] = {{0, 0}, {0, 0}}, kap = a.kappa ? 0.0 : 1.0, gam = a.gamma ? 0.0 : 1.0;
+    if (D == 1) {
+        for (int r = 0; r < p; ++r) {
+            const int64_t k = e1 + 1 + r;
+            J[0][0] = fma(m1t[r], (__ldg(P + k) - __ldg(P + k - 1)) * dscale(v1, p, k), J[0][0]);
+        }
+        for (int r = 0; r <= p; ++r) {
+            if (a.kappa) kap = fma(n1t[2 * r], __ldg(a.kappa + e1 + r), kap);
+            if (a.gamma) gam = fma(n1t[2 * r], __ldg(a.gamma + e1 + r), gam);
+        }
+    } else {
+        const double *X = Xsm + t2 * 6 * K1M;
+        for (int r = 0; r <= p; ++r) {
+            const double nv = n1t[2 * r], mv = r < p ? m1t[r] : 0.0;
             #pragma unroll
-            for (int m = 0; m < 3; ++m) J[c][m] = 0.0;
-        if (D == 1) {
-            for (int r = 0; r < p; ++r) {
-                const int64_t k = e1 + 1 + r;
-                J[0][0] = fma(m1t[r], (__ldg(P + k) - __ldg(P + k - 1)) * dscale(v1, p, k), J[0][0]);
+            for (int c = 0; c < 2; ++c) {
+                if (r < p) J[c][0] = fma(mv, X[c * K1M + c1s + 1 + r], J[c][0]);
+                J[c][1] = fma(nv, X[(2 + c) * K1M + c1s + r], J[c][1]);
             }
-        } else {
-            const double *X = Xsm + (t2 * 3) * 3 * K1M;
-            for (int r = 0; r <= p; ++r) {
-                const double nv = n1t[2 * r], mv = r < p ? m1t[r] : 0.0;
-                #pragma unroll
-                for (int c = 0; c < D; ++c) {
-                    if (r < p) J[c][0] = fma(mv, X[(0 * 3 + c) * K1M + c1s + 1 + r], J[c][0]);
-                    J[c][1] = fma(nv, X[(1 * 3 + c) * K1M + c1s + r], J[c][1]);
-                    if (D == 3) J[c][2] = fma(nv, X[(2 * 3 + c) * K1M + c1s + r], J[c][2]);
-                }
-            }
+            if (a.kappa) kap = fma(nv, X[4 * K1M + c1s + r], kap);
+            if (a.gamma) gam = fma(nv, X[5 * K1M + c1s + r], gam);
         }
-        double det, adj[3][3];
-        if (D == 1) {
-            det = J[0][0];
-            adj[0][0] = 1.0;
-        } else if (D == 2) {
-            det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
-            adj[0][0] = J[1][1]; adj[0][1] = -J[0][1];
-            adj[1][0] = -J[1][0]; adj[1][1] = J[0][0];
-        } else {
-            adj[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
-            adj[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
-            adj[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
-            adj[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
-            adj[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
-            adj[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
-            adj[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
-            adj[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
-            adj[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
-            det = J[0][0] * adj[0][0] + J[0][1] * adj[1][0] + J[0][2] * adj[2][0];
-        }
-        if (!(det > 0.0) && !(det < 0.0)) atomicOr(&a.flags->det_zero, 1);
-        else if (det > 0.0) { if (!a.flags->det_pos) atomicOr(&a.flags->det_pos, 1); }
-        else { if (!a.flags->det_neg) atomicOr(&a.flags->det_neg, 1); }
-        const double ad = fabs(det);
-        const double inv = 1.0 / ad;
-        const int64_t pt = (D == 3 ? a.c0off : 0) + q1 + ld1 * (D >= 2 ? (q2a + t2) : 0) + (D == 3 ? npts_plane * q3l : 0);
-        int comp = 0;
-        if (a.need_s) {
-            #pragma unroll
-            for (int l = 0; l < D; ++l)
-                #pragma unroll
-                for (int m = l; m < D; ++m) {
-                    double s = 0.0;
-                    #pragma unroll
-                    for (int k = 0; k < D; ++k) s = fma(adj[l][k], adj[m][k], s);
-                    if (D == 3 && a.zlayout)
-                        a.coefz[(int64_t)comp * a.zcs + (q1 * v2.nq + q2a + t2) * a.zld + q3l] = s * inv;
-                    else
-                        a.coef[(int64_t)comp * npts + pt] = s * inv;
-                    ++comp;
-                }
-        }
-        if (a.need_m) a.coef[(int64_t)(a.zlayout ? 0 : comp) * npts + pt] = ad;
     }
+    double det, adj[2][2];
+    if (D == 1) {
+        det = J[0][0];
+        adj[0][0] = 1.0;
+    } else {
+        det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        adj[0][0] = J[1][1]; adj[0][1] = -J[0][1];
+        adj[1][0] = -J[1][0]; adj[1][1] = J[0][0];
+    }
+    if (!(det > 0.0) && !(det < 0.0)) atomicOr(&a.flags->det_zero, 1);
+    else if (det > 0.0) { if (!a.flags->det_pos) atomicOr(&a.flags->det_pos, 1); }
+    else { if (!a.flags->det_neg) atomicOr(&a.flags->det_neg, 1); }
+    const double ad = fabs(det);
+    const double inv = kap / ad;
+    const int64_t pt = q1 + (D == 2 ? v1.nq * (q2a + t2) : 0);
+    if (a.need_s) {
+        int comp = 0;
+        #pragma unroll
+        for (int l = 0; l < D; ++l)
+            #pragma unroll
+            for (int m = l; m < D; ++m) {
+                double sv = 0.0;
+                #pragma unroll
+                for (int k = 0; k < D; ++k) sv = fma(adj[l][k], adj[m][k], sv);
+                a.coef[(int64_t)comp * a.cs + pt] = sv * inv;
+                ++comp;
+            }
+    }
+    if (a.need_m) a.coef[(int64_t)a.comp_mass * a.cs + pt] = gam * ad;
 }
 
-// z layout (d = 3, stiffness for the z-line kernel): the same sum factorisation with the roles of
-// the directions permuted so that the fast thread index runs along q_3, the contiguous axis of
-// [comp][q_1][q_2][q_3], while stage A still reads the control net along its contiguous k_1:
+// d = 3 (z layout): the same sum factorisation with the roles of the directions permuted so that the
+// fast thread index runs along q_3, the contiguous axis of [comp][q_1][q_2][q_3], while stage A
+// still reads the control net along its contiguous k_1:
 // CTA = TQF q_3 points x TQM q_1 points of one q_2 plane;
-//   stage A contracts k_2 (plane):   A0 = N2 . Q^1, A1 = M2 . Q^2, A2 = N2 . Q^3   (threads over k_1, k_3)
-//   stage B contracts k_1:           X0 = M1 . A0,  X1 = N1 . A1,  X2 = N1 . A2
-//   stage C contracts k_3 per point: J[:,0] = N3 . X0, J[:,1] = N3 . X1, J[:,2] = M3 . X2
+//   stage A contracts k_2 (plane):   A0 = N2 . Q^1, A1 = M2 . Q^2, A2 = N2 . Q^3, Ak = N2 . kappa, ...
+//   stage B contracts k_1:           X0 = M1 . A0,  X1 = N1 . A1,  X2 = N1 . A2,  Xk = N1 . Ak
+//   stage C contracts k_3 per point: J[:,0] = N3 . X0, J[:,1] = N3 . X1, J[:,2] = M3 . X2,
+//                                    kappa = N3 . Xk, gamma likewise
 constexpr int TQF = 32;
 
 // derivative control nets (d = 3): Q^m_k = (P_k - P_{k - e_m}) p / (xi_{k_m + p} - xi_{k_m}) for k_m >= 1,
-// else 0; [k][m][c], one thread per control point.  Same expressions as the inline differences of
-// k_coef (bit-identical), computed once per build instead of (p+1) times per grid tile.
-__global__ void k_dnet(const double *__restrict__ P, double *__restrict__ Q, DirView v0, DirView v1, DirView v2,
-                       int p, int64_t ntot) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= ntot) return;
+// else 0, then the coefficient nets: [k][NE], NE = 9 + NNU, entries (m, c) = 3 m + c, 9 = kappa,
+// 9 or 10 = gamma; one thread per control point of the planes k_3 in [k3b, k3b + ntot / (n0 n1)).
+template <int NNU>
+__global__ void k_dnet(const double *__restrict__ P, const double *__restrict__ kap, const double *__restrict__ gam,
+                       double *__restrict__ Q, DirView v0, DirView v1, DirView v2, int p, int64_t k3b, int64_t ntot) {
+    constexpr int NE = 9 + NNU;
+    const int64_t kl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (kl >= ntot) return;
     const int64_t n0 = v0.n, n1 = v1.n;
-    const int64_t k0 = k % n0, k1 = (k / n0) % n1, k2 = k / (n0 * n1);
+    const int64_t k0 = kl % n0, k1 = (kl / n0) % n1, k2 = k3b + kl / (n0 * n1);
+    const int64_t k = k0 + n0 * (k1 + n1 * k2);
     const double s0 = k0 >= 1 ? dscale(v0, p, k0) : 0.0;
     const double s1 = k1 >= 1 ? dscale(v1, p, k1) : 0.0;
     const double s2 = k2 >= 1 ? dscale(v2, p, k2) : 0.0;
+    double *q = Q + kl * NE;
     #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const double cur = P[k * 3 + c];
-        Q[k * 9 + 0 + c] = k0 >= 1 ? (cur - P[(k - 1) * 3 + c]) * s0 : 0.0;
-        Q[k * 9 + 3 + c] = k1 >= 1 ? (cur - P[(k - n0) * 3 + c]) * s1 : 0.0;
-        Q[k * 9 + 6 + c] = k2 >= 1 ? (cur - P[(k - n0 * n1) * 3 + c]) * s2 : 0.0;
+        q[0 + c] = k0 >= 1 ? (cur - P[(k - 1) * 3 + c]) * s0 : 0.0;
+        q[3 + c] = k1 >= 1 ? (cur - P[(k - n0) * 3 + c]) * s1 : 0.0;
+        q[6 + c] = k2 >= 1 ? (cur - P[(k - n0 * n1) * 3 + c]) * s2 : 0.0;
     }
+    int e = 9;
+    if (NNU > 0 && kap) q[e++] = kap[k];
+    if (NNU > 0 && gam) q[e++] = gam[k];
 }
 // PP > 0: the degree as a compile-time constant (p <= 6), so that the r loops unroll and each thread
 // issues all of its derivative-net loads of stage A before the first FMA (the kernel is bound by
-// their L2 latency); PP = 0: any degree
-template <int TQM, int PP>
+// their L2 latency); PP = 0: any degree.  NNU: number of coefficient nets (0..2).
+template <int TQM, int PP, int NNU>
 __global__ void __launch_bounds__(TQF * TQM, TQM == 16 ? 3 : 1) k_coefz(CoefArgs a) {
+    constexpr int NE = 9 + NNU;
     extern __shared__ __align__(16) double sm[];
     const int p = PP > 0 ? PP : a.p;
     const DirView &v0 = a.v[0], &v1 = a.v[1], &v2 = a.v[2];
@@ -297,29 +224,29 @@ __global__ void __launch_bounds__(TQF * TQM, TQM == 16 ? 3 : 1) k_coefz(CoefArgs
     const int64_t kma = v0.span[qma], kme = v0.span[qme - 1] + p + 1;
     const int KF = (int)(kfe - kfa), KM = (int)(kme - kma);
     const int KFM = TQF + p + 1, KMM = TQM + p + 1;
-    double *Asm = sm;                      // [3 variants][3 comps][KFM][KMM]  (k_1 fastest)
-    double *Xsm = sm;                      // [TQM][3 variants][3 comps][KFM], over Asm once stage B has read it
+    double *Asm = sm;                      // [NE entries][KFM][KMM]  (k_1 fastest)
+    double *Xsm = sm;                      // [TQM][NE][KFM], over Asm once stage B has read it
     const int tid = threadIdx.x;
-    const double *P = a.ctrl;
     const int64_t n0 = v0.n, n1 = v1.n;
     {
-        // stage A: contract k_2 with the plane's basis.  Threads over (k_3, e) with e = (k_1 - kma)*9 +
-        // 3*variant + comp: for fixed (k_2, k_3) the derivative-net entries of the tile's k_1 range are
-        // one contiguous run, so consecutive threads load consecutive doubles (coalesced); every
-        // entry is an independent sum over k_2 (variants 0, 2 with N2, variant 1 with M2)
+        // stage A: contract k_2 with the plane's basis.  Threads over (k_3, e) with e = (k_1 - kma)*NE +
+        // entry: for fixed (k_2, k_3) the net entries of the tile's k_1 range are one contiguous run, so
+        // consecutive threads load consecutive doubles (coalesced); every entry is an independent sum
+        // over k_2 (derivative in direction 2 (entries 3..5) with M2, all others with N2)
         const double *nt = Ntab(v1, p, q1p), *mt = Mtab(v1, p, q1p);
         const int64_t e1 = v1.span[q1p];
         const double *Q = a.dnet;
-        const int KE = KM * 9;
+        const int KE = KM * NE;
         for (int t = tid; t < KF * KE; t += blockDim.x) {
             const int cf = t / KE, e = t % KE;
-            const int cm = e / 9, vc = e % 9, var = vc / 3;
-            const double *Qe = Q + (kma + n0 * (e1 + n1 * (kfa + cf))) * 9 + e;
+            const int cm = e / NE, vc = e % NE;
+            const bool dv = vc >= 3 && vc < 6;
+            const double *Qe = Q + (kma + n0 * (e1 + n1 * (kfa - a.k3b + cf))) * NE + e;
             double acc = 0.0;
             #pragma unroll
             for (int r = 0; r <= p; ++r) {
-                const double w = var == 1 ? (r >= 1 ? mt[r - 1] : 0.0) : nt[2 * r];
-                if (var != 1 || r >= 1) acc = fma(w, __ldg(Qe + r * n0 * 9), acc);
+                const double w = dv ? (r >= 1 ? mt[r - 1] : 0.0) : nt[2 * r];
+                if (!dv || r >= 1) acc = fma(w, __ldg(Qe + r * n0 * NE), acc);
             }
             Asm[(vc * KFM + cf) * KMM + cm] = acc;
         }
@@ -329,7 +256,7 @@ __global__ void __launch_bounds__(TQF * TQM, TQM == 16 ? 3 : 1) k_coefz(CoefArgs
     // registers until every thread has read Asm, then X is written over it (smem per CTA = max of
     // the two arrays instead of their sum: one more CTA per SM)
     constexpr int XIT = 2;  // ceil((TQF + p + 1) / TQF) items per thread for p < TQF
-    double Xr[XIT][9];
+    double Xr[XIT][NE];
     #pragma unroll
     for (int it = 0; it < XIT; ++it) {
         const int t = tid + it * (int)blockDim.x;
@@ -338,19 +265,23 @@ __global__ void __launch_bounds__(TQF * TQM, TQM == 16 ? 3 : 1) k_coefz(CoefArgs
         const int64_t q0 = qma + tm;
         const double *nt = Ntab(v0, p, q0), *mt = Mtab(v0, p, q0);
         const int cms = (int)(v0.span[q0] - kma);
-        double X0[3] = {0, 0, 0}, X1[3] = {0, 0, 0}, X2[3] = {0, 0, 0};
+        double X[NE];
+        #pragma unroll
+        for (int vc = 0; vc < NE; ++vc) X[vc] = 0.0;
         #pragma unroll
         for (int r = 0; r <= p; ++r) {
             const double nv = nt[2 * r], mv = r < p ? mt[r] : 0.0;
             #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                X1[c] = fma(nv, Asm[((1 * 3 + c) * KFM + cf) * KMM + cms + r], X1[c]);
-                X2[c] = fma(nv, Asm[((2 * 3 + c) * KFM + cf) * KMM + cms + r], X2[c]);
-                if (r < p) X0[c] = fma(mv, Asm[((0 * 3 + c) * KFM + cf) * KMM + cms + 1 + r], X0[c]);
+            for (int vc = 0; vc < NE; ++vc) {
+                if (vc < 3) {  // derivative in direction 1: M1
+                    if (r < p) X[vc] = fma(mv, Asm[(vc * KFM + cf) * KMM + cms + 1 + r], X[vc]);
+                } else {
+                    X[vc] = fma(nv, Asm[(vc * KFM + cf) * KMM + cms + r], X[vc]);
+                }
             }
         }
         #pragma unroll
-        for (int c = 0; c < 3; ++c) { Xr[it][c] = X0[c]; Xr[it][3 + c] = X1[c]; Xr[it][6 + c] = X2[c]; }
+        for (int vc = 0; vc < NE; ++vc) Xr[it][vc] = X[vc];
     }
     __syncthreads();
     #pragma unroll
@@ -359,7 +290,7 @@ __global__ void __launch_bounds__(TQF * TQM, TQM == 16 ? 3 : 1) k_coefz(CoefArgs
         if (t >= ntm * KF) break;
         const int tm = t / KF, cf = t % KF;
         #pragma unroll
-        for (int vc = 0; vc < 9; ++vc) Xsm[(tm * 9 + vc) * KFM + cf] = Xr[it][vc];
+        for (int vc = 0; vc < NE; ++vc) Xsm[(tm * NE + vc) * KFM + cf] = Xr[it][vc];
     }
     __syncthreads();
     // stage C: one thread per point (q_3 fastest)
@@ -368,12 +299,12 @@ __global__ void __launch_bounds__(TQF * TQM, TQM == 16 ? 3 : 1) k_coefz(CoefArgs
     const int64_t q2l = qfa + tf, q0 = qma + tm;
     const double *nt = Ntab(v2, p, cqb + q2l), *mt = Mtab(v2, p, cqb + q2l);
     const int cfs = (int)(v2.span[cqb + q2l] - kfa);
-    double J[3][3];
+    double J[3][3], nu[2] = {0.0, 0.0};
     #pragma unroll
     for (int c = 0; c < 3; ++c)
         #pragma unroll
         for (int m = 0; m < 3; ++m) J[c][m] = 0.0;
-    const double *X = Xsm + (tm * 3) * 3 * KFM;
+    const double *X = Xsm + (tm * NE) * KFM;
     #pragma unroll
     for (int r = 0; r <= p; ++r) {
         const double nv = nt[2 * r], mv = r < p ? mt[r] : 0.0;
@@ -383,7 +314,12 @@ __global__ void __launch_bounds__(TQF * TQM, TQM == 16 ? 3 : 1) k_coefz(CoefArgs
             J[c][1] = fma(nv, X[(1 * 3 + c) * KFM + cfs + r], J[c][1]);
             if (r < p) J[c][2] = fma(mv, X[(2 * 3 + c) * KFM + cfs + 1 + r], J[c][2]);
         }
+        #pragma unroll
+        for (int u = 0; u < NNU; ++u) nu[u] = fma(nv, X[(9 + u) * KFM + cfs + r], nu[u]);
     }
+    // coefficient values: kappa then gamma among the NNU nets
+    const double kap = a.kappa ? nu[0] : 1.0;
+    const double gam = a.gamma ? nu[a.kappa ? 1 : 0] : 1.0;
     double adj[3][3];
     adj[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
     adj[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
@@ -398,51 +334,77 @@ __global__ void __launch_bounds__(TQF * TQM, TQM == 16 ? 3 : 1) k_coefz(CoefArgs
     if (!(det > 0.0) && !(det < 0.0)) atomicOr(&a.flags->det_zero, 1);
     else if (det > 0.0) { if (!a.flags->det_pos) atomicOr(&a.flags->det_pos, 1); }
     else { if (!a.flags->det_neg) atomicOr(&a.flags->det_neg, 1); }
-    const double ad = fabs(det), inv = 1.0 / ad;
-    int comp = 0;
-    #pragma unroll
-    for (int l = 0; l < 3; ++l)
+    const double ad = fabs(det), inv = kap / ad;
+    const int64_t pt = (q0 * v1.nq + q1p) * a.zld + q2l;
+    if (a.need_s) {
+        int comp = 0;
         #pragma unroll
-        for (int m = l; m < 3; ++m) {
-            double sv = 0.0;
+        for (int l = 0; l < 3; ++l)
             #pragma unroll
-            for (int k = 0; k < 3; ++k) sv = fma(adj[l][k], adj[m][k], sv);
-            a.coefz[(int64_t)comp * a.zcs + (q0 * v1.nq + q1p) * a.zld + q2l] = sv * inv;
-            ++comp;
-        }
-    if (a.need_m) a.coef[a.c0off + q0 + a.cld1 * (q1p + v1.nq * q2l)] = ad;  // standard layout, component 0
+            for (int m = l; m < 3; ++m) {
+                double sv = 0.0;
+                #pragma unroll
+                for (int k = 0; k < 3; ++k) sv = fma(adj[l][k], adj[m][k], sv);
+                a.coef[(int64_t)comp * a.cs + pt] = sv * inv;
+                ++comp;
+            }
+    }
+    if (a.need_m) a.coef[(int64_t)a.comp_mass * a.cs + pt] = gam * ad;
 }
 
 }  // namespace
 
-wq_status launch_coef(wq_plan_s *P, const double *ctrl, cudaStream_t s) {
+wq_status launch_coef(wq_plan_s *P, const double *ctrl, const double *kappa, const double *gamma, cudaStream_t s) {
     CoefArgs a;
     a.dnet = nullptr;
     for (int l = 0; l < 3; ++l) a.v[l] = P->dir[l];
     a.d = P->d;
     a.p = P->p;
     a.ctrl = ctrl;
+    a.kappa = kappa;
+    a.gamma = gamma;
     a.coef = P->coef;
+    a.cs = P->zcs;
     a.cq_b = P->cq_b;
     a.nq_loc_d = P->cq_e - P->cq_b;
-    a.cld1 = P->cld1;
-    a.c0off = P->c0off;
-    a.cstride = P->cstride;
     a.ncomp_s = P->ncomp_s;
-    a.ncomp = P->ncomp;
+    a.comp_mass = P->comp_mass;
     a.need_s = P->need_stiff;
     a.need_m = P->need_mass;
     a.flags = P->flags;
-    a.zlayout = P->zlayout;
-    a.coefz = P->coefz;
     a.zld = P->zld;
-    a.zcs = P->zcs;
-    const int K1M = TQ1 + P->p + 1, K2M = TQ2 + P->p + 1;
-    if (P->d == 3 && P->zlayout) {
-        const int64_t ntot = P->dir[0].n * P->dir[1].n * P->dir[2].n;
-        if (P->dnet_bytes < sizeof(double) * 9 * (size_t)ntot) {
+    a.k3b = 0;
+    const int nnu = (kappa ? 1 : 0) + (gamma ? 1 : 0);
+    if (P->d == 3) {
+        // control planes seen by the slab's points: spans of cq_b .. cq_e - 1 plus p, and one below
+        // for the derivative differences (the derivative nets are formed on the slab + halo only)
+        const DirView &v2 = P->dir[2];
+        const int p = P->p;
+        int64_t spb = 0, spe = 0;
+        {
+            // span of a grid point from the integer point layout (reading R1): boundary span 0 holds
+            // points 0..p+1, knot e sits at p + 2e, midpoint of span e at p + 2e + 1
+            auto span_of = [&](int64_t g) -> int64_t {
+                const int64_t E = v2.E, nq = v2.nq;
+                if (g <= p + 1) return 0;
+                if (E >= 2 && g >= p + 2 * (E - 1) + 1) return E - 1;
+                if (g >= nq - 1) return E - 1;
+                const int64_t t = g - p;
+                return (t & 1) == 0 ? (t / 2 < E ? t / 2 : E - 1) : (t - 1) / 2;
+            };
+            spb = span_of(P->cq_b);
+            spe = span_of(P->cq_e - 1);
+        }
+        const int64_t k3b = spb >= 1 ? spb - 1 : 0;       // control index of span s: s .. s + p
+        const int64_t k3e = std::min<int64_t>(spe + p + 1, v2.n);
+        P->k3b = k3b;
+        P->k3e = k3e;
+        a.k3b = k3b;
+        const int64_t ntot = P->dir[0].n * P->dir[1].n * (k3e - k3b);
+        const size_t need = sizeof(double) * (9 + nnu) * (size_t)ntot;
+        if (P->dnet_bytes < need) {
             if (P->dnet) cudaFree(P->dnet);
-            P->dnet_bytes = sizeof(double) * 9 * (size_t)ntot;
+            P->dnet_bytes = need;
             if (cudaMalloc((void **)&P->dnet, P->dnet_bytes) != cudaSuccess) {
                 P->dnet = nullptr;
                 P->dnet_bytes = 0;
@@ -450,40 +412,37 @@ wq_status launch_coef(wq_plan_s *P, const double *ctrl, cudaStream_t s) {
                 return WQ_ENOMEM;
             }
         }
-        k_dnet<<<(unsigned)((ntot + 255) / 256), 256, 0, s>>>(ctrl, P->dnet, P->dir[0], P->dir[1], P->dir[2], P->p, ntot);
+        const unsigned gd = (unsigned)((ntot + 255) / 256);
+        if (nnu == 0) k_dnet<0><<<gd, 256, 0, s>>>(ctrl, kappa, gamma, P->dnet, P->dir[0], P->dir[1], P->dir[2], P->p, k3b, ntot);
+        else if (nnu == 1) k_dnet<1><<<gd, 256, 0, s>>>(ctrl, kappa, gamma, P->dnet, P->dir[0], P->dir[1], P->dir[2], P->p, k3b, ntot);
+        else k_dnet<2><<<gd, 256, 0, s>>>(ctrl, kappa, gamma, P->dnet, P->dir[0], P->dir[1], P->dir[2], P->p, k3b, ntot);
         wq_count_launches(1);
         a.dnet = P->dnet;
-        const int tqm = getenv("WQ_COEF_TQM") ? atoi(getenv("WQ_COEF_TQM")) : 16;  // tile height (tuning experiments)
-        auto run = [&](auto TT, auto PPc) {
-            constexpr int TQM = decltype(TT)::value, PP = decltype(PPc)::value;
-            const size_t na = (size_t)9 * (TQM + P->p + 1) * (TQF + P->p + 1), nx = (size_t)TQM * 9 * (TQF + P->p + 1);
+        constexpr int TQM = 16;
+        auto run = [&](auto PPc, auto NUc) {
+            constexpr int PP = decltype(PPc)::value, NNU = decltype(NUc)::value;
+            const size_t ne = 9 + NNU;
+            const size_t na = ne * (TQM + P->p + 1) * (TQF + P->p + 1), nx = (size_t)TQM * ne * (TQF + P->p + 1);
             const size_t sm = (na > nx ? na : nx) * sizeof(double);
-            cudaFuncSetAttribute(k_coefz<TQM, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            wq_smem_attr((const void *)k_coefz<TQM, PP, NNU>, sm);
             dim3 g((unsigned)((a.nq_loc_d + TQF - 1) / TQF), (unsigned)((P->dir[0].nq + TQM - 1) / TQM), (unsigned)P->dir[1].nq);
-            k_coefz<TQM, PP><<<g, TQF * TQM, sm, s>>>(a);
+            k_coefz<TQM, PP, NNU><<<g, TQF * TQM, sm, s>>>(a);
         };
-        auto run_p = [&](auto TT) {
+        auto run_p = [&](auto NUc) {
             switch (P->p) {
-            case 2: run(TT, std::integral_constant<int, 2>{}); break;
-            case 3: run(TT, std::integral_constant<int, 3>{}); break;
-            case 4: run(TT, std::integral_constant<int, 4>{}); break;
-            case 5: run(TT, std::integral_constant<int, 5>{}); break;
-            case 6: run(TT, std::integral_constant<int, 6>{}); break;
-            default: run(TT, std::integral_constant<int, 0>{}); break;
+            case 2: run(std::integral_constant<int, 2>{}, NUc); break;
+            case 3: run(std::integral_constant<int, 3>{}, NUc); break;
+            case 4: run(std::integral_constant<int, 4>{}, NUc); break;
+            case 5: run(std::integral_constant<int, 5>{}, NUc); break;
+            case 6: run(std::integral_constant<int, 6>{}, NUc); break;
+            default: run(std::integral_constant<int, 0>{}, NUc); break;
             }
         };
-        if (tqm == 4) run_p(std::integral_constant<int, 4>{});
-        else if (tqm == 16) run_p(std::integral_constant<int, 16>{});
-        else run_p(std::integral_constant<int, 8>{});
-    } else if (P->d == 3) {
-        size_t sm = (size_t)(9 * K2M * K1M + TQ2 * 9 * K1M) * sizeof(double);
-        static bool set = false;
-        if (!set) { cudaFuncSetAttribute(k_coef<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024); set = true; }
-        dim3 g((unsigned)a.nq_loc_d, (unsigned)((P->dir[0].nq + TQ1 - 1) / TQ1),
-               (unsigned)((P->dir[1].nq + TQ2 - 1) / TQ2));
-        k_coef<3><<<g, NTC, sm, s>>>(a);
+        if (nnu == 0) run_p(std::integral_constant<int, 0>{});
+        else if (nnu == 1) run_p(std::integral_constant<int, 1>{});
+        else run_p(std::integral_constant<int, 2>{});
     } else if (P->d == 2) {
-        size_t sm = (size_t)(TQ2 * 9 * K1M) * sizeof(double);
+        size_t sm = (size_t)(TQ2 * 6 * (TQ1 + P->p + 1)) * sizeof(double);
         dim3 g((unsigned)((P->dir[0].nq + TQ1 - 1) / TQ1), (unsigned)((a.nq_loc_d + TQ2 - 1) / TQ2), 1);
         k_coef<2><<<g, NTC, sm, s>>>(a);
     } else {

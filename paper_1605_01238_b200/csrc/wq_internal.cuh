@@ -39,6 +39,22 @@ struct Flags {   // device-side latched errors
     int det_zero;
 };
 
+// Coefficient field view: component k at grid point (q1, q2, q3) is
+//   base[k * cs + q1 * s1 + q2 * s2 + (q_d - cq_b) * s_d]
+// with the slab direction d counted from the plan's first point cq_b.
+//   d = 3 (z layout): [comp][q_1][q_2][q_3 - cq_b], q_3 fastest, rows of zld (even) doubles,
+//       so a task box of 2 consecutive q_3 x #Q_1 x #Q_2 points is one 4D TMA tile;
+//   d = 2: [comp][q_2 - cq_b][q_1];  d = 1: [comp][q_1 - cq_b].
+// Components: the d(d+1)/2 stiffness components C_lm (upper triangle, row major) first when the
+// plan needs the stiffness matrix, then c (mass) when it needs the mass matrix.
+struct CoefView {
+    const double *base;
+    int64_t cs, s1, s2, s3;
+    __device__ __forceinline__ const double *ptr(int comp, int64_t q1, int64_t q2, int64_t q3l) const {
+        return base + comp * cs + q1 * s1 + q2 * s2 + q3l * s3;
+    }
+};
+
 struct wq_plan_s {
     int d, p, device;
     int need_mass, need_stiff;
@@ -49,52 +65,48 @@ struct wq_plan_s {
     int dir_src[3];                // direction whose rules tables dir[l] shares (identical knots), or l
     // coefficient sub-grid: q_d in [cq_b, cq_e)
     int64_t cq_b, cq_e, coef_points;
-    int64_t c0off;                 // d = 3: point q_1 is stored at column q_1 + 1 (c0off = 1), so that
-                                   // the 2-point boxes [1 + 2k, 2 + 2k] of the row kernels start 16-B
-                                   // aligned for TMA; else 0
-    int64_t cld1;                  // leading dimension along q_1 (d = 3: nq_1 + 1 rounded up to even)
-    int64_t cstride;               // doubles per component = cld1 * (points / nq_1)
     int ncomp_s, ncomp;            // stiffness components, total components
-    int ncomp_std;                 // components held in coef (standard layout)
-    double *coef;                  // [ncomp][cstride], point (q1, q2, q3) at q1 + c0off + cld1 * (q2 + nq2 * (q3 - cq_b))
+    int comp_mass;                 // component index of c
+    double *coef;                  // [ncomp][cs] (layout: CoefView above)
+    int64_t zld, zcs;              // d = 3: row length along q_3 (even), doubles per component
+    int64_t nld1;                  // d <= 2: leading dimension (nq_1)
+    CoefView cview;                // device view of coef
+    int has_coef;                  // a coefficient field has been built (create or wq_build_coef)
     // Gauss-Legendre rule on [-1,1] in double-double: [p+1] (hi, lo) pairs
     double *gl;                    // [2*(p+1)] t, [2*(p+1)] w
     Flags *flags;                  // device
     void *arena;                   // one allocation for all small tables
     size_t arena_bytes;
-    double *ctrl_dev;              // device control-net staging (wq_form_host)
-    double *dnet;                  // z layout: derivative control nets [N_DOF][3][3] (k_dnet)
-    size_t dnet_bytes;
+    double *ctrl_dev;              // device copies of the control net and coefficient nets (create,
+    double *kappa_dev, *gamma_dev; // wq_form_host staging); kappa/gamma null = 1
     size_t ctrl_bytes;
+    double *dnet;                  // d = 3: derivative control nets (+ coefficient nets) of the slab's
+    size_t dnet_bytes;             // control planes k_3 in [k3b, k3e): [k][NE] (k_dnet)
+    int64_t k3b, k3e;
     // form_host staging
-    double *stage_val; int32_t *stage_col; int64_t *stage_rp; size_t stage_bytes;
+    double *stage_val; size_t stage_bytes;
     int64_t workspace_bytes;
-    // d = 3 row lines (i2 + n2 * (i3 - slab_b)) split by the line kernel's applicability:
-    // interior in directions 2 and 3 (#Q = 2p+1, no boundary span) first, then the rest.
-    // Both sorted; device copy in lines_dev (interior at 0, boundary at n_lines_int).
-    std::vector<int32_t> lines_int, lines_bnd;
-    int32_t *lines_dev;
-    // z-line kernel (d = 3 stiffness): the stiffness components live in the z layout
-    // [comp][q_1][q_2][q_3 - cq_b] (q_3 fastest, row length zld even, zero padded) instead of coef;
-    // coef then holds only the mass component.  Lines (i1 + n1 * i2) interior in directions 1 and 2
-    // first, then the rest (device copy zlines_dev).
-    int zlayout;
-    double *coefz;
-    int64_t zld, zcs;              // row length along q_3, doubles per component
-    int comp_mass;                 // component index of c in coef
+    // z-line kernel (d = 3 stiffness, 2 <= p <= 6): lines (i1 + n1 * i2) with uniform rules
+    // possible, other lines interior in directions 1 and 2, lines touching a boundary span (device
+    // copy zlines_dev; zbounds_dev: cost-balanced CTA chunks of the boundary lines)
+    int zline_ok;
     std::vector<int32_t> zlines_uni, zlines_int, zlines_bnd;
     int32_t *zlines_dev;
-    // uniform-mesh interior rules for the z-line kernel (fetched once per plan at the first
-    // assembly): 0 not checked yet, 1 usable (zuni_buf holds them), -1 not uniform
-    int32_t *zbounds_dev;          // cost-balanced chunks of the boundary lines for zbounds_n CTAs
+    int32_t *zbounds_dev;
     int64_t zbounds_n;
+    // uniform-mesh interior rules (reading R16), fetched and verified once at plan creation:
+    // 1 usable (zuni_buf holds them), -1 not uniform
     int zuni_state;
-    double zuni_buf[3 * 13 * 4 + 3 * 2 * 7 * 2];
+    double zuni_buf[3 * 21 * 4 + 3 * 2 * 11 * 2];
+    int kernel_auto[2];            // wq_kernel AUTO runs for [mass, stiffness]
 };
 
 // host helpers
 int64_t wq_host_qlo(int64_t i, int64_t E, int p);  // first grid point of Q_i (Remark 1, reading R1)
 void wq_count_launches(int n);  // adds n to the process-wide launch counter
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `func` on the current device, set once per
+// (function, device) pair
+cudaError_t wq_smem_attr(const void *func, size_t bytes);
 void wq_set_error(const std::string &msg);
 wq_status wq_cuda_status(cudaError_t e, const char *what);
 
@@ -105,7 +117,6 @@ __host__ __device__ inline int64_t wq_ni(int64_t i, int p, int64_t n) { return w
 
 // kernel launchers (defined in the .cu files)
 wq_status launch_rules(wq_plan_s *P, cudaStream_t s);
-wq_status launch_coef(wq_plan_s *P, const double *ctrl, cudaStream_t s);
 wq_status launch_pattern(wq_plan_s *P, int64_t base, int64_t *rp, int32_t *col, int64_t row_lo,
                          int64_t row_hi, cudaStream_t s);
 // value kernels over the slab planes [plane_lo, plane_hi) (relative to the
@@ -115,13 +126,6 @@ wq_status launch_assemble_direct(wq_plan_s *P, int matrix, double *val, int32_t 
 wq_status launch_assemble_tile(wq_plan_s *P, int matrix, double *val, int32_t *col, int64_t plane_lo,
                                int64_t plane_hi, int64_t val_base, cudaStream_t s);
 bool tile_supported(const wq_plan_s *P, int matrix);
-wq_status launch_assemble_ws(wq_plan_s *P, int matrix, double *val, int32_t *col, int64_t plane_lo,
-                             int64_t plane_hi, int64_t val_base, cudaStream_t s);
-bool ws_supported(const wq_plan_s *P, int matrix);
-// line kernel over a list of lines; bnd = lines touching a boundary span in direction 2 or 3
-wq_status launch_assemble_line(wq_plan_s *P, int matrix, bool bnd, const int32_t *lines, int64_t n_lines,
-                               double *val, int32_t *col, int64_t val_base, cudaStream_t s);
-bool line_supported(const wq_plan_s *P, int matrix, bool bnd);
 // z-line kernel (stiffness, d = 3, coefficients in the z layout) over a list of lines (i1 + n1 * i2)
 // and the planes [pl_lo, pl_hi) of the slab
 bool zline_supported_p(int d, int p, const int64_t *n, const int32_t *maxq, int64_t n2l, int64_t nq2l);
@@ -129,7 +133,14 @@ bool zline_supported_p(int d, int p, const int64_t *n, const int32_t *maxq, int6
 // directions 1 and 2, 2 lines touching a boundary span
 wq_status launch_assemble_zline(wq_plan_s *P, int cls, const int32_t *lines, int64_t n_lines, int64_t pl_lo,
                                 int64_t pl_hi, double *val, int32_t *col, int64_t val_base, cudaStream_t s);
-// tile kernel over an explicit list of lines of the plan's slab
-wq_status launch_assemble_tile_list(wq_plan_s *P, int matrix, const int32_t *lines, int64_t n_lines, double *val,
-                                    int32_t *col, int64_t val_base, cudaStream_t s);
-
+// z-line uniform tables + row-type check (reading R16), once per plan after the rules are built
+// (synchronous device -> host copies; called from wq_plan_create only)
+wq_status zline_prepare(wq_plan_s *P);
+// high-degree / mass line kernel (d = 3, any p)
+bool zhp_supported(const wq_plan_s *P, int matrix);
+wq_status launch_assemble_zhp(wq_plan_s *P, int matrix, int64_t pl_lo, int64_t pl_hi, double *val, int32_t *col,
+                              int64_t val_base, cudaStream_t s);
+// standard element-loop Gauss quadrature (SGQ), scatter-added into the CSR values
+wq_status launch_assemble_sgq(wq_plan_s *P, int matrix, const double *ctrl, const double *kappa, const double *gamma,
+                              double *val, int32_t *col, cudaStream_t s);
+wq_status launch_coef(wq_plan_s *P, const double *ctrl, const double *kappa, const double *gamma, cudaStream_t s);

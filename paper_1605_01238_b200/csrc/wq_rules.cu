@@ -432,11 +432,7 @@ wq_status launch_rules(wq_plan_s *P, cudaStream_t s) {
     int qmax = 1;
     for (int l = 0; l < P->d; ++l) qmax = P->dir[l].maxq > qmax ? P->dir[l].maxq : qmax;
     WSmem L(P->p, qmax);
-    static int attr_set = 0;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_weights, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = 1;
-    }
+    wq_smem_attr((const void *)k_weights, L.bytes);
     dim3 g3((unsigned)maxn, nd);
     k_weights<<<g3, 64, L.bytes, s>>>(a, P->gl, P->flags, qmax);
     wq_count_launches(5);

@@ -970,7 +970,7 @@ wq_status launch_zline_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, i
         cuuint64_t strides[3] = {(cuuint64_t)Pl->zld * 8, (cuuint64_t)Pl->zld * nq1 * 8, (cuuint64_t)Pl->zcs * 8};
         cuuint32_t box[4] = {(cuuint32_t)CF::PTS, (cuuint32_t)CF::QX, (cuuint32_t)CF::QX, 6};
         cuuint32_t es[4] = {1, 1, 1, 1};
-        if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void *)Pl->coefz, dims, strides, box, es,
+        if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void *)Pl->coef, dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
             wq_set_error("cuTensorMapEncodeTiled failed for the z-layout coefficient field");
@@ -989,7 +989,7 @@ wq_status launch_zline_p(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, i
         hunroll<CF::NCH>([&](auto CC) {
             constexpr int CH = decltype(CC)::value;
             if (st != WQ_OK) return;
-            cudaFuncSetAttribute(k_zline<P, BND, PU, CU, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            wq_smem_attr((const void *)k_zline<P, BND, PU, CU, CH>, smem);
             k_zline<P, BND, PU, CU, CH><<<(unsigned)grid, CF::NT, smem, s>>>(m, a, un);
             wq_count_launches(1);
             st = wq_cuda_status(cudaGetLastError(), "z-line assembly kernel");

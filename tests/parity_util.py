@@ -28,10 +28,20 @@ def sample_rows(n, d, p, k_random=64, seed=0, extra=()):
     return np.array(sorted(idx), dtype=np.int64)
 
 
-def compare_rows(rows, g_ptr, g_col, g_val, o_ptr, o_col, o_val, kappa, scale, row_offset=0):
+def line_rows(n, pick):
+    """All rows (i1, i2, i3), i3 = 0..n-1, of the lines with i1, i2 in `pick` (3D, n per direction)."""
+    out = [i1 + n * (i2 + n * i3) for i1 in pick for i2 in pick for i3 in range(n)]
+    return np.array(sorted(out), dtype=np.int64)
+
+
+def compare_rows(rows, g_ptr, g_col, g_val, o_ptr, o_col, o_val, kappa, scale, row_offset=0, strict=False):
     """rows: global ids; g_*: CSR of those rows gathered from the GPU (same order).
+    strict=True additionally asserts that every row is in the strict regime
+    (kappa_i <= 1e4, reading R6), which holds for p <= 6.
     Returns dict of statistics; raises AssertionError on index mismatch or
     value tolerance violation."""
+    if strict:
+        assert np.all(np.asarray(kappa) <= KAPPA_STRICT), f"kappa {np.max(kappa):.3g} above the strict regime"
     assert np.array_equal(np.diff(g_ptr), np.diff(o_ptr)), "row lengths differ"
     assert np.array_equal(g_col, o_col), "column indices differ"
     worst = 0.0
@@ -68,3 +78,16 @@ def gather_rows_device(rp, col, val, local_rows):
     gv = val.index_select(0, it).cpu().numpy()
     gc = col.index_select(0, it).cpu().numpy() if col is not None else None
     return ptr, gc, gv
+
+
+_ORC_CACHE = {}
+
+
+def oracle_rows_cached(key, make_oracle, mat, rows):
+    """Oracle rows memoised per (case key, matrix) across the kernels a test is parametrised over."""
+    k = (key, mat, len(rows), int(rows[0]) if len(rows) else -1, int(rows[-1]) if len(rows) else -1)
+    if k not in _ORC_CACHE:
+        if len(_ORC_CACHE) > 16:
+            _ORC_CACHE.clear()
+        _ORC_CACHE[k] = make_oracle().rows(mat, rows)
+    return _ORC_CACHE[k]

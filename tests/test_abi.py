@@ -69,6 +69,39 @@ def test_plan_create_bad_slab_and_d():
     assert e.value.status == wq.WQ_EINVAL
 
 
+def test_bpts_endpoints_rejected():
+    """Reading R1: the endpoints-included boundary points leave #Q_0 = p-1 < #I_0 = p+1, which Eq.
+    numb_nodes forbids; wq_plan_create reports WQ_ESINGULAR naming row 0."""
+    for p in (1, 2, 5):
+        with pytest.raises(wq.WQError) as e:
+            wq.wq_plan_create(p, [uniform_open_knots(p, 6)], bpts=wq.WQ_BPTS_ENDPOINTS)
+        assert e.value.status == wq.WQ_ESINGULAR and "row 0" in e.value.detail
+
+
+def test_coefficients_need_geometry():
+    k = uniform_open_knots(2, 4)
+    with pytest.raises(wq.WQError) as e:
+        wq.wq_plan_create(2, [k], kappa=np.ones(6))
+    assert e.value.status == wq.WQ_EINVAL
+    with pytest.raises(wq.WQError) as e:
+        wq.wq_plan_create(2, [k], bpts=7)
+    assert e.value.status == wq.WQ_EINVAL
+
+
+def test_binding_checks_buffers():
+    """The binding refuses buffers the C side would misuse (ADVICE: dtype, memory space, size)."""
+    import torch
+    with pytest.raises(wq.WQError):
+        wq._ptr(torch.zeros(4, dtype=torch.float32), "f64", 4, "val")
+    with pytest.raises(wq.WQError):
+        wq._ptr(torch.zeros(4, dtype=torch.float64), "f64", 4, "val")  # host tensor, device expected
+    with pytest.raises(wq.WQError):
+        wq._ptr(np.zeros(3), "f64", 4, "h_val", host=True)  # too short
+    with pytest.raises(wq.WQError):
+        wq._ptr(np.zeros((4, 4))[:, 0], "f64", 4, "h_val", host=True)  # not contiguous
+    assert wq._ptr(np.zeros(4), "f64", 4, "h_val", host=True) != 0
+
+
 def test_null_plan_calls():
     lib = wq.load_library()
     assert lib.wq_build_rules(None, None) == wq.WQ_EINVAL

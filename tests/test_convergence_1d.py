@@ -1,0 +1,27 @@
+"""SURVEY f3 / paper Sect. 5.1 (Fig. 1): Galerkin solutions built from the GPU's WQ
+matrices converge at the optimal rates (L_inf, L2 ~ h^{p+1}, H1 ~ h^p), like those built from
+standard Gauss quadrature, for u'' + u = f on [0, pi/6] through the map t = 2 sin(x)."""
+import os
+import sys
+
+import pytest
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "studies"))
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_optimal_rates(p):
+    import convergence_1d as cv
+    rows = cv.study([p], [8, 16, 32, 64])
+    for method in ("wq", "sgq"):
+        last = [r for r in rows if r["method"] == method][-1]
+        assert last["rate_l2"] >= p + 1 - 0.3, (method, last)
+        assert last["rate_h1"] >= p - 0.3, (method, last)
+        assert last["rate_linf"] >= p + 1 - 0.5, (method, last)
+    wq_last = [r for r in rows if r["method"] == "wq"][-1]
+    sgq_last = [r for r in rows if r["method"] == "sgq"][-1]
+    # same order of accuracy: WQ within a small factor of SGQ (Fig. 1: curves nearly coincide)
+    for k in ("l2", "h1", "linf"):
+        assert wq_last[k] <= 10 * sgq_last[k] + 1e-13, (k, wq_last[k], sgq_last[k])

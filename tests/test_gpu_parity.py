@@ -6,17 +6,12 @@ import pytest
 
 import paper_1605_01238_b200 as wq
 from oracle import MASS, STIFFNESS, Oracle
-from parity_util import compare_rows, gather_rows_device, sample_rows
-from wqinputs import baseline_config, control_net, graded_open_knots, uniform_open_knots
+from parity_util import compare_rows, gather_rows_device, line_rows, oracle_rows_cached, sample_rows
+from wqinputs import control_net, graded_open_knots, greville, uniform_open_knots
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [wq.WQ_KERNEL_DIRECT, wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_WS, wq.WQ_KERNEL_LINE, wq.WQ_KERNEL_ZLINE]
-
-
-def layout_for(kernel):
-    """The z-line kernel (and AUTO) use the library's layout choice; the others need the standard one."""
-    return wq.WQ_LAYOUT_AUTO if kernel in (wq.WQ_KERNEL_AUTO, wq.WQ_KERNEL_ZLINE) else wq.WQ_LAYOUT_STANDARD
+KERNELS = [wq.WQ_KERNEL_AUTO, wq.WQ_KERNEL_DIRECT, wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_ZLINE, wq.WQ_KERNEL_ZHP]
 
 
 def _torch():
@@ -31,18 +26,25 @@ def make_case(d, p, E, geometry="grid", amp=0.1, knots="uniform", seed=0):
     return ks, ctrl
 
 
-def run_full(ks, ctrl, p, matrix, kernel=wq.WQ_KERNEL_AUTO, slab=(0, -1), fused_col=True):
+class Unavailable(Exception):
+    pass
+
+
+def run_full(ks, ctrl, p, matrix, kernel=wq.WQ_KERNEL_AUTO, slab=(0, -1), fused_col=True, kappa=None, gamma=None,
+             need=(True, True)):
+    """Whole device path through the C-ABI for one matrix; raises Unavailable when the requested
+    kernel does not serve (matrix, d, p) (a loud WQ_EINVAL from the library, never a fallback)."""
     torch = _torch()
-    plan = wq.Plan(p, ks, slab=slab, need_mass=True, need_stiffness=True, coef_layout=layout_for(kernel))
-    if kernel in (wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_WS, wq.WQ_KERNEL_LINE, wq.WQ_KERNEL_ZLINE) and \
-            not _kernel_ok(plan, matrix, kernel):
-        plan.close()
-        pytest.skip(f"kernel {kernel} not available for this (d, p)")
-    d_ctrl = torch.from_numpy(ctrl).cuda()
+    plan = wq.Plan(p, ks, ctrl=ctrl, kappa=kappa, gamma=gamma, slab=slab, need_mass=need[0], need_stiffness=need[1])
     rp, col, val = plan.alloc_csr()
-    plan.setup(d_ctrl)
     wq.wq_pattern(plan.h, 0, rp, None if fused_col else col)
-    wq.wq_assemble(plan.h, matrix, val, col if fused_col else None, kernel=kernel)
+    try:
+        wq.wq_assemble(plan.h, matrix, val, col if fused_col else None, kernel=kernel)
+    except wq.WQError as e:
+        plan.close()
+        if e.status == wq.WQ_EINVAL and kernel != wq.WQ_KERNEL_AUTO:
+            raise Unavailable(str(e))
+        raise
     wq.wq_check(plan.h)
     torch.cuda.synchronize()
     info = plan.info
@@ -50,16 +52,30 @@ def run_full(ks, ctrl, p, matrix, kernel=wq.WQ_KERNEL_AUTO, slab=(0, -1), fused_
     return rp, col, val, info
 
 
-def _kernel_ok(plan, matrix, kernel):
-    torch = _torch()
-    try:
-        v = torch.empty(plan.info["nnz_local"], dtype=torch.float64, device="cuda")
-        plan.setup(torch.zeros(plan.info["n_dof_total"] * plan.d, dtype=torch.float64, device="cuda") + 1)
-        wq.wq_assemble(plan.h, matrix, v, None, kernel=kernel)
-        torch.cuda.synchronize()
-        return True
-    except wq.WQError:
-        return False
+def check_every_row(o, mat, rp, col, val, key=None, strict=False):
+    orp, ocol = o.pattern()
+    assert np.array_equal(rp.cpu().numpy(), orp)
+    assert np.array_equal(col.cpu().numpy(), ocol)
+    rows = np.arange(o.ndof)
+    if key is None:
+        ptr, oc, ov, kappa, scale = o.rows(mat, rows)
+    else:
+        ptr, oc, ov, kappa, scale = oracle_rows_cached(key, lambda: o, mat, rows)
+    return compare_rows(rows, ptr, col.cpu().numpy(), val.cpu().numpy(), ptr, oc, ov, kappa, scale, strict=strict)
+
+
+def run_matrices(ks, ctrl, p, kernel, mats, check):
+    """Run each matrix with `kernel`; skip the test only if the kernel serves none of them."""
+    ran = 0
+    for mat in mats:
+        try:
+            rp, col, val, info = run_full(ks, ctrl, p, mat, kernel)
+        except Unavailable:
+            continue
+        check(mat, rp, col, val, info)
+        ran += 1
+    if ran == 0:
+        pytest.skip(f"kernel {kernel} serves none of {mats} for this (d, p)")
 
 
 # ------------------------------------------------------------------ rules
@@ -74,8 +90,6 @@ def test_rules_match_oracle(p, E, knots):
     o = Oracle(p, [k])
     D = o.direction(0)
     plan = wq.Plan(p, [k], need_mass=True, need_stiffness=False)
-    wq.wq_build_rules(plan.h)
-    wq.wq_check(plan.h)
     R = wq.wq_export_rules(plan.h, 0, p)
     plan.close()
     assert np.array_equal(R["points"], D["points"])
@@ -96,32 +110,37 @@ def test_rules_match_oracle(p, E, knots):
             assert err <= 8e-16 * sc, (i, f, err / sc)
 
 
-def test_rules_singular_flag_not_raised_on_valid_input():
+def test_rules_valid_on_every_degree():
+    """wq_plan_create validates the exactness systems (WQ_ESINGULAR) of every row for p = 1..10."""
     for p in range(1, 11):
         k = graded_open_knots(p, 2 * p + 3)
         plan = wq.Plan(p, [k, k], need_mass=True, need_stiffness=False)
-        wq.wq_build_rules(plan.h)
-        wq.wq_check(plan.h)
         plan.close()
 
 
 # ------------------------------------------------------------ coefficients
+def _coef_ref(o, qb, nq_loc, d):
+    """Oracle coefficient field on the plan's sub-grid (all q_1.., q_d in [qb, qb + nq_loc))."""
+    ref, det, st = o.coef_box([0] * (d - 1) + [qb], list(o.nq[:-1]) + [qb + nq_loc])
+    assert st == 0
+    return ref
+
+
 @pytest.mark.parametrize("d,p,E,geom", [(1, 3, 7, "grid"), (2, 2, 5, "annulus"), (2, 5, 6, "grid"),
-                                        (3, 3, 4, "grid"), (3, 4, 5, "annulus"), (3, 10, 2, "grid")])
+                                        (3, 3, 4, "grid"), (3, 4, 5, "annulus"), (3, 10, 2, "grid"),
+                                        (3, 1, 5, "grid"), (3, 7, 9, "annulus"), (3, 4, 14, "grid")])
 def test_coef_matches_oracle(d, p, E, geom):
-    torch = _torch()
+    """Step 5 (Alg. 1 lines 12/15): every component of c and C on the plan's sub-grid within 1e-13
+    of the long-double oracle; d = 3 plans hold the z layout (k_dnet + k_coefz), incl. the
+    uniform-line configuration E >= 4p+2 and p = 1, 7, 10 (generic-degree instantiation)."""
     ks, ctrl = make_case(d, p, E, geom, 0.05)
     o = Oracle(p, ks, ctrl)
-    plan = wq.Plan(p, ks, need_mass=True, need_stiffness=True)
-    plan.setup(torch.from_numpy(ctrl).cuda())
-    wq.wq_check(plan.h)
+    plan = wq.Plan(p, ks, ctrl=ctrl, need_mass=True, need_stiffness=True)
     G, qb = wq.wq_export_coef(plan.h)
     plan.close()
-    # the plan holds q_d in [qb, qb + len) (points inside some Q_i); others in full
     nq_loc = G.shape[1] // int(np.prod(o.nq[:-1]))
-    ref, det, st = o.coef_box([0] * (d - 1) + [qb], list(o.nq[:-1]) + [qb + nq_loc])
-    assert st == 0 and qb == 1 and nq_loc == o.nq[-1] - 2
-    # GPU layout: comps C_00, C_01, .., C_{d-1,d-1} (upper), then c
+    assert qb == 1 and nq_loc == o.nq[-1] - 2
+    ref = _coef_ref(o, qb, nq_loc, d)
     comps = [(l, m) for l in range(d) for m in range(l, d)]
     for k, (l, m) in enumerate(comps):
         r = ref[:, 1 + l * d + m]
@@ -129,17 +148,50 @@ def test_coef_matches_oracle(d, p, E, geom):
     np.testing.assert_allclose(G[len(comps)], ref[:, 0], rtol=1e-13)
 
 
-def test_folded_geometry_rejected():
+def test_coef_C2_zlayout_every_point():
+    """BASELINE configs[1] (C2) coefficient field, every point, z layout (the z-line plan)."""
+    from wqinputs import baseline_config
+    cfg = baseline_config("C2")
+    ks, ctrl = cfg.knots(), cfg.ctrl()
+    o = Oracle(cfg.p, ks, ctrl)
+    plan = wq.Plan(cfg.p, ks, ctrl=ctrl, need_mass=True, need_stiffness=True)
+    assert plan.info["kernel"][1] == wq.WQ_KERNEL_ZLINE
+    G, qb = wq.wq_export_coef(plan.h)
+    plan.close()
+    nq_loc = G.shape[1] // int(np.prod(o.nq[:-1]))
+    ref = _coef_ref(o, qb, nq_loc, 3)
+    for k, (l, m) in enumerate([(l, m) for l in range(3) for m in range(l, 3)]):
+        r = ref[:, 1 + 3 * l + m]
+        np.testing.assert_allclose(G[k], r, rtol=0, atol=1e-13 * np.abs(r).max())
+    np.testing.assert_allclose(G[6], ref[:, 0], rtol=1e-13)
+
+
+def test_folded_geometry_rejected_at_create():
+    """Reading R7: det J changing sign on the grid -> wq_plan_create returns WQ_EGEOMETRY; the same
+    control net passed to the stream-ordered wq_build_coef is reported by wq_check."""
     torch = _torch()
     p = 2
     ks = [uniform_open_knots(p, 4)] * 2
     P = control_net("grid", p, ks, 0.0)
     P[7, 0] += 0.9
+    with pytest.raises(wq.WQError) as e:
+        wq.Plan(p, ks, ctrl=P)
+    assert e.value.status == wq.WQ_EGEOMETRY
     plan = wq.Plan(p, ks)
     plan.setup(torch.from_numpy(P).cuda())
     with pytest.raises(wq.WQError) as e:
         wq.wq_check(plan.h)
     assert e.value.status == wq.WQ_EGEOMETRY
+    plan.close()
+
+
+def test_assemble_without_geometry_refused():
+    ks = [uniform_open_knots(2, 4)] * 3
+    plan = wq.Plan(2, ks)
+    rp, col, val = plan.alloc_csr()
+    with pytest.raises(wq.WQError) as e:
+        wq.wq_assemble(plan.h, STIFFNESS, val, col)
+    assert e.value.status == wq.WQ_EINVAL
     plan.close()
 
 
@@ -151,82 +203,145 @@ SMALL = [(1, 1, 1), (1, 2, 6), (1, 5, 3), (2, 1, 3), (2, 2, 2), (2, 3, 5), (2, 4
 @pytest.mark.parametrize("d,p,E", SMALL)
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_full_parity_small(d, p, E, kernel):
-    """Every row of small problems, both matrices, incl. n_EL = 1 and 2."""
+    """Every row of small problems, both matrices, incl. n_EL = 1 and 2; each matrix runs if the
+    kernel serves it (a kernel refusing one matrix does not skip the other)."""
     ks, ctrl = make_case(d, p, E, "grid", 0.08, knots="graded" if (p + E) % 2 else "uniform", seed=d + p)
     o = Oracle(p, ks, ctrl)
-    orp, ocol = o.pattern()
-    for mat in (MASS, STIFFNESS):
-        rp, col, val, info = run_full(ks, ctrl, p, mat, kernel)
-        assert np.array_equal(rp.cpu().numpy(), orp)
-        assert np.array_equal(col.cpu().numpy(), ocol)
-        rows = np.arange(o.ndof)
-        ptr, oc, ov, kappa, scale = o.rows(mat, rows)
-        compare_rows(rows, ptr, col.cpu().numpy(), val.cpu().numpy(), ptr, oc, ov, kappa, scale)
+    key = ("small", d, p, E)
+    run_matrices(ks, ctrl, p, kernel, (MASS, STIFFNESS),
+                 lambda mat, rp, col, val, info: check_every_row(o, mat, rp, col, val, key))
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_C1_full(kernel):
     """BASELINE configs[0]: 2D p=3, 16x16 elements, S and M, every row."""
+    from wqinputs import baseline_config
     cfg = baseline_config("C1")
     ks, ctrl = cfg.knots(), cfg.ctrl()
     o = Oracle(cfg.p, ks, ctrl)
-    orp, ocol = o.pattern()
-    for mat in (MASS, STIFFNESS):
-        rp, col, val, info = run_full(ks, ctrl, cfg.p, mat, kernel)
-        assert info["nnz_local"] == cfg.exact_nnz() == orp[-1]
-        assert np.array_equal(rp.cpu().numpy(), orp) and np.array_equal(col.cpu().numpy(), ocol)
-        rows = np.arange(o.ndof)
-        ptr, oc, ov, kappa, scale = o.rows(mat, rows)
-        compare_rows(rows, ptr, col.cpu().numpy(), val.cpu().numpy(), ptr, oc, ov, kappa, scale)
 
-
-@pytest.mark.parametrize("name,p,k_random", [("C2", None, 96), ("C3", None, 24), ("C4", 2, 48), ("C4", 4, 32),
-                                             ("C4", 6, 12), ("C4", 8, 4), ("C4", 10, 2)])
-@pytest.mark.parametrize("kernel", KERNELS)
-def test_baseline_sampled(name, p, k_random, kernel):
-    """BASELINE configs at full size in the bench launch configuration:
-    sampled rows (all boundary situations + seeded random rows) vs the oracle,
-    plus pattern invariants on the whole matrix (nnz, row lengths)."""
-    torch = _torch()
-    cfg = baseline_config(name, p)
-    if kernel == wq.WQ_KERNEL_DIRECT and cfg.p >= 8:
-        pytest.skip("direct kernel is O(#Q^3) per entry: too slow at p >= 8 full size")
-    ks, ctrl = cfg.knots(), cfg.ctrl()
-    mats = (STIFFNESS, MASS) if "mass" in cfg.matrices and kernel != wq.WQ_KERNEL_ZLINE else (STIFFNESS,)
-    n = cfg.n_el + cfg.p
-    rows = sample_rows(n, 3, cfg.p, k_random=k_random, seed=1)
-    if cfg.p >= 8:
-        rows = rows[:: max(1, len(rows) // 24)]
-    o = Oracle(cfg.p, ks, ctrl)
-    for mat in mats:
-        rp, col, val, info = run_full(ks, ctrl, cfg.p, mat, kernel)
+    def check(mat, rp, col, val, info):
         assert info["nnz_local"] == cfg.exact_nnz()
-        assert int(rp[-1]) == cfg.exact_nnz()
+        check_every_row(o, mat, rp, col, val, "C1")
+    run_matrices(ks, ctrl, cfg.p, kernel, (MASS, STIFFNESS), check)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+@pytest.mark.parametrize("kernel", [wq.WQ_KERNEL_AUTO, wq.WQ_KERNEL_ZHP])
+def test_uniform_lines_every_row(p, kernel):
+    """Uniform open knots with E = 4p+2 elements: the z-line plan has uniform lines (R16 tables in
+    registers / kernel parameters: PU and CU classes), interior and boundary lines, every row type
+    in every direction -- every row of the stiffness (and, for the kernels that serve it, the
+    mass) matrix against the oracle."""
+    E = 4 * p + 2
+    ks, ctrl = make_case(3, p, E, "annulus", 0.05, seed=p)
+    o = Oracle(p, ks, ctrl)
+    plan = wq.Plan(p, ks, ctrl=ctrl)
+    if kernel == wq.WQ_KERNEL_AUTO:
+        assert plan.info["kernel"][1] == wq.WQ_KERNEL_ZLINE and plan.info["uniform_rules"] == 1
+    plan.close()
+    run_matrices(ks, ctrl, p, kernel, (STIFFNESS, MASS),
+                 lambda mat, rp, col, val, info: check_every_row(o, mat, rp, col, val, ("uni", p), strict=True))
+
+
+@pytest.mark.parametrize("p", [5, 6])
+@pytest.mark.parametrize("kernel", [wq.WQ_KERNEL_AUTO, wq.WQ_KERNEL_ZHP])
+def test_uniform_lines_all_classes(p, kernel):
+    """p = 5, 6 (column-chunked z-line launches) on uniform knots, E = 4p+2: every row of the lines
+    (i1, i2) with i1, i2 over one index of every row type (boundary types 0, 1, p, first interior
+    p+1, first uniform 2p, the middle, and their mirrors) -- uniform, interior and boundary line
+    classes, all i3 -- against the oracle."""
+    torch = _torch()
+    E = 4 * p + 2
+    ks, ctrl = make_case(3, p, E, "annulus", 0.05, seed=p)
+    n = E + p
+    pick = sorted({0, 1, p, p + 1, 2 * p, n // 2, n - 1 - 2 * p, n - 2 - p, n - 1})
+    rows = line_rows(n, pick)
+    o = Oracle(p, ks, ctrl)
+    for mat in (STIFFNESS,):
+        try:
+            rp, col, val, info = run_full(ks, ctrl, p, mat, kernel)
+        except Unavailable:
+            pytest.skip("kernel unavailable")
         ptr, oc, ov, kappa, scale = o.rows(mat, rows)
         gptr, gc, gv = gather_rows_device(rp, col, val, rows)
-        st = compare_rows(rows, gptr, gc, gv, ptr, oc, ov, kappa, scale)
-        print(name, p, mat, st)
+        compare_rows(rows, gptr, gc, gv, ptr, oc, ov, kappa, scale, strict=True)
+        orp, ocol = o.pattern()
+        assert np.array_equal(rp.cpu().numpy(), orp) and np.array_equal(col.cpu().numpy(), ocol)
         del rp, col, val
         torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("p,E", [(2, 7), (3, 8), (4, 9), (6, 8)])
+@pytest.mark.parametrize("kernel", [wq.WQ_KERNEL_AUTO, wq.WQ_KERNEL_ZHP])
+def test_graded_knots_every_row(p, E, kernel):
+    """Non-uniform (graded) knots: every row's own rules (no uniform tables, reading R16
+    inapplicable); every row of the stiffness matrix against the oracle."""
+    ks, ctrl = make_case(3, p, E, "grid", 0.08, knots="graded", seed=3)
+    o = Oracle(p, ks, ctrl)
+    run_matrices(ks, ctrl, p, kernel, (STIFFNESS, MASS),
+                 lambda mat, rp, col, val, info: check_every_row(o, mat, rp, col, val, ("graded", p, E)))
+
+
+# ------------------------------------------------- scalar coefficients (R17)
+@pytest.mark.parametrize("d,p,E", [(1, 3, 9), (2, 3, 6), (3, 2, 6), (3, 4, 5), (3, 7, 2)])
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_coefficients_every_row(d, p, E, kernel):
+    """-div(kappa grad u) + gamma u with spline coefficient nets kappa, gamma (P:435, P:508-509;
+    reading R17): c = gamma |det J| and C = kappa |det J| J^-1 J^-T on the GPU against the oracle,
+    every row, both matrices."""
+    ks, ctrl = make_case(d, p, E, "grid", 0.08, seed=11)
+    rng = np.random.default_rng(7)
+    n = int(np.prod([k.size - p - 1 for k in ks]))
+    kap = 1.0 + 0.5 * rng.uniform(size=n)
+    gam = 0.5 + rng.uniform(size=n)
+    o = Oracle(p, ks, ctrl, kappa=kap, gamma=gam)
+    ran = 0
+    for mat in (STIFFNESS, MASS):
+        try:
+            rp, col, val, info = run_full(ks, ctrl, p, mat, kernel, kappa=kap, gamma=gam)
+        except Unavailable:
+            continue
+        check_every_row(o, mat, rp, col, val, ("coef", d, p, E))
+        ran += 1
+    if not ran:
+        pytest.skip("kernel unavailable")
+
+
+def test_coefficient_example_printed_gpu():
+    """The paper's worked example P:391-402 through the GPU mass path: p = 3, h = 2, identity map,
+    gamma(zeta) = zeta: m~_{8,9} and m~_{9,8} equal the printed sums (2.3647 / 2.3615)."""
+    import json
+    import os
+    from fractions import Fraction as Fr
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))["asymmetry_example"]
+    k = np.array([-10.0] * 4 + [float(x) for x in range(-8, 20, 2)] + [20.0] * 4)
+    gv = greville(3, k)
+    rp, col, val, info = run_full([k], gv.reshape(-1, 1), 3, MASS, gamma=gv, need=(True, False))
+    rp, col, val = rp.cpu().numpy(), col.cpu().numpy(), val.cpu().numpy()
+    m89 = val[rp[8]:rp[9]][list(col[rp[8]:rp[9]]).index(9)]
+    m98 = val[rp[9]:rp[10]][list(col[rp[9]:rp[10]]).index(8)]
+    assert abs(m89 - float(sum(Fr(*a) * b * Fr(*c) for a, b, c in g["Qi_cBj_terms"]))) < 1e-13
+    assert abs(m98 - float(sum(Fr(*a) * b * Fr(*c) for a, b, c in g["Qj_cBi_terms"]))) < 1e-13
+
+
 # ---------------------------------------------------------- slabs / e2e
-@pytest.mark.parametrize("d,p,E,nslab", [(2, 3, 8, 3), (3, 2, 5, 2), (3, 4, 6, 4)])
+@pytest.mark.parametrize("d,p,E,nslab", [(2, 3, 8, 3), (3, 2, 5, 2), (3, 4, 6, 4), (3, 4, 18, 3), (3, 8, 5, 2)])
 def test_slabs_concatenate_bit_exact(d, p, E, nslab):
     """Multi-GPU decomposition, run sequentially on one
     GPU: per-slab CSR blocks with nnz_base from an exclusive scan concatenate
     to the single-plan CSR, bit for bit (indices and values)."""
     torch = _torch()
+    from paper_1605_01238_b200.dist import slab_cuts
     ks, ctrl = make_case(d, p, E)
     rp0, col0, val0, info0 = run_full(ks, ctrl, p, STIFFNESS)
-    n_d = E + p
-    cuts = np.linspace(0, n_d, nslab + 1).astype(int)
+    cuts = slab_cuts(E + p, p, nslab)
     base = 0
     rps, cols, vals = [], [], []
     for s in range(nslab):
-        plan = wq.Plan(p, ks, slab=(int(cuts[s]), int(cuts[s + 1])), need_mass=False, need_stiffness=True)
-        d_ctrl = torch.from_numpy(ctrl).cuda()
-        rp, col, val = plan.form(STIFFNESS, d_ctrl, nnz_base=base)
+        plan = wq.Plan(p, ks, ctrl=ctrl, slab=(cuts[s], cuts[s + 1]), need_mass=False, need_stiffness=True)
+        assert plan.info["kernel"][1] == info0["kernel"][1]
+        rp, col, val = plan.form(STIFFNESS, nnz_base=base)
         base += plan.info["nnz_local"]
         rps.append(rp[:-1].cpu().numpy())
         cols.append(col.cpu().numpy())
@@ -240,71 +355,32 @@ def test_slabs_concatenate_bit_exact(d, p, E, nslab):
 
 
 def test_form_host_equals_device():
-    """wq_form_host (host buffers, chunked, copies overlapped) == device path."""
+    """wq_form_host (host buffers, chunked, copies overlapped) == device path, incl. coefficients."""
     torch = _torch()
     ks, ctrl = make_case(3, 3, 10)
+    n = ctrl.shape[0]
+    kap = np.linspace(1.0, 2.0, n)
     for mat in (MASS, STIFFNESS):
-        rp0, col0, val0, info = run_full(ks, ctrl, 3, mat)
-        plan = wq.Plan(3, ks)
-        n, nnz = plan.info["n_rows_local"], plan.info["nnz_local"]
-        hrp = torch.empty(n + 1, dtype=torch.int64).pin_memory()
-        hcol = torch.empty(nnz, dtype=torch.int32).pin_memory()
-        hval = torch.empty(nnz, dtype=torch.float64).pin_memory()
-        hctrl = torch.from_numpy(ctrl).pin_memory()
-        wq.wq_form_host(plan.h, mat, hctrl, 0, hrp, hcol, hval)
-        plan.close()
-        assert np.array_equal(hrp.numpy(), rp0.cpu().numpy())
-        assert np.array_equal(hcol.numpy(), col0.cpu().numpy())
-        assert np.array_equal(hval.numpy(), val0.cpu().numpy())
-
-
-@pytest.mark.parametrize("p,E", [(2, 11), (3, 10), (4, 9)])
-def test_kernels_agree(p, E):
-    """Direct, tile and warp-specialised kernels agree to roundoff on mid-size
-    3D cases; columns bit-exact."""
-    ks, ctrl = make_case(3, p, E, "annulus", 0.05)
-    for mat in (MASS, STIFFNESS):
-        _, c1, v1, _ = run_full(ks, ctrl, p, mat, wq.WQ_KERNEL_DIRECT)
-        a = v1.cpu().numpy()
-        for k in (wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_WS, wq.WQ_KERNEL_LINE, wq.WQ_KERNEL_ZLINE):
-            if k in (wq.WQ_KERNEL_LINE, wq.WQ_KERNEL_ZLINE) and mat == MASS:
-                continue
-            _, c2, v2, _ = run_full(ks, ctrl, p, mat, k)
-            assert np.array_equal(c1.cpu().numpy(), c2.cpu().numpy())
-            b = v2.cpu().numpy()
-            assert np.abs(a - b).max() <= 1e-12 * np.abs(a).max()
-
-
-@pytest.mark.parametrize("p", [2, 3, 4])
-def test_ws_sub_slab_launch(p):
-    """Warp-specialised kernel on slab sub-ranges (plane_lo > 0, few items per
-    CTA, grid smaller than the SM count) equals the whole-slab launch."""
-    torch = _torch()
-    ks, ctrl = make_case(3, p, 7, "grid", 0.1)
-    rp0, col0, val0, info = run_full(ks, ctrl, p, STIFFNESS, wq.WQ_KERNEL_WS)
-    n_d = 7 + p
-    plan = wq.Plan(p, ks, slab=(2, n_d - 1), need_mass=False, need_stiffness=True,
-                   coef_layout=wq.WQ_LAYOUT_STANDARD)
-    d_ctrl = torch.from_numpy(ctrl).cuda()
-    rp, col, val = plan.alloc_csr()
-    plan.setup(d_ctrl)
-    base = int(rp0[plan.info["row_begin"]])
-    wq.wq_pattern(plan.h, base, rp, None)
-    wq.wq_assemble(plan.h, STIFFNESS, val, col, kernel=wq.WQ_KERNEL_WS)
-    torch.cuda.synchronize()
-    r0 = plan.info["row_begin"]
-    n = plan.info["n_rows_local"]
-    plan.close()
-    lo, hi = int(rp0[r0]), int(rp0[r0 + n])
-    assert np.array_equal(rp.cpu().numpy(), rp0[r0:r0 + n + 1].cpu().numpy())
-    assert np.array_equal(col.cpu().numpy(), col0[lo:hi].cpu().numpy())
-    assert np.array_equal(val.cpu().numpy(), val0[lo:hi].cpu().numpy())
+        for kk in (None, kap):
+            rp0, col0, val0, info = run_full(ks, ctrl, 3, mat, kappa=kk, gamma=kk)
+            plan = wq.Plan(3, ks)
+            nr, nnz = plan.info["n_rows_local"], plan.info["nnz_local"]
+            hrp = torch.empty(nr + 1, dtype=torch.int64).pin_memory()
+            hcol = torch.empty(nnz, dtype=torch.int32).pin_memory()
+            hval = torch.empty(nnz, dtype=torch.float64).pin_memory()
+            hctrl = torch.from_numpy(ctrl).pin_memory()
+            hk = None if kk is None else torch.from_numpy(kk).pin_memory()
+            wq.wq_form_host(plan.h, mat, hctrl, 0, hrp, hcol, hval, h_kappa=hk, h_gamma=hk)
+            plan.close()
+            assert np.array_equal(hrp.numpy(), rp0.cpu().numpy())
+            assert np.array_equal(hcol.numpy(), col0.cpu().numpy())
+            assert np.array_equal(hval.numpy(), val0.cpu().numpy())
 
 
 @pytest.mark.parametrize("p,E,chunk", [(2, 9, 4000), (3, 8, 9000), (4, 7, 20000)])
 def test_zline_plane_ranges(p, E, chunk, monkeypatch):
     """z-line kernel over plane sub-ranges (wq_form_host chunks: odd first task
-    point, few rows per line) and over slabs equals the whole-plan launch bit for bit."""
+    point, few rows per line) equals the whole-plan launch bit for bit."""
     torch = _torch()
     ks, ctrl = make_case(3, p, E, "annulus", 0.05)
     rp0, col0, val0, info = run_full(ks, ctrl, p, STIFFNESS, wq.WQ_KERNEL_ZLINE)
@@ -321,58 +397,59 @@ def test_zline_plane_ranges(p, E, chunk, monkeypatch):
     assert np.array_equal(hval.numpy(), val0.cpu().numpy())
 
 
-def test_zline_layout_guard():
-    """A plan holding the stiffness field in the z layout refuses the kernels
-    that read the standard layout (loud error, no silent fallback)."""
+def test_every_kernel_reads_every_plan():
+    """The coefficient layout is the library's business: on a z-line plan (z layout) the direct and
+    tile kernels still assemble the stiffness matrix, within the oracle tolerance (per row)."""
+    p, E = 3, 6
+    ks, ctrl = make_case(3, p, E)
+    o = Oracle(p, ks, ctrl)
+    for k in (wq.WQ_KERNEL_DIRECT, wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_ZLINE):
+        rp, col, val, info = run_full(ks, ctrl, p, STIFFNESS, k)
+        assert info["kernel"][1] == wq.WQ_KERNEL_ZLINE
+        check_every_row(o, STIFFNESS, rp, col, val)
+
+
+@pytest.mark.parametrize("p,E", [(3, 14), (4, 18)])
+def test_zline_repeatable_bit_exact(p, E):
+    """Stress check of the producer/consumer hand-offs (ADVICE: ring slots are returned with relaxed
+    mbarrier arrives): 20 back-to-back assemblies of the same plan give bit-identical values."""
     torch = _torch()
-    ks, ctrl = make_case(3, 3, 6)
-    plan = wq.Plan(3, ks)
-    plan.setup(torch.from_numpy(ctrl).cuda())
-    v = torch.empty(plan.info["nnz_local"], dtype=torch.float64, device="cuda")
-    for k in (wq.WQ_KERNEL_DIRECT, wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_WS, wq.WQ_KERNEL_LINE):
-        with pytest.raises(wq.WQError):
-            wq.wq_assemble(plan.h, STIFFNESS, v, None, kernel=k)
-    wq.wq_assemble(plan.h, MASS, v, None, kernel=wq.WQ_KERNEL_TILE)
+    ks, ctrl = make_case(3, p, E, "annulus", 0.05)
+    plan = wq.Plan(p, ks, ctrl=ctrl, need_mass=False)
+    rp, col, val = plan.alloc_csr()
+    wq.wq_assemble(plan.h, STIFFNESS, val, col)
+    ref = val.clone()
+    for _ in range(20):
+        val.zero_()
+        wq.wq_assemble(plan.h, STIFFNESS, val, col)
+        torch.cuda.synchronize()
+        assert torch.equal(val, ref)
     plan.close()
 
 
-@pytest.mark.parametrize("p,E,knots", [(5, 8, "uniform"), (6, 9, "uniform"), (6, 14, "uniform")])
-def test_zline_column_chunks(p, E, knots):
-    """p = 5, 6: the z-line kernel in t1 column chunks (one launch per chunk, two stage-A fibre
-    passes, fewer producer warps on boundary lines) against the oracle on sampled rows of every
-    boundary situation, and bit-exact across the plan-layout-independent pattern."""
-    ks, ctrl = make_case(3, p, E, "annulus", 0.05, knots=knots, seed=p)
-    rp, col, val, info = run_full(ks, ctrl, p, STIFFNESS, wq.WQ_KERNEL_ZLINE)
-    o = Oracle(p, ks, ctrl)
-    n = E + p
-    rows = sample_rows(n, 3, p, k_random=24, seed=2)
-    ptr, oc, ov, kappa, scale = o.rows(STIFFNESS, rows)
-    gptr, gc, gv = gather_rows_device(rp, col, val, rows)
-    compare_rows(rows, gptr, gc, gv, ptr, oc, ov, kappa, scale)
-
-
-@pytest.mark.parametrize("p,E", [(2, 7), (3, 8), (4, 9), (6, 10)])
-def test_zline_graded_knots(p, E):
-    """Non-uniform (graded) knots: the z-line kernel runs with every row's own rules (no uniform
-    tables, reading R16 inapplicable); every row against the oracle."""
-    ks, ctrl = make_case(3, p, E, "grid", 0.08, knots="graded", seed=3)
-    rp, col, val, info = run_full(ks, ctrl, p, STIFFNESS, wq.WQ_KERNEL_ZLINE)
-    o = Oracle(p, ks, ctrl)
-    orp, ocol = o.pattern()
-    assert np.array_equal(rp.cpu().numpy(), orp) and np.array_equal(col.cpu().numpy(), ocol)
-    rows = np.arange(o.ndof)
-    ptr, oc, ov, kappa, scale = o.rows(STIFFNESS, rows)
-    compare_rows(rows, ptr, col.cpu().numpy(), val.cpu().numpy(), ptr, oc, ov, kappa, scale)
-
-
-def test_zline_uniform_rules_switch(monkeypatch):
-    """Reading R16: the uniform-rules tables change values only at the FP64 rounding level of the
-    knots (well inside the R6 tolerance); indices identical."""
-    p, E = 4, 14
-    ks, ctrl = make_case(3, p, E, "annulus", 0.05)
-    _, c1, v1, _ = run_full(ks, ctrl, p, STIFFNESS, wq.WQ_KERNEL_ZLINE)
-    monkeypatch.setenv("WQ_ZLINE_NO_UNIFORM", "1")
-    _, c2, v2, _ = run_full(ks, ctrl, p, STIFFNESS, wq.WQ_KERNEL_ZLINE)
-    assert np.array_equal(c1.cpu().numpy(), c2.cpu().numpy())
-    a, b = v1.cpu().numpy(), v2.cpu().numpy()
-    assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
+def test_stream_ordered_calls_capture_in_cuda_graph():
+    """wq_build_rules / wq_build_coef / wq_pattern / wq_assemble never synchronise the host (wq.h):
+    they are captured into a CUDA graph (a synchronising call would invalidate the capture), and
+    the replayed graph reproduces the eager result bit for bit."""
+    torch = _torch()
+    p, E = 4, 10
+    ks, ctrl = make_case(3, p, E)
+    plan = wq.Plan(p, ks, ctrl=ctrl)
+    d_ctrl = torch.from_numpy(ctrl).cuda()
+    rp, col, val = plan.alloc_csr()
+    rp2, col2, val2 = plan.alloc_csr()
+    wq.wq_pattern(plan.h, 0, rp)
+    wq.wq_assemble(plan.h, STIFFNESS, val, col)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        st = torch.cuda.current_stream()
+        wq.wq_build_rules(plan.h, st)
+        wq.wq_build_coef(plan.h, d_ctrl, stream=st)
+        wq.wq_pattern(plan.h, 0, rp2, None, st)
+        wq.wq_assemble(plan.h, STIFFNESS, val2, col2, st)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(rp, rp2) and torch.equal(col, col2) and torch.equal(val, val2)
+    plan.close()

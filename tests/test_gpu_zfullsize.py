@@ -1,0 +1,129 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (one plan, AUTO kernel; C5 as the 8 slabs of the multi-GPU split run one
+after the other on one GPU):
+  - index arrays (row_ptr, col) compared IN FULL, streamed in plane chunks
+    against the oracle's pattern generator (orc_pattern_rows, by definition of
+    I_i), bit-exact;
+  - values on sampled rows (every boundary situation + seeded random rows; for
+    C5 the corner blocks and rows on both sides of every slab seam) against the
+    oracle's direct sums, per-row tolerance of reading R6.
+"""
+import numpy as np
+import pytest
+
+import paper_1605_01238_b200 as wq
+from oracle import MASS, STIFFNESS, Oracle
+from parity_util import compare_rows, gather_rows_device, sample_rows
+from wqinputs import baseline_config
+
+pytestmark = pytest.mark.gpu
+
+CHUNK_NNZ = 1 << 28  # entries per streamed comparison chunk (1 GiB of int32 columns)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def check_pattern_in_full(o, rp_dev, col_dev, row_begin, n_rows):
+    """Stream the device row_ptr / col of the global rows [row_begin, row_begin + n_rows) (row_ptr
+    holding global offsets) against the oracle's pattern of the same rows, in chunks of whole
+    planes; bit-exact.  Returns the number of columns compared."""
+    torch = _torch()
+    rp = rp_dev.cpu().numpy()
+    assert rp.size == n_rows + 1
+    n1n2 = o.n[0] * (o.n[1] if o.d > 1 else 1)
+    r, checked = 0, 0
+    while r < n_rows:
+        r_hi = min(r + n1n2, n_rows)
+        while r_hi < n_rows and rp[min(r_hi + n1n2, n_rows)] - rp[r] <= CHUNK_NNZ:
+            r_hi = min(r_hi + n1n2, n_rows)
+        orp, ocol = o.pattern_rows(row_begin + r, row_begin + r_hi)
+        assert np.array_equal(rp[r:r_hi + 1], orp), f"row_ptr differs in rows [{row_begin + r}, {row_begin + r_hi})"
+        lo, hi = int(rp[r] - rp[0]), int(rp[r_hi] - rp[0])
+        ref = torch.from_numpy(ocol).to(col_dev.device)
+        assert torch.equal(col_dev[lo:hi], ref), f"columns differ in rows [{row_begin + r}, {row_begin + r_hi})"
+        checked += hi - lo
+        r = r_hi
+    return checked
+
+
+@pytest.mark.parametrize("name,p,k_random", [("C2", None, 96), ("C3", None, 24), ("C4", 2, 48), ("C4", 3, 48),
+                                             ("C4", 4, 32), ("C4", 6, 12), ("C4", 8, 4), ("C4", 10, 2)])
+def test_baseline_full_size(name, p, k_random):
+    """BASELINE configs at full size, AUTO kernel (the bench path): row_ptr and col in full,
+    sampled rows' values vs the oracle (strict regime asserted for p <= 6)."""
+    torch = _torch()
+    cfg = baseline_config(name, p)
+    ks, ctrl = cfg.knots(), cfg.ctrl()
+    mats = (STIFFNESS, MASS) if "mass" in cfg.matrices else (STIFFNESS,)
+    n = cfg.n_el + cfg.p
+    rows = sample_rows(n, 3, cfg.p, k_random=k_random, seed=1)
+    if cfg.p >= 8:
+        rows = rows[:: max(1, len(rows) // 24)]
+    o = Oracle(cfg.p, ks, ctrl)
+    plan = wq.Plan(cfg.p, ks, ctrl=ctrl, need_mass="mass" in cfg.matrices, need_stiffness=True)
+    info = plan.info
+    assert info["nnz_local"] == cfg.exact_nnz()
+    rp, col, val = plan.alloc_csr()
+    wq.wq_pattern(plan.h, 0, rp)
+    for mat in mats:
+        wq.wq_assemble(plan.h, mat, val, col)
+        wq.wq_check(plan.h)
+        torch.cuda.synchronize()
+        assert int(rp[-1]) == cfg.exact_nnz()
+        if mat == STIFFNESS:
+            assert check_pattern_in_full(o, rp, col, 0, info["n_rows_local"]) == cfg.exact_nnz()
+        ptr, oc, ov, kappa, scale = o.rows(mat, rows)
+        gptr, gc, gv = gather_rows_device(rp, col, val, rows)
+        st = compare_rows(rows, gptr, gc, gv, ptr, oc, ov, kappa, scale, strict=cfg.p <= 6)
+        print(name, p, mat, wq.KERNEL_NAMES[info["kernel"][mat]], st)
+    plan.close()
+    del rp, col, val
+    torch.cuda.empty_cache()
+
+
+def test_C5_slabs():
+    """BASELINE configs[4] (C5: 3D p=4, 256^3 elements, quarter annulus, 12.49e9 nnz) as the 8
+    x_3-slabs of the multi-GPU run, one after the other on one GPU: every slab plan
+    takes the z-line kernel; the per-slab blocks chain through nnz_base to the whole matrix
+    (row_ptr / col in full against the oracle pattern); values of the 8 corner blocks ((p+2)^3 rows
+    each) and of rows on both planes of every seam against the oracle."""
+    torch = _torch()
+    from paper_1605_01238_b200.dist import slab_cuts
+    cfg = baseline_config("C5")
+    ks, ctrl = cfg.knots(), cfg.ctrl()
+    p, n = cfg.p, cfg.n_el + cfg.p
+    o = Oracle(p, ks, ctrl)
+    cuts = slab_cuts(n, p, 8)
+    rng = np.random.default_rng(5)
+    corner = [a for a in range(p + 2)] + [n - 1 - a for a in range(p + 2)]
+    crow = {i1 + n * (i2 + n * i3) for i1 in corner for i2 in corner for i3 in corner}
+    seam = set()
+    for c in cuts[1:-1]:
+        for i3 in (c - 1, c):
+            for i1, i2 in rng.integers(0, n, size=(48, 2)):
+                seam.add(int(i1) + n * (int(i2) + n * i3))
+    want = np.array(sorted(crow | seam), dtype=np.int64)
+    base = 0
+    total_checked = 0
+    for s in range(8):
+        plan = wq.Plan(p, ks, ctrl=ctrl, slab=(cuts[s], cuts[s + 1]), need_mass=False, need_stiffness=True)
+        info = plan.info
+        assert info["kernel"][1] == wq.WQ_KERNEL_ZLINE
+        rp, col, val = plan.form(STIFFNESS, nnz_base=base)
+        torch.cuda.synchronize()
+        r0, nr = info["row_begin"], info["n_rows_local"]
+        total_checked += check_pattern_in_full(o, rp, col, r0, nr)
+        mine = want[(want >= r0) & (want < r0 + nr)]
+        ptr, oc, ov, kappa, scale = o.rows(STIFFNESS, mine)
+        gptr, gc, gv = gather_rows_device(rp - base, col, val, mine - r0)
+        compare_rows(mine, gptr, gc, gv, ptr, oc, ov, kappa, scale, strict=True)
+        assert int(rp[0]) == base
+        base += info["nnz_local"]
+        assert int(rp[-1]) == base
+        plan.close()
+        del rp, col, val
+        torch.cuda.empty_cache()
+    assert base == cfg.exact_nnz() == total_checked
