@@ -44,6 +44,7 @@ wq_status fail(wq_status st, const std::string &msg) {
 }  // namespace
 
 int64_t wq_host_qlo(int64_t i, int64_t E, int p) { return host_qlo(i, E, p); }
+int64_t wq_host_qhi(int64_t i, int64_t E, int p) { return host_qhi(i, E, p); }
 
 static std::atomic<uint64_t> g_launches{0};
 void wq_count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
@@ -409,6 +410,22 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
         }
         cbytes += zl;
     }
+    if (d == 3) {
+        // lines of the ZHP kernel: interior in directions 1 and 2 (boxes of 2p+1 points), then the rest
+        const int64_t n0 = P->dir[0].n, n1 = P->dir[1].n;
+        auto inter = [&](int l, int64_t i) {
+            return host_qhi(i, P->dir[l].E, p) - host_qlo(i, P->dir[l].E, p) + 1 == 2 * p + 1;
+        };
+        for (int64_t i1 = 0; i1 < n1; ++i1)
+            for (int64_t i0 = 0; i0 < n0; ++i0)
+                (inter(0, i0) && inter(1, i1) ? P->zh_int : P->zh_bnd).push_back((int32_t)(i0 + n0 * i1));
+        std::vector<int32_t> all(P->zh_int);
+        all.insert(all.end(), P->zh_bnd.begin(), P->zh_bnd.end());
+        ce = cudaMalloc((void **)&P->zh_dev, sizeof(int32_t) * all.size());
+        if (ce != cudaSuccess) { P->zh_dev = nullptr; wq_plan_destroy(P); return fail(WQ_ENOMEM, "line lists"); }
+        cudaMemcpy(P->zh_dev, all.data(), sizeof(int32_t) * all.size(), cudaMemcpyHostToDevice);
+        cbytes += sizeof(int32_t) * all.size();
+    }
     // ---- control net and coefficient nets (copied; the plan owns the device copies)
     wq_status st = WQ_OK;
     if (desc->ctrl) {
@@ -448,6 +465,7 @@ wq_status wq_plan_destroy(wq_plan P) {
     if (P->arena) cudaFree(P->arena);
     if (P->coef) cudaFree(P->coef);
     if (P->zlines_dev) cudaFree(P->zlines_dev);
+    if (P->zh_dev) cudaFree(P->zh_dev);
     if (P->ctrl_dev) cudaFree(P->ctrl_dev);
     if (P->kappa_dev) cudaFree(P->kappa_dev);
     if (P->gamma_dev) cudaFree(P->gamma_dev);

@@ -99,10 +99,15 @@ struct wq_plan_s {
     int zuni_state;
     double zuni_buf[3 * 21 * 4 + 3 * 2 * 11 * 2];
     int kernel_auto[2];            // wq_kernel AUTO runs for [mass, stiffness]
+    // z-line (ZHP) kernel lines (i1 + n1 * i2): interior in directions 1 and 2 first (#Q = 2p+1),
+    // then the rest; device copy zh_dev
+    std::vector<int32_t> zh_int, zh_bnd;
+    int32_t *zh_dev;
 };
 
 // host helpers
 int64_t wq_host_qlo(int64_t i, int64_t E, int p);  // first grid point of Q_i (Remark 1, reading R1)
+int64_t wq_host_qhi(int64_t i, int64_t E, int p);  // last grid point of Q_i
 void wq_count_launches(int n);  // adds n to the process-wide launch counter
 // cudaFuncAttributeMaxDynamicSharedMemorySize for `func` on the current device, set once per
 // (function, device) pair

@@ -1,0 +1,622 @@
+#pragma once
+// wq_zhp.cuh -- step 7, the z-line kernel for every degree and both matrices (WQ_KERNEL_ZHP):
+// lines along direction 3 like k_zline, but with CTA-wide phases instead of warp roles, so that
+// the shared-memory pipeline stays within the SM at high p.
+//
+// Arithmetic (Eq. sumfactorization P:837 / Alg. 3; stiffness reading R8, families R3).
+// A LINE is the set of rows i = (i0, i1, i2), (i0, i1) fixed, i2 over the plan's slab; an ITEM is a
+// line and a chunk of T consecutive values of t_0 (the first trial index).  With the weights of
+// directions 0 and 1 pushed onto the coefficient field pointwise:
+//   stiffness (6 chains (m, a2): m = trial-derivative direction, a2 = test derivative in dir. 2)
+//     H_{m,1} = w0^(0,b0) w1^(0,b1) C_2m,  H_{m,0} = w0^(1,b0) w1^(0,b1) C_0m + w0^(0,b0) w1^(1,b1) C_1m,
+//     b_k = [m == k];
+//     stage A (contract c0):  Y_{m,a2}(c1, t0) = sum_c0 D^{b0}B0_{t0}(c0) H_{m,a2}(c0, c1)
+//     stage B (contract c1):  G[b2][a2](t0, t1) = sum_{m: [m==2]=b2} sum_c1 D^{b1}B1_{t1}(c1) Y_{m,a2}(c1, t0)
+//     stage C (contract c2, per row i2):
+//       S(i; t0, t1, t2) = sum_c2 B2_{t2}(c2) U0(c2) + B2'_{t2}(c2) U1(c2),
+//       U0 = w2^(0,0) G[0][0] + w2^(1,0) G[0][1],  U1 = w2^(0,1) G[1][0] + w2^(1,1) G[1][1];
+//   mass (one chain): H = w0^(0,0) w1^(0,0) c, Y = sum_c0 B0 H, G = sum_c1 B1 Y,
+//       M(i; t) = sum_c2 w2^(0,0) B2_{t2}(c2) G(c2).
+// Staircases for every row type: the points c of a row are grouped by their staircase offset
+// o(c) = span(c) - jlo (non-decreasing in c, 0 <= o <= p for every row of every knot vector), and
+// the kernel loops over o at compile time and over the points of the group at run time, so each
+// accumulator index o + r is a compile-time register index while the group bounds come from
+// small per-row tables: one code path for interior, boundary and graded rows.
+//
+// CTA (256 threads, one or two per SM, persistent over items): per step of R rows of the line
+//   production of the G planes the step needs, pair of points by pair of points (the coefficient
+//   box of a pair, 2 x QX x QX x ncomp, is one 4D TMA tile of the z layout, double buffered):
+//     stage A (threads = fibres (m, c1, point)), barrier, next box load, stage B (threads =
+//     (point, family, t0)) into a ring of G planes (+ the planes' direction-2 basis pairs);
+//   stage C: threads = (row, column (t0, t1)), acc[t2] in registers, plain coalesced stores of
+//   values (and fused columns) straight from registers.
+// The chunks of a line are consecutive items, so they run at the same time on neighbouring CTAs
+// and their interleaved partial-sector stores merge in L2.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <algorithm>
+#include "wq_rows.cuh"
+#include "wq_dev.cuh"
+
+namespace zhp {
+using namespace wqdev;
+
+constexpr int NPRO = 128;             // producer threads (stages A, B)
+constexpr int NCON = 256;             // consumer threads (stage C)
+constexpr int NT = NPRO + NCON;
+
+// column chunks of t_0 per degree (the G ring of a chunk, T (2p+1) x 4 doubles per point, and the
+// coefficient boxes must fit the SM's shared memory)
+__host__ __device__ constexpr int nch_of(int p) { return p <= 5 ? 1 : (p <= 7 ? 2 : (p <= 9 ? 3 : 5)); }
+template <int P>
+struct Chunks {
+    static constexpr int K = 2 * P + 1, NCH = nch_of(P), T = (K + NCH - 1) / NCH;
+    __host__ __device__ static constexpr int ta(int ch) { return ch * K / NCH; }  // balanced: widths T or T-1
+    __host__ __device__ static constexpr int tn(int ch) { return ta(ch + 1) - ta(ch); }
+};
+
+template <int P, bool MASS, int T, int QX>
+struct Cfg {
+    static constexpr int K = 2 * P + 1;
+    static constexpr int NP = P + 1;
+    static constexpr int NCH = nch_of(P);
+    static_assert(T == Chunks<P>::T, "chunk width");
+    static constexpr int NC = MASS ? 1 : 6;       // coefficient components in the box
+    static constexpr int NCHAIN = MASS ? 1 : 6;   // stage-A chains
+    static constexpr int NGF = MASS ? 1 : 4;      // G families per column
+    static constexpr int COLS = T * K;            // columns (t0 local, t1) of an item, t0 fastest
+    static constexpr int BOXD = (NC * QX * QX * 2 + 15) / 16 * 16;  // doubles per box buffer (128-B aligned TMA dst)
+    static constexpr int YPAIR = 2 * NCHAIN * QX * T;  // doubles of Y per pair [pt][chain][c1][t0]
+    static constexpr int SLOT = COLS * NGF;       // doubles of a G ring slot [col][family]
+    static constexpr int QR = 3 * P + 1;          // max #Q of a row (n_EL >= p+2)
+};
+
+struct Args {
+    DirView v[3];
+    int64_t n0, n1;          // DOFs in directions 0, 1
+    int64_t L0, L1;          // sum_i #I_{0,i}, sum_i #I_{1,i}
+    int64_t slab_b;          // first owned plane of i2 (CSR offsets relative to it)
+    int64_t i2b, n2l;        // rows of this launch: planes [i2b, i2b + n2l) of the slab
+    int64_t cq_b;            // first q2 of the coefficient sub-grid
+    int64_t qoff;            // even local q2 (relative to cq_b) of this launch's first pair
+    const int32_t *lines;    // line = i0 + n0 * i1
+    int64_t n_lines;
+    int ns;                  // G ring slots
+    int R;                   // rows per step
+    int nb;                  // box buffers
+    double *val;
+    int32_t *col;
+    int64_t val_base;
+};
+
+// shared-memory carve-up (byte offsets), identical on host and device
+struct Layout {
+    size_t bar, box, y, ring, rb2, t0, t1, w0, w1, o0, o1, g0, g1, w2, g2, d2, total;
+};
+template <int P, bool MASS, int T, int QX>
+__host__ __device__ inline Layout layout(int nb, int R, int ns, int64_t n2l) {
+    using CF = Cfg<P, MASS, T, QX>;
+    Layout L;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 127) & ~(size_t)127; return r; };
+    L.bar = take(8 * 8);
+    L.box = take(8 * (size_t)nb * CF::BOXD);
+    L.y = take(8 * (size_t)R * CF::YPAIR);
+    L.ring = take(8 * (size_t)ns * CF::SLOT);
+    L.rb2 = take(16 * (size_t)ns * CF::NP);
+    L.t0 = take(16 * (size_t)QX * CF::NP);
+    L.t1 = take(16 * (size_t)QX * CF::NP);
+    L.w0 = take(8 * 4 * (size_t)QX);
+    L.w1 = take(8 * 4 * (size_t)QX);
+    L.o0 = take(4 * (size_t)QX);
+    L.o1 = take(4 * (size_t)QX);
+    L.g0 = take(4 * (size_t)(CF::NP + 1));
+    L.g1 = take(4 * (size_t)(CF::NP + 1));
+    L.w2 = take(8 * 4 * 2 * (size_t)R * CF::QR);
+    L.g2 = take(4 * 2 * (size_t)R * (CF::NP + 1));
+    L.d2 = take(8 * (size_t)(n2l + 1) + 16 * (size_t)n2l);
+    L.total = o;
+    return L;
+}
+
+// group bounds of a point range: g[o] = first point c with off[c] >= o, o = 0..NP (g[NP] = n)
+template <int NP>
+__device__ __forceinline__ void groups(const int *off, int n, int *g, int tid) {
+    if (tid <= NP) {
+        int c = 0;
+        while (c < n && off[c] < tid) ++c;
+        g[tid] = tid == NP ? n : c;
+    }
+}
+
+template <int P, bool MASS, int T, int QX, int CH>
+__device__ __forceinline__ void stage_a(const double *box, double *Y, const double2 *B0t, const double *W0t,
+                                        const double *W1t, const int *g0, int nq0, int nq1, int tid) {
+    using CF = Cfg<P, MASS, T, QX>;
+    constexpr int TA = Chunks<P>::ta(CH), TN = Chunks<P>::tn(CH);  // t0 range of the chunk
+    const int nfib = (MASS ? 1 : 3) * nq1 * 2;
+    for (int f = tid; f < nfib; f += NPRO) {
+        const int pt = f & 1, c1 = (f >> 1) % nq1, m = (f >> 1) / nq1;
+        double y0[T], y1[T];
+        #pragma unroll
+        for (int t = 0; t < T; ++t) { y0[t] = 0.0; y1[t] = 0.0; }
+        if constexpr (MASS) {
+            const double w1 = W1t[c1 * 4 + 0];
+            unroll<CF::NP>([&](auto O) {
+                constexpr int o = decltype(O)::value;
+                for (int c0 = g0[o]; c0 < g0[o + 1]; ++c0) {
+                    const double h = W0t[c0 * 4 + 0] * w1 * box[(c0 * QX + c1) * 2 + pt];
+                    const double2 *bp = B0t + c0 * CF::NP;
+                    #pragma unroll
+                    for (int r = 0; r <= P; ++r) {
+                        const int t = o + r - TA;
+                        if (t >= 0 && t < TN) y0[t] = fma(bp[r].x, h, y0[t]);
+                    }
+                }
+            });
+            double *Yo = Y + ((pt * CF::NCHAIN + 0) * QX + c1) * T;
+            #pragma unroll
+            for (int t = 0; t < T; ++t) Yo[t] = y0[t];
+        } else {
+            // components C00 C01 C02 C11 C12 C22: ka = C_2m, kb = C_0m, kc = C_1m
+            const int ka = m == 0 ? 2 : (m == 1 ? 4 : 5);
+            const int kb = m == 0 ? 0 : (m == 1 ? 1 : 2);
+            const int kc = m == 0 ? 1 : (m == 1 ? 3 : 4);
+            const double2 w1p = *(const double2 *)(W1t + c1 * 4 + (m == 1 ? 2 : 0));  // (w1^(0,b1), w1^(1,b1))
+            const int w0o = m == 0 ? 2 : 0;
+            const bool der0 = m == 0;
+            unroll<CF::NP>([&](auto O) {
+                constexpr int o = decltype(O)::value;
+                for (int c0 = g0[o]; c0 < g0[o + 1]; ++c0) {
+                    const double2 w0p = *(const double2 *)(W0t + c0 * 4 + w0o);  // (w0^(0,b0), w0^(1,b0))
+                    const double s1 = w0p.x * w1p.x, s2 = w0p.y * w1p.x, s3 = w0p.x * w1p.y;
+                    const double ca = box[((ka * QX + c0) * QX + c1) * 2 + pt];
+                    const double cb = box[((kb * QX + c0) * QX + c1) * 2 + pt];
+                    const double cc = box[((kc * QX + c0) * QX + c1) * 2 + pt];
+                    const double h1 = s1 * ca;                  // a2 = 1 (l = 2)
+                    const double h0 = fma(s2, cb, s3 * cc);     // a2 = 0 (l = 0, 1)
+                    const double2 *bp = B0t + c0 * CF::NP;
+                    #pragma unroll
+                    for (int r = 0; r <= P; ++r) {
+                        const int t = o + r - TA;
+                        if (t >= 0 && t < TN) {
+                            const double bv = der0 ? bp[r].y : bp[r].x;
+                            y0[t] = fma(bv, h0, y0[t]);
+                            y1[t] = fma(bv, h1, y1[t]);
+                        }
+                    }
+                }
+            });
+            double *Y0 = Y + ((pt * CF::NCHAIN + m * 2 + 0) * QX + c1) * T;
+            double *Y1 = Y + ((pt * CF::NCHAIN + m * 2 + 1) * QX + c1) * T;
+            #pragma unroll
+            for (int t = 0; t < T; ++t) { Y0[t] = y0[t]; Y1[t] = y1[t]; }
+        }
+    }
+}
+
+template <int P, bool MASS, int T, int QX>
+__global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorMap tm, Args a) {
+    using CF = Cfg<P, MASS, T, QX>;
+    constexpr int K = CF::K, NP = CF::NP, NCH = CF::NCH, COLS = CF::COLS, NGF = CF::NGF;
+    constexpr int BS = wq_bstride(P);
+    extern __shared__ __align__(128) unsigned char smb[];
+    const int tid = threadIdx.x;
+    const int R = a.R, NS = a.ns, NB = a.nb;
+    const int n2l = (int)a.n2l;
+    const Layout Ly = layout<P, MASS, T, QX>(NB, R, NS, a.n2l);
+    uint64_t *full = (uint64_t *)(smb + Ly.bar);  // [NB] box loads
+    uint64_t *ready = full + 4;                   // [2] step planes produced (count NPRO)
+    uint64_t *freeb = full + 6;                   // [2] step consumed (count NCON)
+    double *Box = (double *)(smb + Ly.box);
+    double *Y = (double *)(smb + Ly.y);
+    double *Ring = (double *)(smb + Ly.ring);
+    double2 *RB2 = (double2 *)(smb + Ly.rb2);
+    double2 *B0t = (double2 *)(smb + Ly.t0), *B1t = (double2 *)(smb + Ly.t1);
+    double *W0t = (double *)(smb + Ly.w0), *W1t = (double *)(smb + Ly.w1);
+    int *off0 = (int *)(smb + Ly.o0), *off1 = (int *)(smb + Ly.o1);
+    int *g0 = (int *)(smb + Ly.g0), *g1 = (int *)(smb + Ly.g1);
+    double *W2s = (double *)(smb + Ly.w2);  // [2 parities][R][QR][4]
+    int *g2s = (int *)(smb + Ly.g2);        // [2 parities][R][NP+1]
+    int64_t *pref2 = (int64_t *)(smb + Ly.d2);
+    int *qlo2 = (int *)(pref2 + n2l + 1), *qlen2 = qlo2 + n2l, *jlo2 = qlen2 + n2l, *jlen2 = jlo2 + n2l;
+
+    const DirView &v0 = a.v[0], &v1 = a.v[1], &v2 = a.v[2];
+    const int i2b = (int)a.i2b;
+    const int cqb = (int)(a.cq_b + a.qoff);  // global index of local point 0 (even offset in the z field)
+    for (int x = tid; x < n2l; x += NT) {
+        qlo2[x] = v2.qlo[i2b + x] - cqb; qlen2[x] = v2.qlen[i2b + x]; jlo2[x] = v2.jlo[i2b + x]; jlen2[x] = v2.jlen[i2b + x];
+    }
+    for (int x = tid; x <= n2l; x += NT) pref2[x] = v2.pref[i2b + x] - v2.pref[a.slab_b];
+    if (tid == 0) {
+        for (int b = 0; b < NB; ++b) mbar_init(&full[b], 1);
+        for (int b = 0; b < 2; ++b) { mbar_init(&ready[b], NPRO); mbar_init(&freeb[b], NCON); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int q_end = qlo2[n2l - 1] + qlen2[n2l - 1];  // local end of the last row's Q
+    const int npairs = (q_end + 1) / 2;
+    const int nsteps = (n2l + R - 1) / R;
+    const int64_t n_items = a.n_lines * NCH;
+    constexpr unsigned BOX_BYTES = CF::NC * QX * QX * 2 * 8;
+
+    if (tid < NPRO) {
+        // ================================================================ producers
+        const int ptid = tid;
+        unsigned use_bits = 0;  // phase parity of each box buffer's next use (bit b)
+        int64_t gs = 0;         // global step counter (shared sequence with the consumers)
+        for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+            const int line = a.lines[it / NCH];
+            const int ch = (int)(it % NCH);
+            const int i0 = (int)(line % a.n0), i1 = (int)(line / a.n0);
+            const int ql0 = v0.qlo[i0], nq0 = v0.qlen[i0], jl0 = v0.jlo[i0];
+            const int ql1 = v1.qlo[i1], nq1 = v1.qlen[i1], jl1 = v1.jlo[i1];
+            // the ring restarts at plane 0: wait until the consumers have finished the previous item
+            if (gs >= 1) mbar_wait(&freeb[(gs - 1) & 1], ((gs - 1) >> 1) & 1);
+            bar_sync(1, NPRO);  // every producer is past the previous item (tables free)
+            if (ptid == 0) {
+                for (int b = 0; b < NB && b < npairs; ++b) {
+                    mbar_arrive_tx(&full[b], BOX_BYTES);
+                    tma_load_4d(Box + b * CF::BOXD, &tm, &full[b], (int)a.qoff + 2 * b, ql1, ql0, 0);
+                }
+            }
+            for (int x = ptid; x < QX * NP; x += NPRO) {
+                const int c = x / NP, r = x % NP;
+                B0t[x] = c < nq0 ? __ldg((const double2 *)(v0.B + (int64_t)(ql0 + c) * BS) + r) : make_double2(0.0, 0.0);
+                B1t[x] = c < nq1 ? __ldg((const double2 *)(v1.B + (int64_t)(ql1 + c) * BS) + r) : make_double2(0.0, 0.0);
+            }
+            for (int x = ptid; x < 4 * QX; x += NPRO) {
+                W0t[x] = x / 4 < nq0 ? __ldg(v0.W + (int64_t)i0 * v0.maxq * 4 + x) : 0.0;
+                W1t[x] = x / 4 < nq1 ? __ldg(v1.W + (int64_t)i1 * v1.maxq * 4 + x) : 0.0;
+            }
+            for (int x = ptid; x < QX; x += NPRO) {
+                off0[x] = x < nq0 ? v0.span[ql0 + x] - jl0 : 1 << 20;
+                off1[x] = x < nq1 ? v1.span[ql1 + x] - jl1 : 1 << 20;
+            }
+            bar_sync(1, NPRO);
+            groups<NP>(off0, nq0, g0, ptid);
+            if (ptid >= 32 && ptid <= 32 + NP) groups<NP>(off1, nq1, g1, ptid - 32);
+            bar_sync(1, NPRO);
+            int pairs_done = 0;
+            for (int st = 0; st < nsteps; ++st, ++gs) {
+                const int r0 = st * R;
+                const int rl = (r0 + R <= n2l ? r0 + R : n2l) - 1;
+                const int need = (qlo2[rl] + qlen2[rl] + 1) / 2;  // pairs covering the step's last point
+                // the slots this step writes were last read two steps ago
+                if (gs >= 2) mbar_wait(&freeb[gs & 1], ((gs >> 1) - 1) & 1);
+                while (pairs_done < need) {
+                    const int nbat = need - pairs_done < R ? need - pairs_done : R;
+                    for (int k = 0; k < nbat; ++k) {
+                        const int pp = pairs_done + k, b = pp % NB;
+                        mbar_wait(&full[b], (use_bits >> b) & 1);
+                        const double *bx = Box + b * CF::BOXD;
+                        double *Yk = Y + k * CF::YPAIR;
+                        switch (ch) {
+                        case 0: stage_a<P, MASS, T, QX, 0>(bx, Yk, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
+                        case 1: if constexpr (NCH > 1) stage_a<P, MASS, T, QX, 1>(bx, Yk, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
+                        case 2: if constexpr (NCH > 2) stage_a<P, MASS, T, QX, 2>(bx, Yk, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
+                        case 3: if constexpr (NCH > 3) stage_a<P, MASS, T, QX, 3>(bx, Yk, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
+                        case 4: if constexpr (NCH > 4) stage_a<P, MASS, T, QX, 4>(bx, Yk, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
+                        default: break;
+                        }
+                        bar_sync(1, NPRO);  // box b consumed, Y_k written
+                        use_bits ^= 1u << b;
+                        if (ptid == 0 && pp + NB < npairs) {
+                            fence_async_smem();
+                            mbar_arrive_tx(&full[b], BOX_BYTES);
+                            tma_load_4d(Box + b * CF::BOXD, &tm, &full[b], (int)a.qoff + 2 * (pp + NB), ql1, ql0, 0);
+                        }
+                    }
+                    // stage B for the batch: items (plane j, t0, family g) -> G ring, + the planes' B2 pairs
+                    const int nitem = nbat * 2 * NGF * T;
+                    for (int x = ptid; x < nitem; x += NPRO) {
+                        const int g = x % NGF, tl = (x / NGF) % T, j = x / (NGF * T);
+                        const int k = j >> 1, pt = j & 1;
+                        const int q = 2 * (pairs_done + k) + pt;  // local point
+                        const double *Yk = Y + k * CF::YPAIR + pt * CF::NCHAIN * QX * T;
+                        double acc[K];
+                        #pragma unroll
+                        for (int t = 0; t < K; ++t) acc[t] = 0.0;
+                        if constexpr (MASS) {
+                            unroll<NP>([&](auto O) {
+                                constexpr int o = decltype(O)::value;
+                                for (int c1 = g1[o]; c1 < g1[o + 1]; ++c1) {
+                                    const double yv = Yk[c1 * T + tl];
+                                    const double2 *bp = B1t + c1 * NP;
+                                    #pragma unroll
+                                    for (int r = 0; r <= P; ++r) acc[o + r] = fma(bp[r].x, yv, acc[o + r]);
+                                }
+                            });
+                        } else {
+                            // g = a2 + 2 b2: b2 = 0 sums chains m = 0 (B1 values) and m = 1 (B1
+                            // derivatives), b2 = 1 is chain m = 2 (B1 values)
+                            const int a2 = g & 1, b2 = g >> 1;
+                            const double *Ya = Yk + ((b2 ? 4 : 0) + a2) * QX * T;
+                            const double *Yb = Yk + (2 + a2) * QX * T;
+                            unroll<NP>([&](auto O) {
+                                constexpr int o = decltype(O)::value;
+                                for (int c1 = g1[o]; c1 < g1[o + 1]; ++c1) {
+                                    const double ya = Ya[c1 * T + tl];
+                                    const double yb = b2 ? 0.0 : Yb[c1 * T + tl];
+                                    const double2 *bp = B1t + c1 * NP;
+                                    #pragma unroll
+                                    for (int r = 0; r <= P; ++r) acc[o + r] = fma(bp[r].y, yb, fma(bp[r].x, ya, acc[o + r]));
+                                }
+                            });
+                        }
+                        double *G = Ring + (size_t)(q % NS) * CF::SLOT;
+                        #pragma unroll
+                        for (int t = 0; t < K; ++t) G[(tl + T * t) * NGF + g] = acc[t];
+                    }
+                    for (int x = ptid; x < nbat * 2 * NP; x += NPRO) {
+                        const int q = 2 * pairs_done + x / NP, r = x % NP;
+                        RB2[(q % NS) * NP + r] = q < q_end ? __ldg((const double2 *)(v2.B + (int64_t)(cqb + q) * BS) + r)
+                                                           : make_double2(0.0, 0.0);
+                    }
+                    bar_sync(1, NPRO);  // Y free for the next batch
+                    pairs_done += nbat;
+                }
+                mbar_arrive(&ready[gs & 1]);  // release: this step's planes are in the ring
+            }
+        }
+        return;
+    }
+    // ==================================================================== consumers
+    const int ctid = tid - NPRO;
+    int64_t gs = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int line = a.lines[it / NCH];
+        const int ch = (int)(it % NCH);
+        const int i0 = (int)(line % a.n0), i1 = (int)(line / a.n0);
+        const int jl0 = v0.jlo[i0], ni0 = v0.jlen[i0];
+        const int jl1 = v1.jlo[i1], ni1 = v1.jlen[i1];
+        const int ta = Chunks<P>::ta(ch), tn = Chunks<P>::tn(ch);
+        // CSR offset of row (i0, i1, i2) relative to the first owned row minus val_base:
+        // (pref2[i2] - pref2[slab_b]) L1 L0 + ni2 pref1[i1] L0 + ni2 ni1 pref0[i0]
+        const int64_t p1L0 = v1.pref[i1] * a.L0, p0n1 = v0.pref[i0] * (int64_t)ni1;
+        for (int st = 0; st < nsteps; ++st, ++gs) {
+            const int r0 = st * R;
+            const int nr = r0 + R <= n2l ? R : n2l - r0;
+            const int par = (int)(gs & 1);
+            double *W2p = W2s + (size_t)par * R * CF::QR * 4;
+            int *g2p = g2s + par * R * (NP + 1);
+            // row tables of the step: weights of direction 2 and the staircase groups
+            for (int x = ctid; x < nr * CF::QR * 4; x += NCON) {
+                const int rho = x / (CF::QR * 4), e = x % (CF::QR * 4);
+                const int i2 = i2b + r0 + rho;
+                W2p[x] = e / 4 < qlen2[r0 + rho] ? __ldg(v2.W + (int64_t)i2 * v2.maxq * 4 + e) : 0.0;
+            }
+            if (ctid < nr * (NP + 1)) {
+                const int rho = ctid / (NP + 1), o = ctid % (NP + 1), rr = r0 + rho;
+                const int q0 = qlo2[rr], n = qlen2[rr], j = jlo2[rr];
+                int c = 0;
+                while (c < n && v2.span[cqb + q0 + c] - j < o) ++c;
+                g2p[rho * (NP + 1) + o] = o == NP ? n : c;
+            }
+            bar_sync(2, NCON);
+            mbar_wait(&ready[par], (gs >> 1) & 1);  // acquire: the step's planes
+            for (int x = ctid; x < nr * COLS; x += NCON) {
+                const int rho = x / COLS, cl = x % COLS;
+                const int tl = cl % T, t1 = cl / T, tg = ta + tl;
+                const int rr = r0 + rho;
+                const int q0 = qlo2[rr];
+                const double *Wr = W2p + rho * CF::QR * 4;
+                const int *gg = g2p + rho * (NP + 1);
+                double acc[K];
+                #pragma unroll
+                for (int t = 0; t < K; ++t) acc[t] = 0.0;
+                unroll<NP>([&](auto O) {
+                    constexpr int o = decltype(O)::value;
+                    for (int c = gg[o]; c < gg[o + 1]; ++c) {
+                        const int s = (q0 + c) % NS;
+                        const double2 *bp = RB2 + s * NP;
+                        if constexpr (MASS) {
+                            const double u = Wr[c * 4] * Ring[(size_t)s * CF::SLOT + cl];
+                            #pragma unroll
+                            for (int r = 0; r <= P; ++r) acc[o + r] = fma(bp[r].x, u, acc[o + r]);
+                        } else {
+                            const double4 G = *(const double4 *)(Ring + (size_t)s * CF::SLOT + cl * 4);
+                            const double4 w = *(const double4 *)(Wr + c * 4);
+                            const double u0 = fma(w.x, G.x, w.y * G.y), u1 = fma(w.z, G.z, w.w * G.w);
+                            #pragma unroll
+                            for (int r = 0; r <= P; ++r) acc[o + r] = fma(bp[r].y, u1, fma(bp[r].x, u0, acc[o + r]));
+                        }
+                    }
+                });
+                if (tl < tn && tg < ni0 && t1 < ni1) {
+                    const int ni2 = jlen2[rr];
+                    const int64_t row = pref2[rr] * a.L1 * a.L0 + (int64_t)ni2 * (p1L0 + p0n1) - a.val_base;
+                    const int64_t e0 = row + tg + (int64_t)ni0 * t1, stp = (int64_t)ni0 * ni1;
+                    #pragma unroll
+                    for (int t = 0; t < K; ++t)
+                        if (t < ni2) a.val[e0 + stp * t] = acc[t];
+                    if (a.col) {
+                        const int jb = (jl0 + tg) + (int)a.n0 * ((jl1 + t1) + (int)a.n1 * jlo2[rr]);
+                        const int js = (int)(a.n0 * a.n1);
+                        #pragma unroll
+                        for (int t = 0; t < K; ++t)
+                            if (t < ni2) a.col[e0 + stp * t] = jb + js * t;
+                    }
+                }
+            }
+            mbar_arrive(&freeb[par]);  // this step's ring slots may be overwritten
+        }
+    }
+}
+
+}  // namespace zhp
+
+// ---------------------------------------------------------------- host side
+namespace zhp {
+
+inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+struct Plan2 {  // launch geometry along the slab direction for the planes [pl_lo, pl_hi)
+    int64_t i2b, n2l, qoff;
+    std::vector<int32_t> qlo, qhi;  // local (relative to cq_b + qoff)
+};
+inline Plan2 plan2(const wq_plan_s *Pl, int64_t pl_lo, int64_t pl_hi) {
+    Plan2 g;
+    const int p = Pl->p;
+    const int64_t E = Pl->dir[2].E;
+    g.i2b = Pl->slab_b + pl_lo;
+    g.n2l = pl_hi - pl_lo;
+    g.qoff = (wq_host_qlo(g.i2b, E, p) - Pl->cq_b) & ~(int64_t)1;
+    for (int64_t i = g.i2b; i < g.i2b + g.n2l; ++i) {
+        g.qlo.push_back((int32_t)(wq_host_qlo(i, E, p) - Pl->cq_b - g.qoff));
+        g.qhi.push_back((int32_t)(wq_host_qhi(i, E, p) - Pl->cq_b - g.qoff));
+    }
+    return g;
+}
+// ring slots for R rows per step: the production of a step overwrites slot (q mod NS) of planes q <
+// 2 need while the step's rows read planes >= qlo(first row)
+// (the producers write the planes of step s+1 while the consumers read those of step s)
+inline int ring_slots(const Plan2 &g, int R) {
+    int ns = 2;
+    for (int64_t r0 = 0; r0 < g.n2l; r0 += R) {
+        const int64_t r1 = std::min<int64_t>(r0 + 2 * R, g.n2l) - 1;  // last row of the next step
+        const int need = (g.qhi[r1] + 2) / 2;
+        ns = std::max(ns, 2 * need - g.qlo[r0]);
+    }
+    return ns;
+}
+
+template <int P, bool MASS, int QX>
+bool choose(const Plan2 &g, int &nb, int &R, int &ns, size_t &smem, int optin) {
+    constexpr int T = Chunks<P>::T;
+    using CF = Cfg<P, MASS, T, QX>;
+    // rows per step: as many as one pass of the consumer threads covers (stage C items = rows x COLS)
+    int rbest = NCON / CF::COLS;
+    rbest = rbest < 1 ? 1 : (rbest > 8 ? 8 : rbest);
+    if (getenv("WQ_ZHP_R")) rbest = atoi(getenv("WQ_ZHP_R"));
+    const int nb_env = getenv("WQ_ZHP_NB") ? atoi(getenv("WQ_ZHP_NB")) : 0;
+    for (int r = rbest; r >= 1; --r)
+        for (int b = 3; b >= 1; --b) {
+            if (nb_env && b != nb_env) continue;
+            const int n = ring_slots(g, r);
+            const Layout L = layout<P, MASS, T, QX>(b, r, n, g.n2l);
+            if (L.total <= (size_t)optin) {
+                nb = b;
+                R = r;
+                ns = n;
+                smem = L.total;
+                return true;
+            }
+        }
+    return false;
+}
+
+template <int P, bool MASS, int QX>
+wq_status launch_cls(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, const Plan2 &g, double *val, int32_t *col,
+                     int64_t val_base, cudaStream_t s) {
+    constexpr int T = Chunks<P>::T, NCH = Chunks<P>::NCH;
+    using CF = Cfg<P, MASS, T, QX>;
+    if (n_lines <= 0 || g.n2l <= 0) return WQ_OK;
+    int optin = 0, nsm = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, Pl->device);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, Pl->device);
+    Args a;
+    int nb = 0, R = 0, ns = 0;
+    size_t smem = 0;
+    if (!choose<P, MASS, QX>(g, nb, R, ns, smem, optin)) {
+        wq_set_error("ZHP kernel: shared memory does not fit this slab");
+        return WQ_EINVAL;
+    }
+    for (int l = 0; l < 3; ++l) a.v[l] = Pl->dir[l];
+    a.n0 = Pl->dir[0].n;
+    a.n1 = Pl->dir[1].n;
+    a.L0 = Pl->L[0];
+    a.L1 = Pl->L[1];
+    a.slab_b = Pl->slab_b;
+    a.i2b = g.i2b;
+    a.n2l = g.n2l;
+    a.cq_b = Pl->cq_b;
+    a.qoff = g.qoff;
+    a.lines = lines;
+    a.n_lines = n_lines;
+    a.ns = ns;
+    a.R = R;
+    a.nb = nb;
+    a.val = val;
+    a.col = col;
+    a.val_base = val_base;
+    auto fn = encode_fn();
+    if (!fn) { wq_set_error("cuTensorMapEncodeTiled unavailable"); return WQ_ECUDA; }
+    CUtensorMap m;
+    const int64_t nq0 = Pl->dir[0].nq, nq1 = Pl->dir[1].nq;
+    const double *base = Pl->coef + (MASS ? (int64_t)Pl->comp_mass * Pl->zcs : 0);
+    cuuint64_t dims[4] = {(cuuint64_t)Pl->zld, (cuuint64_t)nq1, (cuuint64_t)nq0, (cuuint64_t)CF::NC};
+    cuuint64_t strides[3] = {(cuuint64_t)Pl->zld * 8, (cuuint64_t)Pl->zld * nq1 * 8, (cuuint64_t)Pl->zcs * 8};
+    cuuint32_t box[4] = {2, (cuuint32_t)QX, (cuuint32_t)QX, (cuuint32_t)CF::NC};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void *)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS) {
+        wq_set_error("cuTensorMapEncodeTiled failed for the coefficient field");
+        return WQ_ECUDA;
+    }
+    const int64_t items = n_lines * NCH;
+    int per_sm = 1;
+    if (getenv("WQ_ZHP_CTAS")) per_sm = atoi(getenv("WQ_ZHP_CTAS"));
+    const int64_t grid = std::min<int64_t>(items, (int64_t)nsm * per_sm);
+    cudaError_t ce = wq_smem_attr((const void *)k_zhp<P, MASS, T, QX>, smem);
+    if (ce != cudaSuccess) return wq_cuda_status(ce, "ZHP smem attribute");
+    k_zhp<P, MASS, T, QX><<<(unsigned)grid, NT, smem, s>>>(m, a);
+    wq_count_launches(1);
+    return wq_cuda_status(cudaGetLastError(), "ZHP assembly kernel");
+}
+
+template <int P>
+bool supported_p(const wq_plan_s *Pl, int matrix) {
+    const Plan2 g = plan2(Pl, 0, Pl->slab_e - Pl->slab_b);
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, Pl->device);
+    if (optin <= 0) optin = 227 * 1024;
+    int nb, R, ns;
+    size_t sm;
+    return matrix == WQ_MASS ? choose<P, true, 3 * P + 1>(g, nb, R, ns, sm, optin) &&
+                                   choose<P, true, 2 * P + 1>(g, nb, R, ns, sm, optin)
+                             : choose<P, false, 3 * P + 1>(g, nb, R, ns, sm, optin) &&
+                                   choose<P, false, 2 * P + 1>(g, nb, R, ns, sm, optin);
+}
+
+template <int P>
+wq_status launch_p(wq_plan_s *Pl, int matrix, int64_t pl_lo, int64_t pl_hi, double *val, int32_t *col,
+                   int64_t val_base, cudaStream_t s) {
+    const Plan2 g = plan2(Pl, pl_lo, pl_hi);
+    const int64_t ni = (int64_t)Pl->zh_int.size(), nbd = (int64_t)Pl->zh_bnd.size();
+    wq_status st;
+    if (matrix == WQ_MASS) {
+        st = launch_cls<P, true, 2 * P + 1>(Pl, Pl->zh_dev, ni, g, val, col, val_base, s);
+        if (!st) st = launch_cls<P, true, 3 * P + 1>(Pl, Pl->zh_dev + ni, nbd, g, val, col, val_base, s);
+    } else {
+        st = launch_cls<P, false, 2 * P + 1>(Pl, Pl->zh_dev, ni, g, val, col, val_base, s);
+        if (!st) st = launch_cls<P, false, 3 * P + 1>(Pl, Pl->zh_dev + ni, nbd, g, val, col, val_base, s);
+    }
+    return st;
+}
+
+}  // namespace zhp
+
+#define WQ_ZHP_DEG_DECL(PP)                                                                                          \
+    bool zhp_supported_deg_##PP(const wq_plan_s *Pl, int matrix);                                                 \
+    wq_status zhp_launch_deg_##PP(wq_plan_s *Pl, int matrix, int64_t pl_lo, int64_t pl_hi, double *val, int32_t *col, \
+                                  int64_t val_base, cudaStream_t s);
+#define WQ_ZHP_DEG_DEF(PP)                                                                                           \
+    bool zhp_supported_deg_##PP(const wq_plan_s *Pl, int matrix) { return zhp::supported_p<PP>(Pl, matrix); }      \
+    wq_status zhp_launch_deg_##PP(wq_plan_s *Pl, int matrix, int64_t pl_lo, int64_t pl_hi, double *val, int32_t *col, \
+                                  int64_t val_base, cudaStream_t s) {                                               \
+        return zhp::launch_p<PP>(Pl, matrix, pl_lo, pl_hi, val, col, val_base, s);                                   \
+    }
+WQ_ZHP_DEG_DECL(1) WQ_ZHP_DEG_DECL(2) WQ_ZHP_DEG_DECL(3) WQ_ZHP_DEG_DECL(4) WQ_ZHP_DEG_DECL(5)
+WQ_ZHP_DEG_DECL(6) WQ_ZHP_DEG_DECL(7) WQ_ZHP_DEG_DECL(8) WQ_ZHP_DEG_DECL(9) WQ_ZHP_DEG_DECL(10)

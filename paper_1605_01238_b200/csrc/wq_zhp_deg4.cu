@@ -1,0 +1,3 @@
+// wq_zhp_deg4.cu -- instantiation of the ZHP line kernel for p = 4 (one TU per degree: parallel builds)
+#include "wq_zhp.cuh"
+WQ_ZHP_DEG_DEF(4)

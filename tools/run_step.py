@@ -18,7 +18,7 @@ ap.add_argument("--kernel", type=int, default=0)
 a = ap.parse_args()
 cfg = baseline_config(a.config, a.p)
 mat = wq.WQ_STIFFNESS if a.matrix == "stiffness" else wq.WQ_MASS
-plan = wq.Plan(cfg.p, cfg.knots(), need_mass=mat == wq.WQ_MASS, need_stiffness=mat == wq.WQ_STIFFNESS)
+plan = wq.Plan(cfg.p, cfg.knots(), ctrl=cfg.ctrl(), need_mass=mat == wq.WQ_MASS, need_stiffness=mat == wq.WQ_STIFFNESS)
 ctrl = torch.from_numpy(cfg.ctrl()).cuda()
 rp, col, val = plan.alloc_csr()
 for _ in range(a.steps):

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out/r2
+python tools/run_step.py --p 4 --steps 1 --kernel 4 && \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_zhp -c 1 -o gpurun_out/r2/zhp_p4 python tools/run_step.py --p 4 --steps 1 --kernel 4 > gpurun_out/r2/ncu_zhp.log 2>&1; tail -3 gpurun_out/r2/ncu_zhp.log

@@ -1,4 +1,4 @@
-"""Time the row-block kernels (CUDA events, L2 flushed) on BASELINE C4 degrees."""
+"""Time the row-block kernels (CUDA events, L2 flushed, median of reps) on BASELINE configs."""
 import argparse
 import json
 import os
@@ -8,23 +8,23 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_1605_01238_b200 as wq  # noqa: E402
-from wqinputs import baseline_config  # noqa: E402
+from wqinputs import Config, baseline_config  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--p", default="2,3,4")
-ap.add_argument("--kernels", default="2,3")
+ap.add_argument("--kernels", default="3,4")
 ap.add_argument("--matrix", default="stiffness")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--config", default="C4")
+ap.add_argument("--nel", type=int, default=0, help="override n_el (grid geometry)")
 a = ap.parse_args()
 mat = wq.WQ_STIFFNESS if a.matrix == "stiffness" else wq.WQ_MASS
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 for p in [int(x) for x in a.p.split(",")]:
-    cfg = baseline_config(a.config, p)
-    plan = wq.Plan(cfg.p, cfg.knots(), need_mass=mat == wq.WQ_MASS, need_stiffness=mat == wq.WQ_STIFFNESS)
-    ctrl = torch.from_numpy(cfg.ctrl()).cuda()
+    cfg = baseline_config(a.config, p) if not a.nel else Config(f"G{a.nel}p{p}", 3, p, a.nel, "grid", 0.1)
+    plan = wq.Plan(cfg.p, cfg.knots(), ctrl=cfg.ctrl(), need_mass=mat == wq.WQ_MASS,
+                   need_stiffness=mat == wq.WQ_STIFFNESS)
     rp, col, val = plan.alloc_csr()
-    plan.setup(ctrl)
     wq.wq_pattern(plan.h, 0, rp, None)
     ref = None
     for k in [int(x) for x in a.kernels.split(",")]:
@@ -32,7 +32,7 @@ for p in [int(x) for x in a.p.split(",")]:
             wq.wq_assemble(plan.h, mat, val, col, kernel=k)
             torch.cuda.synchronize()
         except wq.WQError as e:
-            print(json.dumps({"p": p, "kernel": k, "error": str(e)}))
+            print(json.dumps({"p": p, "kernel": k, "error": str(e)[:120]}))
             continue
         ts = []
         for _ in range(a.reps):
@@ -50,8 +50,9 @@ for p in [int(x) for x in a.p.split(",")]:
         diff = None if ref is None else float((v - ref).abs().max() / ref.abs().max())
         if ref is None:
             ref = v
-        print(json.dumps({"p": p, "kernel": k, "ms": ms, "nnz": nnz, "Gnnz_s": nnz / ms / 1e6,
-                          "GBs": 12 * nnz / ms / 1e6, "rel_diff_vs_first": diff}))
+        print(json.dumps({"cfg": cfg.name, "p": p, "mat": a.matrix, "kernel": wq.KERNEL_NAMES[k], "ms": round(ms, 3),
+                          "nnz": nnz, "Gnnz_s": round(nnz / ms / 1e6, 1), "GBs": round(12 * nnz / ms / 1e6, 1),
+                          "hbm_frac": round(12 * nnz / ms / 1e6 / 6552.6, 3), "rel_diff_vs_first": diff}), flush=True)
     plan.close()
     del rp, col, val
     torch.cuda.empty_cache()
