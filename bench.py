@@ -156,7 +156,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------- ours
-def run_ours(cfg, matrix, steps, warmup, rank, world, device, dist, want_e2e=True, sgq=False):
+def run_ours(cfg, matrix, steps, warmup, rank, world, device, dist, want_e2e=True, sgq=False, dump=None):
     """Time `steps` whole-path steps on this rank's slab; returns per-rank timings (max over ranks
     where it matters)."""
     import torch
@@ -176,8 +176,10 @@ def run_ours(cfg, matrix, steps, warmup, rank, world, device, dist, want_e2e=Tru
     d_ctrl = torch.from_numpy(ctrl).to(device)
     rp, col, val = plan.alloc_csr()
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=device)
-    nnz_all = torch.zeros(world, dtype=torch.int64, device=device)
-    my_nnz = torch.tensor([info["nnz_local"]], dtype=torch.int64, device=device)
+    # the exchange runs on the device with NCCL; gloo (CPU tests of the rank path) needs host tensors
+    xdev = "cpu" if dist is not None and dist.get_backend() == "gloo" else device
+    nnz_all = torch.zeros(world, dtype=torch.int64, device=xdev)
+    my_nnz = torch.tensor([info["nnz_local"]], dtype=torch.int64, device=xdev)
     ev_a0 = torch.cuda.Event(enable_timing=True)
     ev_a1 = torch.cuda.Event(enable_timing=True)
 
@@ -220,10 +222,14 @@ def run_ours(cfg, matrix, steps, warmup, rank, world, device, dist, want_e2e=Tru
             t_asm.append(ev_a0.elapsed_time(ev_a1) / 1e3)
     launches = wq.wq_launch_count() - launches0
     wq.wq_check(plan.h, stream)
+    if dump:  # rank's CSR block (tests of the multi-rank path)
+        os.makedirs(dump, exist_ok=True)
+        for nm, t in (("rp", rp), ("col", col), ("val", val)):
+            np.save(os.path.join(dump, f"rank{rank}_{nm}.npy"), t.cpu().numpy())
     t_total = sum(t_steps)
     t_asm_mean = sum(t_asm) / len(t_asm)
     if world > 1:
-        tt = torch.tensor([t_total, t_asm_mean], dtype=torch.float64, device=device)
+        tt = torch.tensor([t_total, t_asm_mean], dtype=torch.float64, device=xdev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_total, t_asm_mean = float(tt[0]), float(tt[1])
         dist.barrier()
@@ -256,7 +262,7 @@ def run_ours(cfg, matrix, steps, warmup, rank, world, device, dist, want_e2e=Tru
             e_t.append(e0.elapsed_time(e1) / 1e3)
         te = sum(e_t)
         if world > 1:
-            tt = torch.tensor([te], dtype=torch.float64, device=device)
+            tt = torch.tensor([te], dtype=torch.float64, device=xdev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt[0])
         res["e2e"] = dict(t=te / e2e_steps, steps=e2e_steps, h2d=int(hctrl.numel() * 8),
@@ -376,6 +382,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--oracle-seconds", type=float, default=20.0)
+    ap.add_argument("--n-el", type=int, default=0, help="override the config's elements per direction (tests)")
+    ap.add_argument("--dump-csr", default=None, help="directory: each rank saves its CSR block (tests)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -384,6 +392,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = config_of(args.config, args.p)
+    if args.n_el:
+        cfg = Config(f"{cfg.name}e{args.n_el}", cfg.d, cfg.p, args.n_el, cfg.geometry, cfg.amp, cfg.matrices)
     matrix = 0 if args.matrix == "mass" else 1
     workload = workload_name(cfg, matrix)
     config = {"workload": workload, "nnz": cfg.exact_nnz(), "n_dof": cfg.n_dof,
@@ -421,13 +431,18 @@ def main():
     import torch
     import paper_1605_01238_b200 as wq
     dist = None
+    device = local_rank % max(1, torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    device = local_rank
+        torch.cuda.set_device(device)
+        backend = os.environ.get("WQ_DIST_BACKEND", "nccl")  # gloo: CPU tests of the rank path
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(backend)
 
-    res = run_ours(cfg, matrix, args.steps, args.warmup, rank, world, device, dist, want_e2e=not args.no_e2e)
+    res = run_ours(cfg, matrix, args.steps, args.warmup, rank, world, device, dist, want_e2e=not args.no_e2e,
+                   dump=args.dump_csr)
     res["traffic_key"] = cfg.name + ("" if matrix == 1 else "_mass")
     hbm_peak, peak_src, peaks_doc = peaks()
     nnz = res["nnz"]

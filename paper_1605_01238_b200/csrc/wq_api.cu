@@ -413,8 +413,9 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     if (d == 3) {
         // lines of the ZHP kernel: interior in directions 1 and 2 (boxes of 2p+1 points), then the rest
         const int64_t n0 = P->dir[0].n, n1 = P->dir[1].n;
-        auto inter = [&](int l, int64_t i) {
-            return host_qhi(i, P->dir[l].E, p) - host_qlo(i, P->dir[l].E, p) + 1 == 2 * p + 1;
+        auto inter = [&](int l, int64_t i) {  // interior row type: touches no boundary span (R14)
+            return i >= p + 1 && i <= P->dir[l].n - p - 2 &&
+                   host_qhi(i, P->dir[l].E, p) - host_qlo(i, P->dir[l].E, p) + 1 == 2 * p + 1;
         };
         for (int64_t i1 = 0; i1 < n1; ++i1)
             for (int64_t i0 = 0; i0 < n0; ++i0)
@@ -437,15 +438,19 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     }
     // ---- which kernel WQ_KERNEL_AUTO runs
     if (!st) {
+        // measured on C4 (100^3 elements, BASELINE configs[3]): mass by the row-tile
+        // kernel except p = 6, 7 (ZHP faster), stiffness by the z-line kernel for p <= 6 and ZHP above
+        const bool zhp_m = zhp_supported(P, WQ_MASS) && (p == 6 || p == 7);
         P->kernel_auto[0] = !P->need_mass ? 0
                           : d < 3 ? WQ_KERNEL_DIRECT
-                          : zhp_supported(P, WQ_MASS) ? WQ_KERNEL_ZHP
-                          : tile_supported(P, WQ_MASS) ? WQ_KERNEL_TILE : WQ_KERNEL_DIRECT;
+                          : zhp_m ? WQ_KERNEL_ZHP
+                          : tile_supported(P, WQ_MASS) ? WQ_KERNEL_TILE
+                          : zhp_supported(P, WQ_MASS) ? WQ_KERNEL_ZHP : WQ_KERNEL_DIRECT;
         st = create_build(P);
         P->kernel_auto[1] = !P->need_stiff ? 0
                           : d < 3 ? WQ_KERNEL_DIRECT
                           : P->zline_ok ? WQ_KERNEL_ZLINE
-                          : zhp_supported(P, WQ_STIFFNESS) ? WQ_KERNEL_ZHP
+                          : zhp_supported(P, WQ_STIFFNESS) && (p >= 7 || !tile_supported(P, WQ_STIFFNESS)) ? WQ_KERNEL_ZHP
                           : tile_supported(P, WQ_STIFFNESS) ? WQ_KERNEL_TILE : WQ_KERNEL_DIRECT;
     }
     if (st) {

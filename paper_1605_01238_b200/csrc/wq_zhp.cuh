@@ -41,13 +41,13 @@
 namespace zhp {
 using namespace wqdev;
 
-constexpr int NPRO = 128;             // producer threads (stages A, B)
+constexpr int NPRO = 256;             // producer threads (stages A, B)
 constexpr int NCON = 256;             // consumer threads (stage C)
 constexpr int NT = NPRO + NCON;
 
 // column chunks of t_0 per degree (the G ring of a chunk, T (2p+1) x 4 doubles per point, and the
 // coefficient boxes must fit the SM's shared memory)
-__host__ __device__ constexpr int nch_of(int p) { return p <= 5 ? 1 : (p <= 7 ? 2 : (p <= 9 ? 3 : 5)); }
+__host__ __device__ constexpr int nch_of(int p) { return p <= 6 ? 1 : (p <= 7 ? 2 : (p <= 8 ? 3 : (p == 9 ? 5 : 7))); }
 template <int P>
 struct Chunks {
     static constexpr int K = 2 * P + 1, NCH = nch_of(P), T = (K + NCH - 1) / NCH;
@@ -99,7 +99,7 @@ __host__ __device__ inline Layout layout(int nb, int R, int ns, int64_t n2l) {
     Layout L;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 127) & ~(size_t)127; return r; };
-    L.bar = take(8 * 8);
+    L.bar = take(8 * 12);
     L.box = take(8 * (size_t)nb * CF::BOXD);
     L.y = take(8 * (size_t)R * CF::YPAIR);
     L.ring = take(8 * (size_t)ns * CF::SLOT);
@@ -129,29 +129,50 @@ __device__ __forceinline__ void groups(const int *off, int n, int *g, int tid) {
     }
 }
 
+// f(c, integral_constant<o>) for every point c of a row in order, o = staircase offset of c.
+// INT: an interior row (the 2P+1 points mid, knot, mid, .., with offsets (c+1)/2, P:537-542 and
+// Remark 1), fully unrolled with compile-time c; else the points of each offset group at run time.
+template <int P, bool INT, class F>
+__device__ __forceinline__ void staircase(const int *g, F &&f) {
+    if constexpr (INT) {
+        unroll<2 * P + 1>([&](auto C) {
+            constexpr int c = decltype(C)::value;
+            f(c, std::integral_constant<int, (c + 1) / 2>{});
+        });
+    } else {
+        unroll<P + 1>([&](auto O) {
+            constexpr int o = decltype(O)::value;
+            for (int c = g[o]; c < g[o + 1]; ++c) f(c, O);
+        });
+    }
+}
+
+// stage A of the pairs pp0 .. pp0 + nbat - 1 (box of pair pp in buffer pp % nb, Y of batch pair k)
 template <int P, bool MASS, int T, int QX, int CH>
-__device__ __forceinline__ void stage_a(const double *box, double *Y, const double2 *B0t, const double *W0t,
-                                        const double *W1t, const int *g0, int nq0, int nq1, int tid) {
+__device__ __forceinline__ void stage_a(const double *Boxes, int nb, int pp0, int nbat, double *Yall,
+                                        const double2 *B0t, const double *W0t, const double *W1t, const int *g0,
+                                        int nq0, int nq1, int tid) {
     using CF = Cfg<P, MASS, T, QX>;
     constexpr int TA = Chunks<P>::ta(CH), TN = Chunks<P>::tn(CH);  // t0 range of the chunk
     const int nfib = (MASS ? 1 : 3) * nq1 * 2;
-    for (int f = tid; f < nfib; f += NPRO) {
+    for (int fx = tid; fx < nbat * nfib; fx += NPRO) {
+        const int k = fx / nfib, f = fx % nfib;
+        const double *box = Boxes + ((pp0 + k) % nb) * CF::BOXD;
+        double *Y = Yall + k * CF::YPAIR;
         const int pt = f & 1, c1 = (f >> 1) % nq1, m = (f >> 1) / nq1;
         double y0[T], y1[T];
         #pragma unroll
         for (int t = 0; t < T; ++t) { y0[t] = 0.0; y1[t] = 0.0; }
         if constexpr (MASS) {
             const double w1 = W1t[c1 * 4 + 0];
-            unroll<CF::NP>([&](auto O) {
+            staircase<P, QX == 2 * P + 1>(g0, [&](int c0, auto O) {
                 constexpr int o = decltype(O)::value;
-                for (int c0 = g0[o]; c0 < g0[o + 1]; ++c0) {
-                    const double h = W0t[c0 * 4 + 0] * w1 * box[(c0 * QX + c1) * 2 + pt];
-                    const double2 *bp = B0t + c0 * CF::NP;
-                    #pragma unroll
-                    for (int r = 0; r <= P; ++r) {
-                        const int t = o + r - TA;
-                        if (t >= 0 && t < TN) y0[t] = fma(bp[r].x, h, y0[t]);
-                    }
+                const double h = W0t[c0 * 4 + 0] * w1 * box[(c0 * QX + c1) * 2 + pt];
+                const double2 *bp = B0t + c0 * CF::NP;
+                #pragma unroll
+                for (int r = 0; r <= P; ++r) {
+                    const int t = o + r - TA;
+                    if (t >= 0 && t < TN) y0[t] = fma(bp[r].x, h, y0[t]);
                 }
             });
             double *Yo = Y + ((pt * CF::NCHAIN + 0) * QX + c1) * T;
@@ -165,25 +186,23 @@ __device__ __forceinline__ void stage_a(const double *box, double *Y, const doub
             const double2 w1p = *(const double2 *)(W1t + c1 * 4 + (m == 1 ? 2 : 0));  // (w1^(0,b1), w1^(1,b1))
             const int w0o = m == 0 ? 2 : 0;
             const bool der0 = m == 0;
-            unroll<CF::NP>([&](auto O) {
+            staircase<P, QX == 2 * P + 1>(g0, [&](int c0, auto O) {
                 constexpr int o = decltype(O)::value;
-                for (int c0 = g0[o]; c0 < g0[o + 1]; ++c0) {
-                    const double2 w0p = *(const double2 *)(W0t + c0 * 4 + w0o);  // (w0^(0,b0), w0^(1,b0))
-                    const double s1 = w0p.x * w1p.x, s2 = w0p.y * w1p.x, s3 = w0p.x * w1p.y;
-                    const double ca = box[((ka * QX + c0) * QX + c1) * 2 + pt];
-                    const double cb = box[((kb * QX + c0) * QX + c1) * 2 + pt];
-                    const double cc = box[((kc * QX + c0) * QX + c1) * 2 + pt];
-                    const double h1 = s1 * ca;                  // a2 = 1 (l = 2)
-                    const double h0 = fma(s2, cb, s3 * cc);     // a2 = 0 (l = 0, 1)
-                    const double2 *bp = B0t + c0 * CF::NP;
-                    #pragma unroll
-                    for (int r = 0; r <= P; ++r) {
-                        const int t = o + r - TA;
-                        if (t >= 0 && t < TN) {
-                            const double bv = der0 ? bp[r].y : bp[r].x;
-                            y0[t] = fma(bv, h0, y0[t]);
-                            y1[t] = fma(bv, h1, y1[t]);
-                        }
+                const double2 w0p = *(const double2 *)(W0t + c0 * 4 + w0o);  // (w0^(0,b0), w0^(1,b0))
+                const double s1 = w0p.x * w1p.x, s2 = w0p.y * w1p.x, s3 = w0p.x * w1p.y;
+                const double ca = box[((ka * QX + c0) * QX + c1) * 2 + pt];
+                const double cb = box[((kb * QX + c0) * QX + c1) * 2 + pt];
+                const double cc = box[((kc * QX + c0) * QX + c1) * 2 + pt];
+                const double h1 = s1 * ca;                  // a2 = 1 (l = 2)
+                const double h0 = fma(s2, cb, s3 * cc);     // a2 = 0 (l = 0, 1)
+                const double2 *bp = B0t + c0 * CF::NP;
+                #pragma unroll
+                for (int r = 0; r <= P; ++r) {
+                    const int t = o + r - TA;
+                    if (t >= 0 && t < TN) {
+                        const double bv = der0 ? bp[r].y : bp[r].x;
+                        y0[t] = fma(bv, h0, y0[t]);
+                        y1[t] = fma(bv, h1, y1[t]);
                     }
                 }
             });
@@ -206,8 +225,8 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
     const int n2l = (int)a.n2l;
     const Layout Ly = layout<P, MASS, T, QX>(NB, R, NS, a.n2l);
     uint64_t *full = (uint64_t *)(smb + Ly.bar);  // [NB] box loads
-    uint64_t *ready = full + 4;                   // [2] step planes produced (count NPRO)
-    uint64_t *freeb = full + 6;                   // [2] step consumed (count NCON)
+    uint64_t *ready = full + 8;                   // [2] step planes produced (count NPRO)
+    uint64_t *freeb = full + 10;                  // [2] step consumed (count NCON)
     double *Box = (double *)(smb + Ly.box);
     double *Y = (double *)(smb + Ly.y);
     double *Ring = (double *)(smb + Ly.ring);
@@ -287,22 +306,25 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                 while (pairs_done < need) {
                     const int nbat = need - pairs_done < R ? need - pairs_done : R;
                     for (int k = 0; k < nbat; ++k) {
-                        const int pp = pairs_done + k, b = pp % NB;
+                        const int b = (pairs_done + k) % NB;
                         mbar_wait(&full[b], (use_bits >> b) & 1);
-                        const double *bx = Box + b * CF::BOXD;
-                        double *Yk = Y + k * CF::YPAIR;
-                        switch (ch) {
-                        case 0: stage_a<P, MASS, T, QX, 0>(bx, Yk, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
-                        case 1: if constexpr (NCH > 1) stage_a<P, MASS, T, QX, 1>(bx, Yk, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
-                        case 2: if constexpr (NCH > 2) stage_a<P, MASS, T, QX, 2>(bx, Yk, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
-                        case 3: if constexpr (NCH > 3) stage_a<P, MASS, T, QX, 3>(bx, Yk, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
-                        case 4: if constexpr (NCH > 4) stage_a<P, MASS, T, QX, 4>(bx, Yk, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
-                        default: break;
-                        }
-                        bar_sync(1, NPRO);  // box b consumed, Y_k written
+                    }
+                    switch (ch) {
+                    case 0: stage_a<P, MASS, T, QX, 0>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
+                    case 1: if constexpr (NCH > 1) stage_a<P, MASS, T, QX, 1>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
+                    case 2: if constexpr (NCH > 2) stage_a<P, MASS, T, QX, 2>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
+                    case 3: if constexpr (NCH > 3) stage_a<P, MASS, T, QX, 3>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
+                    case 4: if constexpr (NCH > 4) stage_a<P, MASS, T, QX, 4>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
+                    case 5: if constexpr (NCH > 5) stage_a<P, MASS, T, QX, 5>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
+                    case 6: if constexpr (NCH > 6) stage_a<P, MASS, T, QX, 6>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
+                    default: break;
+                    }
+                    bar_sync(1, NPRO);  // the batch's boxes consumed, Y written
+                    for (int k = 0; k < nbat; ++k) {
+                        const int pp = pairs_done + k, b = pp % NB;
                         use_bits ^= 1u << b;
                         if (ptid == 0 && pp + NB < npairs) {
-                            fence_async_smem();
+                            if (k == 0) fence_async_smem();
                             mbar_arrive_tx(&full[b], BOX_BYTES);
                             tma_load_4d(Box + b * CF::BOXD, &tm, &full[b], (int)a.qoff + 2 * (pp + NB), ql1, ql0, 0);
                         }
@@ -318,14 +340,12 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                         #pragma unroll
                         for (int t = 0; t < K; ++t) acc[t] = 0.0;
                         if constexpr (MASS) {
-                            unroll<NP>([&](auto O) {
+                            staircase<P, QX == 2 * P + 1>(g1, [&](int c1, auto O) {
                                 constexpr int o = decltype(O)::value;
-                                for (int c1 = g1[o]; c1 < g1[o + 1]; ++c1) {
-                                    const double yv = Yk[c1 * T + tl];
-                                    const double2 *bp = B1t + c1 * NP;
-                                    #pragma unroll
-                                    for (int r = 0; r <= P; ++r) acc[o + r] = fma(bp[r].x, yv, acc[o + r]);
-                                }
+                                const double yv = Yk[c1 * T + tl];
+                                const double2 *bp = B1t + c1 * NP;
+                                #pragma unroll
+                                for (int r = 0; r <= P; ++r) acc[o + r] = fma(bp[r].x, yv, acc[o + r]);
                             });
                         } else {
                             // g = a2 + 2 b2: b2 = 0 sums chains m = 0 (B1 values) and m = 1 (B1
@@ -333,15 +353,13 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                             const int a2 = g & 1, b2 = g >> 1;
                             const double *Ya = Yk + ((b2 ? 4 : 0) + a2) * QX * T;
                             const double *Yb = Yk + (2 + a2) * QX * T;
-                            unroll<NP>([&](auto O) {
+                            staircase<P, QX == 2 * P + 1>(g1, [&](int c1, auto O) {
                                 constexpr int o = decltype(O)::value;
-                                for (int c1 = g1[o]; c1 < g1[o + 1]; ++c1) {
-                                    const double ya = Ya[c1 * T + tl];
-                                    const double yb = b2 ? 0.0 : Yb[c1 * T + tl];
-                                    const double2 *bp = B1t + c1 * NP;
-                                    #pragma unroll
-                                    for (int r = 0; r <= P; ++r) acc[o + r] = fma(bp[r].y, yb, fma(bp[r].x, ya, acc[o + r]));
-                                }
+                                const double ya = Ya[c1 * T + tl];
+                                const double yb = b2 ? 0.0 : Yb[c1 * T + tl];
+                                const double2 *bp = B1t + c1 * NP;
+                                #pragma unroll
+                                for (int r = 0; r <= P; ++r) acc[o + r] = fma(bp[r].y, yb, fma(bp[r].x, ya, acc[o + r]));
                             });
                         }
                         double *G = Ring + (size_t)(q % NS) * CF::SLOT;
@@ -393,8 +411,15 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                 while (c < n && v2.span[cqb + q0 + c] - j < o) ++c;
                 g2p[rho * (NP + 1) + o] = o == NP ? n : c;
             }
+            bool all_int = true;
+            for (int rho = 0; rho < nr; ++rho) {
+                const int i2 = i2b + r0 + rho;
+                all_int = all_int && i2 >= P + 1 && i2 <= (int)v2.n - P - 2 && qlen2[r0 + rho] == 2 * P + 1;
+            }
             bar_sync(2, NCON);
             mbar_wait(&ready[par], (gs >> 1) & 1);  // acquire: the step's planes
+            auto stage_c = [&](auto IC) {
+                constexpr bool INTC = decltype(IC)::value;
             for (int x = ctid; x < nr * COLS; x += NCON) {
                 const int rho = x / COLS, cl = x % COLS;
                 const int tl = cl % T, t1 = cl / T, tg = ta + tl;
@@ -405,9 +430,9 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                 double acc[K];
                 #pragma unroll
                 for (int t = 0; t < K; ++t) acc[t] = 0.0;
-                unroll<NP>([&](auto O) {
+                staircase<P, INTC>(gg, [&](int c, auto O) {
                     constexpr int o = decltype(O)::value;
-                    for (int c = gg[o]; c < gg[o + 1]; ++c) {
+                    {
                         const int s = (q0 + c) % NS;
                         const double2 *bp = RB2 + s * NP;
                         if constexpr (MASS) {
@@ -439,6 +464,9 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                     }
                 }
             }
+            };
+            if (all_int) stage_c(std::true_type{});
+            else stage_c(std::false_type{});
             mbar_arrive(&freeb[par]);  // this step's ring slots may be overwritten
         }
     }
@@ -495,14 +523,15 @@ template <int P, bool MASS, int QX>
 bool choose(const Plan2 &g, int &nb, int &R, int &ns, size_t &smem, int optin) {
     constexpr int T = Chunks<P>::T;
     using CF = Cfg<P, MASS, T, QX>;
-    // rows per step: as many as one pass of the consumer threads covers (stage C items = rows x COLS)
+    // rows per step: as many as one pass of the consumer threads covers (stage C items = rows x COLS);
+    // box buffers: a batch of R pairs (stage A runs over the whole batch), doubled for prefetch
     int rbest = NCON / CF::COLS;
-    rbest = rbest < 1 ? 1 : (rbest > 8 ? 8 : rbest);
+    rbest = rbest < 1 ? 1 : (rbest > 6 ? 6 : rbest);
     if (getenv("WQ_ZHP_R")) rbest = atoi(getenv("WQ_ZHP_R"));
     const int nb_env = getenv("WQ_ZHP_NB") ? atoi(getenv("WQ_ZHP_NB")) : 0;
     for (int r = rbest; r >= 1; --r)
-        for (int b = 3; b >= 1; --b) {
-            if (nb_env && b != nb_env) continue;
+        for (int b = 2 * r; b >= r; --b) {
+            if (b > 8 || (nb_env && b != nb_env)) continue;
             const int n = ring_slots(g, r);
             const Layout L = layout<P, MASS, T, QX>(b, r, n, g.n2l);
             if (L.total <= (size_t)optin) {

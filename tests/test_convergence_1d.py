@@ -14,7 +14,8 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("p", [1, 2, 3, 4])
 def test_optimal_rates(p):
     import convergence_1d as cv
-    rows = cv.study([p], [8, 16, 32, 64])
+    # the finest meshes stop short of the FP64 floor of the errors (~1e-12 at h^{p+1})
+    rows = cv.study([p], [8, 16, 32, 64] if p <= 2 else [4, 8, 16, 32])
     for method in ("wq", "sgq"):
         last = [r for r in rows if r["method"] == method][-1]
         assert last["rate_l2"] >= p + 1 - 0.3, (method, last)
