@@ -475,6 +475,7 @@ wq_status wq_plan_destroy(wq_plan P) {
     if (P->kappa_dev) cudaFree(P->kappa_dev);
     if (P->gamma_dev) cudaFree(P->gamma_dev);
     if (P->dnet) cudaFree(P->dnet);
+    if (P->x2) cudaFree(P->x2);
     if (P->stage_val) cudaFree(P->stage_val);
     delete P;
     return WQ_OK;

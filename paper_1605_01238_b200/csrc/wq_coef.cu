@@ -168,16 +168,6 @@ __global__ void __launch_bounds__(NTC) k_coef(CoefArgs a) {
     if (a.need_m) a.coef[(int64_t)a.comp_mass * a.cs + pt] = gam * ad;
 }
 
-// d = 3 (z layout): the same sum factorisation with the roles of the directions permuted so that the
-// fast thread index runs along q_3, the contiguous axis of [comp][q_1][q_2][q_3], while stage A
-// still reads the control net along its contiguous k_1:
-// CTA = TQF q_3 points x TQM q_1 points of one q_2 plane;
-//   stage A contracts k_2 (plane):   A0 = N2 . Q^1, A1 = M2 . Q^2, A2 = N2 . Q^3, Ak = N2 . kappa, ...
-//   stage B contracts k_1:           X0 = M1 . A0,  X1 = N1 . A1,  X2 = N1 . A2,  Xk = N1 . Ak
-//   stage C contracts k_3 per point: J[:,0] = N3 . X0, J[:,1] = N3 . X1, J[:,2] = M3 . X2,
-//                                    kappa = N3 . Xk, gamma likewise
-constexpr int TQF = 32;
-
 // derivative control nets (d = 3): Q^m_k = (P_k - P_{k - e_m}) p / (xi_{k_m + p} - xi_{k_m}) for k_m >= 1,
 // else 0, then the coefficient nets: [k][NE], NE = 9 + NNU, entries (m, c) = 3 m + c, 9 = kappa,
 // 9 or 10 = gamma; one thread per control point of the planes k_3 in [k3b, k3b + ntot / (n0 n1)).
@@ -205,6 +195,13 @@ __global__ void k_dnet(const double *__restrict__ P, const double *__restrict__ 
     if (NNU > 0 && kap) q[e++] = kap[k];
     if (NNU > 0 && gam) q[e++] = gam[k];
 }
+// Tiled form (p <= 6): CTA = TQF points q_3 x TQM points q_1 of one q_2 plane, the three
+// contractions of the tile in one kernel:
+//   stage A contracts k_2 (plane):   A0 = N2 . Q^1, A1 = M2 . Q^2, A2 = N2 . Q^3, Ak = N2 . kappa, ...
+//   stage B contracts k_1:           X0 = M1 . A0,  X1 = N1 . A1,  X2 = N1 . A2,  Xk = N1 . Ak
+//   stage C contracts k_3 per point: J[:,0] = N3 . X0, J[:,1] = N3 . X1, J[:,2] = M3 . X2,
+//                                    kappa = N3 . Xk, gamma likewise
+constexpr int TQF = 32;
 // PP > 0: the degree as a compile-time constant (p <= 6), so that the r loops unroll and each thread
 // issues all of its derivative-net loads of stage A before the first FMA (the kernel is bound by
 // their L2 latency); PP = 0: any degree.  NNU: number of coefficient nets (0..2).
@@ -352,6 +349,151 @@ __global__ void __launch_bounds__(TQF * TQM, TQM == 16 ? 3 : 1) k_coefz(CoefArgs
     if (a.need_m) a.coef[(int64_t)a.comp_mass * a.cs + pt] = gam * ad;
 }
 
+// Streaming form of the d = 3 sum factorisation (3 passes over the whole sub-grid, each a 1D
+// contraction with coalesced access; the degree is a compile-time constant PP):
+//   k_dnet  derivative control nets Q^m (+ coefficient nets), [k][NE]
+//   k_cz12  X2[k_3][q_1][q_0][e] = sum_{k_1} T1_e(q_1, k_1) sum_{k_0} T0_e(q_0, k_0) Q[k_3][k_1][k_0][e]
+//           (thread = column (q_0, e) of one control plane k_3, marching along q_1 with the p+1 rows
+//           k_1 of the current span in a sliding register window)
+//   k_cz3   J_e(q) = sum_{k_3} T2_e(q_2, k_3) X2[k_3][q_1][q_0][e] per point, then det J, adj J,
+//           c and C; CTA = 32 points q_2 (the contiguous axis of the z layout) x 8 points q_0 of
+//           one q_1 row, the X2 rows of the tile's k_3 window staged in shared memory.
+// T_e is the degree p-1 table M (functions span+1..span+p) in the entry's derivative direction
+// and the degree p table N (functions span..span+p) elsewhere.
+template <int PP, int NNU>
+__global__ void __launch_bounds__(256) k_cz12(CoefArgs a, double *__restrict__ X2, int64_t n2l) {
+    constexpr int NE = 9 + NNU, p = PP;
+    const DirView &v0 = a.v[0], &v1 = a.v[1];
+    const int64_t nq0 = v0.nq, nq1 = v1.nq, n0 = v0.n, n1 = v1.n;
+    const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t k2l = blockIdx.y;
+    if (col >= nq0 * NE) return;
+    const int q0 = (int)(col / NE), e = (int)(col % NE);
+    const bool m0 = e < 3, m1 = e >= 3 && e < 6;  // derivative in direction 0 / 1
+    // direction-0 table of this column (registers): N values or M values
+    double t0[PP + 1];
+    const int64_t s0 = v0.span[q0];
+    {
+        const double *nt = Ntab(v0, p, q0), *mt = Mtab(v0, p, q0);
+        #pragma unroll
+        for (int r = 0; r <= PP; ++r) t0[r] = m0 ? (r < PP ? mt[r] : 0.0) : nt[2 * r];
+    }
+    const int64_t kb0 = s0 + (m0 ? 1 : 0);  // first k_0 of the contraction
+    const double *Qp = a.dnet + (k2l * n1 * n0) * NE + e;
+    auto x1row = [&](int64_t k1) {  // sum_{k_0} T0 Q[k_3][k_1][k_0][e]
+        double s = 0.0;
+        const double *q = Qp + (k1 * n0 + kb0) * NE;
+        #pragma unroll
+        for (int r = 0; r <= PP; ++r)
+            if (!m0 || r < PP) s = fma(t0[r], __ldg(q + r * NE), s);
+        return s;
+    };
+    double win[PP + 1];
+    int64_t cur = v1.span[0];
+    #pragma unroll
+    for (int r = 0; r <= PP; ++r) win[r] = x1row(cur + r);
+    double *out = X2 + (k2l * nq1 * nq0 + q0) * NE + e;
+    for (int64_t q1 = 0; q1 < nq1; ++q1) {
+        const int64_t s1 = v1.span[q1];
+        while (cur < s1) {  // slide the window by one control row
+            #pragma unroll
+            for (int r = 0; r < PP; ++r) win[r] = win[r + 1];
+            ++cur;
+            win[PP] = x1row(cur + PP);
+        }
+        const double *nt = Ntab(v1, p, q1), *mt = Mtab(v1, p, q1);
+        double s = 0.0;
+        #pragma unroll
+        for (int r = 0; r <= PP; ++r) {
+            if (m1) { if (r < PP) s = fma(mt[r], win[r + 1], s); }
+            else s = fma(nt[2 * r], win[r], s);
+        }
+        out[q1 * nq0 * NE] = s;
+    }
+}
+
+constexpr int CZ_T2 = 32, CZ_T0 = 8;
+// shared row stride of k_cz3 (doubles): CZ_T0 * NE + 1, so that the lanes' different rows k_3 fall on
+// different banks
+__host__ __device__ constexpr int cz_rs(int ne) { return CZ_T0 * ne + 1; }
+
+template <int PP, int NNU>
+__global__ void __launch_bounds__(CZ_T2 * CZ_T0) k_cz3(CoefArgs a, const double *__restrict__ X2) {
+    constexpr int NE = 9 + NNU, p = PP;
+    extern __shared__ __align__(16) double sm[];
+    const DirView &v0 = a.v[0], &v1 = a.v[1], &v2 = a.v[2];
+    const int64_t nq0 = v0.nq, nq1 = v1.nq, nql = a.nq_loc_d;
+    const int64_t q2a = (int64_t)blockIdx.x * CZ_T2, q0a = (int64_t)blockIdx.y * CZ_T0, q1 = blockIdx.z;
+    const int64_t q2e = q2a + CZ_T2 < nql ? q2a + CZ_T2 : nql, q0e = q0a + CZ_T0 < nq0 ? q0a + CZ_T0 : nq0;
+    const int64_t cqb = a.cq_b;
+    const int64_t kfa = v2.span[cqb + q2a], kfe = v2.span[cqb + q2e - 1] + p + 1;
+    const int KF = (int)(kfe - kfa), n0t = (int)(q0e - q0a);
+    const int tid = threadIdx.x;
+    // stage the rows k_3 in [kfa, kfe) of X2 for this q_1 and the tile's q_0 (contiguous (q_0, e) runs)
+    const int rowlen = n0t * NE;
+    for (int x = tid; x < KF * rowlen; x += blockDim.x) {
+        const int kr = x / rowlen, j = x % rowlen;
+        sm[kr * cz_rs(NE) + j] = __ldg(X2 + (((kfa - a.k3b + kr) * nq1 + q1) * nq0 + q0a) * NE + j);
+    }
+    __syncthreads();
+    const int t2 = tid % CZ_T2, t0 = tid / CZ_T2;
+    const int64_t q2l = q2a + t2, q0 = q0a + t0;
+    if (q2l >= q2e || q0 >= q0e) return;
+    const double *nt = Ntab(v2, p, cqb + q2l), *mt = Mtab(v2, p, cqb + q2l);
+    const int ks = (int)(v2.span[cqb + q2l] - kfa);
+    double J[3][3], nu[2] = {0.0, 0.0};
+    #pragma unroll
+    for (int c = 0; c < 3; ++c)
+        #pragma unroll
+        for (int m = 0; m < 3; ++m) J[c][m] = 0.0;
+    const double *S = sm + t0 * NE;
+    #pragma unroll
+    for (int r = 0; r <= PP; ++r) {
+        const double nv = nt[2 * r], mv = r < PP ? mt[r] : 0.0;
+        const double *Sr = S + (ks + r) * cz_rs(NE), *Sm = Sr + cz_rs(NE);  // M: functions span+1..
+        #pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            J[c][0] = fma(nv, Sr[0 * 3 + c], J[c][0]);
+            J[c][1] = fma(nv, Sr[1 * 3 + c], J[c][1]);
+            if (r < PP) J[c][2] = fma(mv, Sm[2 * 3 + c], J[c][2]);
+        }
+        #pragma unroll
+        for (int u = 0; u < NNU; ++u) nu[u] = fma(nv, Sr[9 + u], nu[u]);
+    }
+    const double kap = a.kappa ? nu[0] : 1.0;
+    const double gam = a.gamma ? nu[a.kappa ? 1 : 0] : 1.0;
+    double adj[3][3];
+    adj[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    adj[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+    adj[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+    adj[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    adj[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+    adj[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+    adj[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    adj[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+    adj[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    const double det = J[0][0] * adj[0][0] + J[0][1] * adj[1][0] + J[0][2] * adj[2][0];
+    if (!(det > 0.0) && !(det < 0.0)) atomicOr(&a.flags->det_zero, 1);
+    else if (det > 0.0) { if (!a.flags->det_pos) atomicOr(&a.flags->det_pos, 1); }
+    else { if (!a.flags->det_neg) atomicOr(&a.flags->det_neg, 1); }
+    const double ad = fabs(det), inv = kap / ad;
+    const int64_t pt = (q0 * nq1 + q1) * a.zld + q2l;
+    if (a.need_s) {
+        int comp = 0;
+        #pragma unroll
+        for (int l = 0; l < 3; ++l)
+            #pragma unroll
+            for (int m = l; m < 3; ++m) {
+                double sv = 0.0;
+                #pragma unroll
+                for (int k = 0; k < 3; ++k) sv = fma(adj[l][k], adj[m][k], sv);
+                a.coef[(int64_t)comp * a.cs + pt] = sv * inv;
+                ++comp;
+            }
+    }
+    if (a.need_m) a.coef[(int64_t)a.comp_mass * a.cs + pt] = gam * ad;
+}
+
 }  // namespace
 
 wq_status launch_coef(wq_plan_s *P, const double *ctrl, const double *kappa, const double *gamma, cudaStream_t s) {
@@ -418,24 +560,70 @@ wq_status launch_coef(wq_plan_s *P, const double *ctrl, const double *kappa, con
         else k_dnet<2><<<gd, 256, 0, s>>>(ctrl, kappa, gamma, P->dnet, P->dir[0], P->dir[1], P->dir[2], P->p, k3b, ntot);
         wq_count_launches(1);
         a.dnet = P->dnet;
-        constexpr int TQM = 16;
+        // measured at C4 (tools/time_step.py): the tiled kernel for p <= 4, the streaming passes above
+        const bool tiled = P->p >= 2 && P->p <= 4 && !getenv("WQ_COEF_STREAM");
+        if (tiled) {
+            constexpr int TQM = 16;
+            auto runt = [&](auto PPc, auto NUc) {
+                constexpr int PP = decltype(PPc)::value, NNU = decltype(NUc)::value;
+                const size_t ne = 9 + NNU;
+                const size_t na = ne * (TQM + P->p + 1) * (TQF + P->p + 1), nx = (size_t)TQM * ne * (TQF + P->p + 1);
+                const size_t sm = (na > nx ? na : nx) * sizeof(double);
+                wq_smem_attr((const void *)k_coefz<TQM, PP, NNU>, sm);
+                dim3 g((unsigned)((a.nq_loc_d + TQF - 1) / TQF), (unsigned)((P->dir[0].nq + TQM - 1) / TQM), (unsigned)P->dir[1].nq);
+                k_coefz<TQM, PP, NNU><<<g, TQF * TQM, sm, s>>>(a);
+            };
+            auto runt_p = [&](auto NUc) {
+                switch (P->p) {
+                case 2: runt(std::integral_constant<int, 2>{}, NUc); break;
+                case 3: runt(std::integral_constant<int, 3>{}, NUc); break;
+                default: runt(std::integral_constant<int, 4>{}, NUc); break;
+                }
+            };
+            if (nnu == 0) runt_p(std::integral_constant<int, 0>{});
+            else if (nnu == 1) runt_p(std::integral_constant<int, 1>{});
+            else runt_p(std::integral_constant<int, 2>{});
+            wq_count_launches(1);
+            return wq_cuda_status(cudaGetLastError(), "coefficient kernel");
+        }
+        // X2 workspace: the slab's control planes x nq_1 x nq_0 x NE
+        const int64_t n2l = k3e - k3b;
+        const int ne = 9 + nnu;
+        const size_t xb = sizeof(double) * (size_t)n2l * P->dir[1].nq * P->dir[0].nq * ne;
+        if (P->x2_bytes < xb) {
+            if (P->x2) cudaFree(P->x2);
+            P->x2_bytes = xb;
+            if (cudaMalloc((void **)&P->x2, xb) != cudaSuccess) {
+                P->x2 = nullptr;
+                P->x2_bytes = 0;
+                wq_set_error("coefficient workspace allocation failed");
+                return WQ_ENOMEM;
+            }
+        }
         auto run = [&](auto PPc, auto NUc) {
             constexpr int PP = decltype(PPc)::value, NNU = decltype(NUc)::value;
-            const size_t ne = 9 + NNU;
-            const size_t na = ne * (TQM + P->p + 1) * (TQF + P->p + 1), nx = (size_t)TQM * ne * (TQF + P->p + 1);
-            const size_t sm = (na > nx ? na : nx) * sizeof(double);
-            wq_smem_attr((const void *)k_coefz<TQM, PP, NNU>, sm);
-            dim3 g((unsigned)((a.nq_loc_d + TQF - 1) / TQF), (unsigned)((P->dir[0].nq + TQM - 1) / TQM), (unsigned)P->dir[1].nq);
-            k_coefz<TQM, PP, NNU><<<g, TQF * TQM, sm, s>>>(a);
+            dim3 g1((unsigned)((P->dir[0].nq * (9 + NNU) + 255) / 256), (unsigned)n2l);
+            k_cz12<PP, NNU><<<g1, 256, 0, s>>>(a, P->x2, n2l);
+            const int kfmax = CZ_T2 + PP + 1;
+            const size_t sm = sizeof(double) * (size_t)kfmax * cz_rs(9 + NNU);
+            dim3 g3((unsigned)((a.nq_loc_d + CZ_T2 - 1) / CZ_T2), (unsigned)((P->dir[0].nq + CZ_T0 - 1) / CZ_T0),
+                    (unsigned)P->dir[1].nq);
+            wq_smem_attr((const void *)k_cz3<PP, NNU>, sm);
+            k_cz3<PP, NNU><<<g3, CZ_T2 * CZ_T0, sm, s>>>(a, P->x2);
+            wq_count_launches(1);
         };
         auto run_p = [&](auto NUc) {
             switch (P->p) {
+            case 1: run(std::integral_constant<int, 1>{}, NUc); break;
             case 2: run(std::integral_constant<int, 2>{}, NUc); break;
             case 3: run(std::integral_constant<int, 3>{}, NUc); break;
             case 4: run(std::integral_constant<int, 4>{}, NUc); break;
             case 5: run(std::integral_constant<int, 5>{}, NUc); break;
             case 6: run(std::integral_constant<int, 6>{}, NUc); break;
-            default: run(std::integral_constant<int, 0>{}, NUc); break;
+            case 7: run(std::integral_constant<int, 7>{}, NUc); break;
+            case 8: run(std::integral_constant<int, 8>{}, NUc); break;
+            case 9: run(std::integral_constant<int, 9>{}, NUc); break;
+            default: run(std::integral_constant<int, 10>{}, NUc); break;
             }
         };
         if (nnu == 0) run_p(std::integral_constant<int, 0>{});

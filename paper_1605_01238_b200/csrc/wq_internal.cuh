@@ -80,6 +80,8 @@ struct wq_plan_s {
     double *ctrl_dev;              // device copies of the control net and coefficient nets (create,
     double *kappa_dev, *gamma_dev; // wq_form_host staging); kappa/gamma null = 1
     size_t ctrl_bytes;
+    double *x2;                    // d = 3: coefficient-field workspace (k_cz12 -> k_cz3)
+    size_t x2_bytes;
     double *dnet;                  // d = 3: derivative control nets (+ coefficient nets) of the slab's
     size_t dnet_bytes;             // control planes k_3 in [k3b, k3e): [k][NE] (k_dnet)
     int64_t k3b, k3e;
