@@ -438,9 +438,10 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     }
     // ---- which kernel WQ_KERNEL_AUTO runs
     if (!st) {
-        // measured on C4 (100^3 elements, BASELINE configs[3]): mass by the row-tile
-        // kernel except p = 6, 7 (ZHP faster), stiffness by the z-line kernel for p <= 6 and ZHP above
-        const bool zhp_m = zhp_supported(P, WQ_MASS) && (p == 6 || p == 7);
+        // measured on C4 (100^3 elements, BASELINE configs[3]): mass by ZHP for
+        // 4 <= p <= 7 and the row-tile kernel otherwise, stiffness by the z-line kernel for p <= 6
+        // and ZHP above
+        const bool zhp_m = zhp_supported(P, WQ_MASS) && p >= 4 && p <= 7;
         P->kernel_auto[0] = !P->need_mass ? 0
                           : d < 3 ? WQ_KERNEL_DIRECT
                           : zhp_m ? WQ_KERNEL_ZHP

@@ -69,6 +69,7 @@ struct Cfg {
     static constexpr int YPAIR = 2 * NCHAIN * QX * T;  // doubles of Y per pair [pt][chain][c1][t0]
     static constexpr int SLOT = COLS * NGF;       // doubles of a G ring slot [col][family]
     static constexpr int QR = 3 * P + 1;          // max #Q of a row (n_EL >= p+2)
+    static constexpr int CPT = 2 * P + 1 <= 17 ? 2 : 1;  // stage-C columns per consumer thread
 };
 
 struct Args {
@@ -87,6 +88,7 @@ struct Args {
     double *val;
     int32_t *col;
     int64_t val_base;
+    int cl;                  // launched as clusters of the NCH chunk CTAs of a line (lockstep per step)
 };
 
 // shared-memory carve-up (byte offsets), identical on host and device
@@ -119,6 +121,10 @@ __host__ __device__ inline Layout layout(int nb, int R, int ns, int64_t n2l) {
     return L;
 }
 
+// split cluster barrier: keeps the chunk CTAs of a line (one cluster) within a step of each other
+__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+
 // group bounds of a point range: g[o] = first point c with off[c] >= o, o = 0..NP (g[NP] = n)
 template <int NP>
 __device__ __forceinline__ void groups(const int *off, int n, int *g, int tid) {
@@ -147,37 +153,48 @@ __device__ __forceinline__ void staircase(const int *g, F &&f) {
     }
 }
 
-// stage A of the pairs pp0 .. pp0 + nbat - 1 (box of pair pp in buffer pp % nb, Y of batch pair k)
+// stage A of the pairs pp0 .. pp0 + nbat - 1 (box of pair pp in buffer pp % nb, Y of batch pair k);
+// a thread = fibre (m, c1) of one pair, both points (the box holds the pair's points side by side, so
+// one 16-B load serves both and the tables are loaded once per two points)
 template <int P, bool MASS, int T, int QX, int CH>
 __device__ __forceinline__ void stage_a(const double *Boxes, int nb, int pp0, int nbat, double *Yall,
                                         const double2 *B0t, const double *W0t, const double *W1t, const int *g0,
                                         int nq0, int nq1, int tid) {
     using CF = Cfg<P, MASS, T, QX>;
     constexpr int TA = Chunks<P>::ta(CH), TN = Chunks<P>::tn(CH);  // t0 range of the chunk
-    const int nfib = (MASS ? 1 : 3) * nq1 * 2;
+    const int nfib = (MASS ? 1 : 3) * nq1;
     for (int fx = tid; fx < nbat * nfib; fx += NPRO) {
         const int k = fx / nfib, f = fx % nfib;
         const double *box = Boxes + ((pp0 + k) % nb) * CF::BOXD;
         double *Y = Yall + k * CF::YPAIR;
-        const int pt = f & 1, c1 = (f >> 1) % nq1, m = (f >> 1) / nq1;
-        double y0[T], y1[T];
+        const int c1 = f % nq1, m = f / nq1;
+        double y0[2][T], y1[2][T];
         #pragma unroll
-        for (int t = 0; t < T; ++t) { y0[t] = 0.0; y1[t] = 0.0; }
+        for (int t = 0; t < T; ++t) { y0[0][t] = 0.0; y0[1][t] = 0.0; y1[0][t] = 0.0; y1[1][t] = 0.0; }
         if constexpr (MASS) {
             const double w1 = W1t[c1 * 4 + 0];
             staircase<P, QX == 2 * P + 1>(g0, [&](int c0, auto O) {
                 constexpr int o = decltype(O)::value;
-                const double h = W0t[c0 * 4 + 0] * w1 * box[(c0 * QX + c1) * 2 + pt];
+                const double2 cv = *(const double2 *)(box + (c0 * QX + c1) * 2);
+                const double s = W0t[c0 * 4 + 0] * w1;
+                const double ha = s * cv.x, hb = s * cv.y;
                 const double2 *bp = B0t + c0 * CF::NP;
                 #pragma unroll
                 for (int r = 0; r <= P; ++r) {
                     const int t = o + r - TA;
-                    if (t >= 0 && t < TN) y0[t] = fma(bp[r].x, h, y0[t]);
+                    if (t >= 0 && t < TN) {
+                        const double bv = bp[r].x;
+                        y0[0][t] = fma(bv, ha, y0[0][t]);
+                        y0[1][t] = fma(bv, hb, y0[1][t]);
+                    }
                 }
             });
-            double *Yo = Y + ((pt * CF::NCHAIN + 0) * QX + c1) * T;
             #pragma unroll
-            for (int t = 0; t < T; ++t) Yo[t] = y0[t];
+            for (int pt = 0; pt < 2; ++pt) {
+                double *Yo = Y + ((pt * CF::NCHAIN + 0) * QX + c1) * T;
+                #pragma unroll
+                for (int t = 0; t < T; ++t) Yo[t] = y0[pt][t];
+            }
         } else {
             // components C00 C01 C02 C11 C12 C22: ka = C_2m, kb = C_0m, kc = C_1m
             const int ka = m == 0 ? 2 : (m == 1 ? 4 : 5);
@@ -190,26 +207,31 @@ __device__ __forceinline__ void stage_a(const double *Boxes, int nb, int pp0, in
                 constexpr int o = decltype(O)::value;
                 const double2 w0p = *(const double2 *)(W0t + c0 * 4 + w0o);  // (w0^(0,b0), w0^(1,b0))
                 const double s1 = w0p.x * w1p.x, s2 = w0p.y * w1p.x, s3 = w0p.x * w1p.y;
-                const double ca = box[((ka * QX + c0) * QX + c1) * 2 + pt];
-                const double cb = box[((kb * QX + c0) * QX + c1) * 2 + pt];
-                const double cc = box[((kc * QX + c0) * QX + c1) * 2 + pt];
-                const double h1 = s1 * ca;                  // a2 = 1 (l = 2)
-                const double h0 = fma(s2, cb, s3 * cc);     // a2 = 0 (l = 0, 1)
+                const double2 ca = *(const double2 *)(box + ((ka * QX + c0) * QX + c1) * 2);
+                const double2 cb = *(const double2 *)(box + ((kb * QX + c0) * QX + c1) * 2);
+                const double2 cc = *(const double2 *)(box + ((kc * QX + c0) * QX + c1) * 2);
+                const double h1a = s1 * ca.x, h1b = s1 * ca.y;                                // a2 = 1 (l = 2)
+                const double h0a = fma(s2, cb.x, s3 * cc.x), h0b = fma(s2, cb.y, s3 * cc.y);  // a2 = 0 (l = 0, 1)
                 const double2 *bp = B0t + c0 * CF::NP;
                 #pragma unroll
                 for (int r = 0; r <= P; ++r) {
                     const int t = o + r - TA;
                     if (t >= 0 && t < TN) {
                         const double bv = der0 ? bp[r].y : bp[r].x;
-                        y0[t] = fma(bv, h0, y0[t]);
-                        y1[t] = fma(bv, h1, y1[t]);
+                        y0[0][t] = fma(bv, h0a, y0[0][t]);
+                        y0[1][t] = fma(bv, h0b, y0[1][t]);
+                        y1[0][t] = fma(bv, h1a, y1[0][t]);
+                        y1[1][t] = fma(bv, h1b, y1[1][t]);
                     }
                 }
             });
-            double *Y0 = Y + ((pt * CF::NCHAIN + m * 2 + 0) * QX + c1) * T;
-            double *Y1 = Y + ((pt * CF::NCHAIN + m * 2 + 1) * QX + c1) * T;
             #pragma unroll
-            for (int t = 0; t < T; ++t) { Y0[t] = y0[t]; Y1[t] = y1[t]; }
+            for (int pt = 0; pt < 2; ++pt) {
+                double *Y0 = Y + ((pt * CF::NCHAIN + m * 2 + 0) * QX + c1) * T;
+                double *Y1 = Y + ((pt * CF::NCHAIN + m * 2 + 1) * QX + c1) * T;
+                #pragma unroll
+                for (int t = 0; t < T; ++t) { Y0[t] = y0[pt][t]; Y1[t] = y1[pt][t]; }
+            }
         }
     }
 }
@@ -256,7 +278,14 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
     const int q_end = qlo2[n2l - 1] + qlen2[n2l - 1];  // local end of the last row's Q
     const int npairs = (q_end + 1) / 2;
     const int nsteps = (n2l + R - 1) / R;
-    const int64_t n_items = a.n_lines * NCH;
+    int narr = 0;  // cluster-barrier arrivals of this thread (NCH > 1: one per step)
+    auto step_sync = [&]() {
+        if (NCH > 1 && a.cl) {
+            if (narr > 0) cl_wait();
+            cl_arrive();
+            ++narr;
+        }
+    };
     constexpr unsigned BOX_BYTES = CF::NC * QX * QX * 2 * 8;
 
     if (tid < NPRO) {
@@ -264,9 +293,9 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
         const int ptid = tid;
         unsigned use_bits = 0;  // phase parity of each box buffer's next use (bit b)
         int64_t gs = 0;         // global step counter (shared sequence with the consumers)
-        for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-            const int line = a.lines[it / NCH];
-            const int ch = (int)(it % NCH);
+        for (int64_t li = blockIdx.x / NCH; li < a.n_lines; li += gridDim.x / NCH) {
+            const int line = a.lines[li];
+            const int ch = (int)(blockIdx.x % NCH);  // the CTA's rank in its cluster (NCH > 1)
             const int i0 = (int)(line % a.n0), i1 = (int)(line / a.n0);
             const int ql0 = v0.qlo[i0], nq0 = v0.qlen[i0], jl0 = v0.jlo[i0];
             const int ql1 = v1.qlo[i1], nq1 = v1.qlen[i1], jl1 = v1.jlo[i1];
@@ -375,16 +404,18 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                     pairs_done += nbat;
                 }
                 mbar_arrive(&ready[gs & 1]);  // release: this step's planes are in the ring
+                step_sync();
             }
         }
+        if (NCH > 1 && a.cl && narr > 0) cl_wait();
         return;
     }
     // ==================================================================== consumers
     const int ctid = tid - NPRO;
     int64_t gs = 0;
-    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int line = a.lines[it / NCH];
-        const int ch = (int)(it % NCH);
+    for (int64_t li = blockIdx.x / NCH; li < a.n_lines; li += gridDim.x / NCH) {
+        const int line = a.lines[li];
+        const int ch = (int)(blockIdx.x % NCH);
         const int i0 = (int)(line % a.n0), i1 = (int)(line / a.n0);
         const int jl0 = v0.jlo[i0], ni0 = v0.jlen[i0];
         const int jl1 = v1.jlo[i1], ni1 = v1.jlen[i1];
@@ -418,58 +449,88 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
             }
             bar_sync(2, NCON);
             mbar_wait(&ready[par], (gs >> 1) & 1);  // acquire: the step's planes
+            // stage C: CPT adjacent columns per thread (the row's point weights and basis pairs are
+            // loaded once for them)
             auto stage_c = [&](auto IC) {
                 constexpr bool INTC = decltype(IC)::value;
-            for (int x = ctid; x < nr * COLS; x += NCON) {
-                const int rho = x / COLS, cl = x % COLS;
-                const int tl = cl % T, t1 = cl / T, tg = ta + tl;
-                const int rr = r0 + rho;
-                const int q0 = qlo2[rr];
-                const double *Wr = W2p + rho * CF::QR * 4;
-                const int *gg = g2p + rho * (NP + 1);
-                double acc[K];
-                #pragma unroll
-                for (int t = 0; t < K; ++t) acc[t] = 0.0;
-                staircase<P, INTC>(gg, [&](int c, auto O) {
-                    constexpr int o = decltype(O)::value;
-                    {
+                constexpr int CPT = CF::CPT, NCP = (COLS + CPT - 1) / CPT;
+                for (int x = ctid; x < nr * NCP; x += NCON) {
+                    const int rho = x / NCP, cl0 = (x % NCP) * CPT;
+                    const int rr = r0 + rho;
+                    const int q0 = qlo2[rr];
+                    const double *Wr = W2p + rho * CF::QR * 4;
+                    const int *gg = g2p + rho * (NP + 1);
+                    int clc[CPT];
+                    #pragma unroll
+                    for (int j = 0; j < CPT; ++j) clc[j] = cl0 + j < COLS ? cl0 + j : COLS - 1;
+                    double acc[CPT][K];
+                    #pragma unroll
+                    for (int j = 0; j < CPT; ++j)
+                        #pragma unroll
+                        for (int t = 0; t < K; ++t) acc[j][t] = 0.0;
+                    staircase<P, INTC>(gg, [&](int c, auto O) {
+                        constexpr int o = decltype(O)::value;
                         const int s = (q0 + c) % NS;
                         const double2 *bp = RB2 + s * NP;
+                        const double *Gs = Ring + (size_t)s * CF::SLOT;
                         if constexpr (MASS) {
-                            const double u = Wr[c * 4] * Ring[(size_t)s * CF::SLOT + cl];
+                            const double wv = Wr[c * 4];
+                            double uu[CPT];
                             #pragma unroll
-                            for (int r = 0; r <= P; ++r) acc[o + r] = fma(bp[r].x, u, acc[o + r]);
+                            for (int j = 0; j < CPT; ++j) uu[j] = wv * Gs[clc[j]];
+                            #pragma unroll
+                            for (int r = 0; r <= P; ++r) {
+                                const double bx = bp[r].x;
+                                #pragma unroll
+                                for (int j = 0; j < CPT; ++j) acc[j][o + r] = fma(bx, uu[j], acc[j][o + r]);
+                            }
                         } else {
-                            const double4 G = *(const double4 *)(Ring + (size_t)s * CF::SLOT + cl * 4);
                             const double4 w = *(const double4 *)(Wr + c * 4);
-                            const double u0 = fma(w.x, G.x, w.y * G.y), u1 = fma(w.z, G.z, w.w * G.w);
+                            double u0[CPT], u1[CPT];
                             #pragma unroll
-                            for (int r = 0; r <= P; ++r) acc[o + r] = fma(bp[r].y, u1, fma(bp[r].x, u0, acc[o + r]));
+                            for (int j = 0; j < CPT; ++j) {
+                                const double4 G = *(const double4 *)(Gs + clc[j] * 4);
+                                u0[j] = fma(w.x, G.x, w.y * G.y);
+                                u1[j] = fma(w.z, G.z, w.w * G.w);
+                            }
+                            #pragma unroll
+                            for (int r = 0; r <= P; ++r) {
+                                const double2 b2 = bp[r];
+                                #pragma unroll
+                                for (int j = 0; j < CPT; ++j) acc[j][o + r] = fma(b2.y, u1[j], fma(b2.x, u0[j], acc[j][o + r]));
+                            }
                         }
-                    }
-                });
-                if (tl < tn && tg < ni0 && t1 < ni1) {
+                    });
                     const int ni2 = jlen2[rr];
                     const int64_t row = pref2[rr] * a.L1 * a.L0 + (int64_t)ni2 * (p1L0 + p0n1) - a.val_base;
-                    const int64_t e0 = row + tg + (int64_t)ni0 * t1, stp = (int64_t)ni0 * ni1;
+                    const int64_t stp = (int64_t)ni0 * ni1;
                     #pragma unroll
-                    for (int t = 0; t < K; ++t)
-                        if (t < ni2) a.val[e0 + stp * t] = acc[t];
-                    if (a.col) {
-                        const int jb = (jl0 + tg) + (int)a.n0 * ((jl1 + t1) + (int)a.n1 * jlo2[rr]);
-                        const int js = (int)(a.n0 * a.n1);
-                        #pragma unroll
-                        for (int t = 0; t < K; ++t)
-                            if (t < ni2) a.col[e0 + stp * t] = jb + js * t;
+                    for (int j = 0; j < CPT; ++j) {
+                        const int cl = cl0 + j;
+                        const int tl = cl % T, t1 = cl / T, tg = ta + tl;
+                        if (cl < COLS && tl < tn && tg < ni0 && t1 < ni1) {
+                            const int64_t e0 = row + tg + (int64_t)ni0 * t1;
+                            #pragma unroll
+                            for (int t = 0; t < K; ++t)
+                                if (t < ni2) a.val[e0 + stp * t] = acc[j][t];
+                            if (a.col) {
+                                const int jb = (jl0 + tg) + (int)a.n0 * ((jl1 + t1) + (int)a.n1 * jlo2[rr]);
+                                const int js = (int)(a.n0 * a.n1);
+                                #pragma unroll
+                                for (int t = 0; t < K; ++t)
+                                    if (t < ni2) a.col[e0 + stp * t] = jb + js * t;
+                            }
+                        }
                     }
                 }
-            }
             };
             if (all_int) stage_c(std::true_type{});
             else stage_c(std::false_type{});
             mbar_arrive(&freeb[par]);  // this step's ring slots may be overwritten
+            step_sync();
         }
     }
+    if (NCH > 1 && a.cl && narr > 0) cl_wait();
 }
 
 }  // namespace zhp
@@ -525,7 +586,7 @@ bool choose(const Plan2 &g, int &nb, int &R, int &ns, size_t &smem, int optin) {
     using CF = Cfg<P, MASS, T, QX>;
     // rows per step: as many as one pass of the consumer threads covers (stage C items = rows x COLS);
     // box buffers: a batch of R pairs (stage A runs over the whole batch), doubled for prefetch
-    int rbest = NCON / CF::COLS;
+    int rbest = NCON / ((CF::COLS + CF::CPT - 1) / CF::CPT);
     rbest = rbest < 1 ? 1 : (rbest > 6 ? 6 : rbest);
     if (getenv("WQ_ZHP_R")) rbest = atoi(getenv("WQ_ZHP_R"));
     const int nb_env = getenv("WQ_ZHP_NB") ? atoi(getenv("WQ_ZHP_NB")) : 0;
@@ -594,14 +655,29 @@ wq_status launch_cls(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, const
         wq_set_error("cuTensorMapEncodeTiled failed for the coefficient field");
         return WQ_ECUDA;
     }
-    const int64_t items = n_lines * NCH;
-    int per_sm = 1;
-    if (getenv("WQ_ZHP_CTAS")) per_sm = atoi(getenv("WQ_ZHP_CTAS"));
-    const int64_t grid = std::min<int64_t>(items, (int64_t)nsm * per_sm);
+    // one cluster of NCH CTAs per line (the chunks of a line side by side, kept within a step of each
+    // other so that their interleaved partial-sector stores merge in L2)
+    const int64_t nclusters = std::max<int64_t>(1, std::min<int64_t>(n_lines, nsm / NCH));
     cudaError_t ce = wq_smem_attr((const void *)k_zhp<P, MASS, T, QX>, smem);
     if (ce != cudaSuccess) return wq_cuda_status(ce, "ZHP smem attribute");
-    k_zhp<P, MASS, T, QX><<<(unsigned)grid, NT, smem, s>>>(m, a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nclusters * NCH));
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = NCH;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    // measured: lockstep clusters pay with two chunks (C4 p = 7 mass 42.9 -> 34.6 ms) and cost with
+    // three or more (p = 8 stiffness 155 -> 298 ms)
+    a.cl = NCH == 2 && !getenv("WQ_ZHP_NOCLUSTER");
+    cfg.numAttrs = a.cl ? 1 : 0;
+    ce = cudaLaunchKernelEx(&cfg, k_zhp<P, MASS, T, QX>, m, a);
     wq_count_launches(1);
+    if (ce != cudaSuccess) return wq_cuda_status(ce, "ZHP assembly kernel");
     return wq_cuda_status(cudaGetLastError(), "ZHP assembly kernel");
 }
 
