@@ -447,11 +447,29 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
                           : zhp_m ? WQ_KERNEL_ZHP
                           : tile_supported(P, WQ_MASS) ? WQ_KERNEL_TILE
                           : zhp_supported(P, WQ_MASS) ? WQ_KERNEL_ZHP : WQ_KERNEL_DIRECT;
-        st = create_build(P);
+        if (d == 3 && P->need_stiff && !P->zline_ok && !(zhp_supported(P, WQ_STIFFNESS) && p >= 7 && p <= 9) &&
+            tile_supported(P, WQ_STIFFNESS)) {
+            // the row-tile stiffness reads a standard-layout copy (made after every coefficient build;
+            // measured at C4 p = 10: 574 -> 407 ms; its mass path is faster on the z layout)
+            const size_t sb = sizeof(double) * (size_t)P->ncomp * (size_t)cp;
+            ce = cudaMalloc((void **)&P->coef_std, sb);
+            if (ce != cudaSuccess) { P->coef_std = nullptr; st = fail(WQ_ENOMEM, "standard-layout coefficient copy"); }
+            else {
+                cbytes += sb;
+                P->cview_std.base = P->coef_std;
+                P->cview_std.cs = cp;
+                P->cview_std.s1 = 1;
+                P->cview_std.s2 = P->dir[0].nq;
+                P->cview_std.s3 = P->dir[0].nq * P->dir[1].nq;
+            }
+        }
+        if (!st) st = create_build(P);
+        // stiffness: ZHP for p = 7..9, the row-tile kernel on the standard-layout copy at p = 10
         P->kernel_auto[1] = !P->need_stiff ? 0
                           : d < 3 ? WQ_KERNEL_DIRECT
                           : P->zline_ok ? WQ_KERNEL_ZLINE
-                          : zhp_supported(P, WQ_STIFFNESS) && (p >= 7 || !tile_supported(P, WQ_STIFFNESS)) ? WQ_KERNEL_ZHP
+                          : zhp_supported(P, WQ_STIFFNESS) && ((p >= 7 && p <= 9) || !tile_supported(P, WQ_STIFFNESS))
+                              ? WQ_KERNEL_ZHP
                           : tile_supported(P, WQ_STIFFNESS) ? WQ_KERNEL_TILE : WQ_KERNEL_DIRECT;
     }
     if (st) {
@@ -470,6 +488,7 @@ wq_status wq_plan_destroy(wq_plan P) {
     cudaSetDevice(P->device);
     if (P->arena) cudaFree(P->arena);
     if (P->coef) cudaFree(P->coef);
+    if (P->coef_std) cudaFree(P->coef_std);
     if (P->zlines_dev) cudaFree(P->zlines_dev);
     if (P->zh_dev) cudaFree(P->zh_dev);
     if (P->ctrl_dev) cudaFree(P->ctrl_dev);

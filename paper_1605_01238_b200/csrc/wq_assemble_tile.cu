@@ -499,7 +499,7 @@ wq_status launch_tile_p(wq_plan_s *Pl, double *val, int32_t *col, int64_t pl_lo,
     TileArgs a;
     a.g.init(Pl);
     for (int l = 0; l < 3; ++l) a.v[l] = Pl->dir[l];
-    a.cv = Pl->cview;
+    a.cv = STIFF && Pl->coef_std ? Pl->cview_std : Pl->cview;  // stiffness: standard-layout copy if the plan keeps one
     a.cq_b = Pl->cq_b;
     a.comp_mass = Pl->comp_mass;
     a.val = val;

@@ -494,7 +494,36 @@ __global__ void __launch_bounds__(CZ_T2 * CZ_T0) k_cz3(CoefArgs a, const double 
     if (a.need_m) a.coef[(int64_t)a.comp_mass * a.cs + pt] = gam * ad;
 }
 
+// z layout [comp][q_1][q_2][q_3 - cq_b] -> standard layout [comp][q_3 - cq_b][q_2][q_1] (row-tile kernel):
+// 32 x 32 tiles of (q_1, q_3) for one (comp, q_2), transposed through shared memory
+__global__ void __launch_bounds__(256) k_z2std(const double *__restrict__ z, double *__restrict__ st, int64_t nq0,
+                                               int64_t nq1, int64_t nql, int64_t zld, int64_t zcs, int64_t scs) {
+    __shared__ double tile[32][33];
+    const int64_t q3a = (int64_t)blockIdx.x * 32, q0a = (int64_t)blockIdx.y * 32;
+    const int64_t q1 = blockIdx.z % nq1, comp = blockIdx.z / nq1;
+    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+    for (int r = ty; r < 32; r += 8) {  // read rows q_0, contiguous along q_3
+        const int64_t q0 = q0a + r, q3 = q3a + tx;
+        tile[r][tx] = (q0 < nq0 && q3 < nql) ? z[comp * zcs + (q0 * nq1 + q1) * zld + q3] : 0.0;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {  // write rows q_3, contiguous along q_0
+        const int64_t q3 = q3a + r, q0 = q0a + tx;
+        if (q0 < nq0 && q3 < nql) st[comp * scs + (q3 * nq1 + q1) * nq0 + q0] = tile[tx][r];
+    }
+}
+
 }  // namespace
+
+static wq_status finish_coef(wq_plan_s *P, cudaStream_t s) {
+    if (P->d == 3 && P->coef_std) {
+        const int64_t nql = P->cq_e - P->cq_b, nq0 = P->dir[0].nq, nq1 = P->dir[1].nq;
+        dim3 g((unsigned)((nql + 31) / 32), (unsigned)((nq0 + 31) / 32), (unsigned)(nq1 * P->ncomp));
+        k_z2std<<<g, 256, 0, s>>>(P->coef, P->coef_std, nq0, nq1, nql, P->zld, P->zcs, P->coef_points);
+        wq_count_launches(1);
+    }
+    return wq_cuda_status(cudaGetLastError(), "coefficient kernel");
+}
 
 wq_status launch_coef(wq_plan_s *P, const double *ctrl, const double *kappa, const double *gamma, cudaStream_t s) {
     CoefArgs a;
@@ -584,7 +613,7 @@ wq_status launch_coef(wq_plan_s *P, const double *ctrl, const double *kappa, con
             else if (nnu == 1) runt_p(std::integral_constant<int, 1>{});
             else runt_p(std::integral_constant<int, 2>{});
             wq_count_launches(1);
-            return wq_cuda_status(cudaGetLastError(), "coefficient kernel");
+            return finish_coef(P, s);
         }
         // X2 workspace: the slab's control planes x nq_1 x nq_0 x NE
         const int64_t n2l = k3e - k3b;
@@ -638,5 +667,5 @@ wq_status launch_coef(wq_plan_s *P, const double *ctrl, const double *kappa, con
         k_coef<1><<<g, NTC, 0, s>>>(a);
     }
     wq_count_launches(1);
-    return wq_cuda_status(cudaGetLastError(), "coefficient kernel");
+    return finish_coef(P, s);
 }

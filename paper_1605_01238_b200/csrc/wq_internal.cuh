@@ -71,6 +71,9 @@ struct wq_plan_s {
     int64_t zld, zcs;              // d = 3: row length along q_3 (even), doubles per component
     int64_t nld1;                  // d <= 2: leading dimension (nq_1)
     CoefView cview;                // device view of coef
+    double *coef_std;              // d = 3: copy of the field in the standard layout [comp][q_3][q_2][q_1]
+    CoefView cview_std;            // (q_1 contiguous, coalesced fibre loads of the row-tile kernel), made
+                                   // by launch_coef when AUTO runs the row-tile kernel for a matrix
     int has_coef;                  // a coefficient field has been built (create or wq_build_coef)
     // Gauss-Legendre rule on [-1,1] in double-double: [p+1] (hi, lo) pairs
     double *gl;                    // [2*(p+1)] t, [2*(p+1)] w
