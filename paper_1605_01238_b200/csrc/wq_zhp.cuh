@@ -393,7 +393,13 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                         }
                         double *G = Ring + (size_t)(q % NS) * CF::SLOT;
                         #pragma unroll
-                        for (int t = 0; t < K; ++t) G[(tl + T * t) * NGF + g] = acc[t];
+                        for (int t = 0; t < K; ++t) {
+                            // ring slot [b2][column][a2] (stage C loads (a2 = 0, 1) pairs with a 16-B
+                            // lane stride: conflict-free)
+                            const int cl = tl + T * t;
+                            if constexpr (MASS) G[cl] = acc[t];
+                            else G[((g >> 1) * COLS + cl) * 2 + (g & 1)] = acc[t];
+                        }
                     }
                     for (int x = ptid; x < nbat * 2 * NP; x += NPRO) {
                         const int q = 2 * pairs_done + x / NP, r = x % NP;
@@ -455,14 +461,14 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                 constexpr bool INTC = decltype(IC)::value;
                 constexpr int CPT = CF::CPT, NCP = (COLS + CPT - 1) / CPT;
                 for (int x = ctid; x < nr * NCP; x += NCON) {
-                    const int rho = x / NCP, cl0 = (x % NCP) * CPT;
+                    const int rho = x / NCP, cl0 = x % NCP;  // columns cl0 + j NCP (consecutive lanes, consecutive columns)
                     const int rr = r0 + rho;
                     const int q0 = qlo2[rr];
                     const double *Wr = W2p + rho * CF::QR * 4;
                     const int *gg = g2p + rho * (NP + 1);
                     int clc[CPT];
                     #pragma unroll
-                    for (int j = 0; j < CPT; ++j) clc[j] = cl0 + j < COLS ? cl0 + j : COLS - 1;
+                    for (int j = 0; j < CPT; ++j) clc[j] = cl0 + j * NCP < COLS ? cl0 + j * NCP : COLS - 1;
                     double acc[CPT][K];
                     #pragma unroll
                     for (int j = 0; j < CPT; ++j)
@@ -489,9 +495,10 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                             double u0[CPT], u1[CPT];
                             #pragma unroll
                             for (int j = 0; j < CPT; ++j) {
-                                const double4 G = *(const double4 *)(Gs + clc[j] * 4);
-                                u0[j] = fma(w.x, G.x, w.y * G.y);
-                                u1[j] = fma(w.z, G.z, w.w * G.w);
+                                const double2 Ga = *(const double2 *)(Gs + clc[j] * 2);               // b2 = 0: a2 = 0, 1
+                                const double2 Gb = *(const double2 *)(Gs + (COLS + clc[j]) * 2);      // b2 = 1
+                                u0[j] = fma(w.x, Ga.x, w.y * Ga.y);
+                                u1[j] = fma(w.z, Gb.x, w.w * Gb.y);
                             }
                             #pragma unroll
                             for (int r = 0; r <= P; ++r) {
@@ -506,7 +513,7 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                     const int64_t stp = (int64_t)ni0 * ni1;
                     #pragma unroll
                     for (int j = 0; j < CPT; ++j) {
-                        const int cl = cl0 + j;
+                        const int cl = cl0 + j * NCP;
                         const int tl = cl % T, t1 = cl / T, tg = ta + tl;
                         if (cl < COLS && tl < tn && tg < ni0 && t1 < ni1) {
                             const int64_t e0 = row + tg + (int64_t)ni0 * t1;
