@@ -205,11 +205,12 @@ constexpr int TQF = 32;
 // PP > 0: the degree as a compile-time constant (p <= 6), so that the r loops unroll and each thread
 // issues all of its derivative-net loads of stage A before the first FMA (the kernel is bound by
 // their L2 latency); PP = 0: any degree.  NNU: number of coefficient nets (0..2).
-template <int TQM, int PP, int NNU>
-__global__ void __launch_bounds__(TQF * TQM, TQM == 16 ? 3 : 1) k_coefz(CoefArgs a) {
+template <int TQM, int PP, int NNU, int MINB>
+__global__ void __launch_bounds__(TQF * TQM, MINB) k_coefz(CoefArgs a) {
     constexpr int NE = 9 + NNU;
     extern __shared__ __align__(16) double sm[];
-    const int p = PP > 0 ? PP : a.p;
+    static_assert(PP > 0, "compile-time degree");
+    const int p = PP;
     const DirView &v0 = a.v[0], &v1 = a.v[1], &v2 = a.v[2];
     const int64_t q1p = blockIdx.z;  // plane (direction 2)
     const int64_t qfa = (int64_t)blockIdx.x * TQF, qma = (int64_t)blockIdx.y * TQM;  // q_3 local, q_1
@@ -220,99 +221,112 @@ __global__ void __launch_bounds__(TQF * TQM, TQM == 16 ? 3 : 1) k_coefz(CoefArgs
     const int64_t kfa = v2.span[cqb + qfa], kfe = v2.span[cqb + qfe - 1] + p + 1;
     const int64_t kma = v0.span[qma], kme = v0.span[qme - 1] + p + 1;
     const int KF = (int)(kfe - kfa), KM = (int)(kme - kma);
-    const int KFM = TQF + p + 1, KMM = TQM + p + 1;
-    double *Asm = sm;                      // [NE entries][KFM][KMM]  (k_1 fastest)
-    double *Xsm = sm;                      // [TQM][NE][KFM], over Asm once stage B has read it
+    // k windows of the tile: 32 (16) consecutive points lie in at most 17 (9) spans (two points per
+    // interior span, reading R1), so KF <= TQF/2 + 1 + p and KM <= TQM/2 + 1 + p
+    constexpr int KFM = TQF / 2 + 2 + PP, KMM = TQM / 2 + 2 + PP;
+    if (KF > KFM || KM > KMM) __trap();  // point-layout invariant
+    constexpr int NEP = (NE + 1) & ~1;     // X row: the NE entries padded to whole double2 pairs
+    constexpr int BS = wq_bstride(PP), BSP = BS + 1;  // table rows, padded to an odd stride in smem
+    double *Asm = sm;                                   // [NE entries][KFM][KMM]  (k_1 fastest)
+    double *Xsm = Asm + ((NE * KFM * KMM + 1) & ~1);    // [TQM][KFM][NEP]
+    double *T2s = Xsm + TQM * KFM * NEP;                // [TQF][BSP] basis rows of the tile's q_3 points
+    double *T0s = T2s + TQF * BSP;                      // [TQM][BSP] basis rows of the tile's q_1 points
     const int tid = threadIdx.x;
     const int64_t n0 = v0.n, n1 = v1.n;
+    for (int x = tid; x < ntf * BS; x += blockDim.x) T2s[(x / BS) * BSP + x % BS] = v2.B[(cqb + qfa) * BS + x];
+    for (int x = tid; x < ntm * BS; x += blockDim.x) T0s[(x / BS) * BSP + x % BS] = v0.B[qma * BS + x];
     {
-        // stage A: contract k_2 with the plane's basis.  Threads over (k_3, e) with e = (k_1 - kma)*NE +
-        // entry: for fixed (k_2, k_3) the net entries of the tile's k_1 range are one contiguous run, so
-        // consecutive threads load consecutive doubles (coalesced); every entry is an independent sum
-        // over k_2 (derivative in direction 2 (entries 3..5) with M2, all others with N2)
+        // stage A: contract k_2 with the plane's basis.  Thread = one fixed column e = (k_1 - kma)*NE +
+        // entry of the tile and a row group g, looping over the rows k_3 = g, g + G, ...: for fixed
+        // (k_2, k_3) the net entries of the tile's k_1 range are one contiguous run, so consecutive
+        // threads load consecutive doubles (coalesced); the column's weights sit in registers and the
+        // loop only advances two pointers (derivative in direction 2 (entries 3..5) with M2, all others
+        // with N2; the M2 column's weight 0 is paired with the valid row span, so every lane loads)
         const double *nt = Ntab(v1, p, q1p), *mt = Mtab(v1, p, q1p);
         const int64_t e1 = v1.span[q1p];
-        const double *Q = a.dnet;
-        const int KE = KM * NE;
-        for (int t = tid; t < KF * KE; t += blockDim.x) {
-            const int cf = t / KE, e = t % KE;
-            const int cm = e / NE, vc = e % NE;
+        const int KE = KM * NE, G = (int)blockDim.x / KE;
+        const int g = tid / KE, e = tid - g * KE;
+        if (g < G) {
+            const int cm = e / NE, vc = e - cm * NE;
             const bool dv = vc >= 3 && vc < 6;
-            const double *Qe = Q + (kma + n0 * (e1 + n1 * (kfa - a.k3b + cf))) * NE + e;
-            double acc = 0.0;
+            double w[PP + 1];
             #pragma unroll
-            for (int r = 0; r <= p; ++r) {
-                const double w = dv ? (r >= 1 ? mt[r - 1] : 0.0) : nt[2 * r];
-                if (!dv || r >= 1) acc = fma(w, __ldg(Qe + r * n0 * NE), acc);
+            for (int r = 0; r <= PP; ++r) w[r] = dv ? (r >= 1 ? mt[r - 1] : 0.0) : nt[2 * r];
+            const int64_t rs = n0 * NE, ps = n0 * n1 * NE * G;
+            const double *Qe = a.dnet + (kma + n0 * (e1 + n1 * (kfa - a.k3b + g))) * NE + e;
+            double *As = Asm + (vc * KFM + g) * KMM + cm;
+            #pragma unroll 2
+            for (int cf = g; cf < KF; cf += G, Qe += ps, As += G * KMM) {
+                double acc = 0.0;
+                #pragma unroll
+                for (int r = 0; r <= PP; ++r) acc = fma(w[r], __ldg(Qe + r * rs), acc);
+                *As = acc;
             }
-            Asm[(vc * KFM + cf) * KMM + cm] = acc;
         }
     }
     __syncthreads();
-    // stage B: contract k_1 for each q_1 point of the tile.  A thread's (at most XIT) items are held in
-    // registers until every thread has read Asm, then X is written over it (smem per CTA = max of
-    // the two arrays instead of their sum: one more CTA per SM)
-    constexpr int XIT = 2;  // ceil((TQF + p + 1) / TQF) items per thread for p < TQF
-    double Xr[XIT][NE];
-    #pragma unroll
-    for (int it = 0; it < XIT; ++it) {
-        const int t = tid + it * (int)blockDim.x;
-        if (t >= ntm * KF) break;
-        const int tm = t / KF, cf = t % KF;
-        const int64_t q0 = qma + tm;
-        const double *nt = Ntab(v0, p, q0), *mt = Mtab(v0, p, q0);
-        const int cms = (int)(v0.span[q0] - kma);
-        double X[NE];
+    // stage B: contract k_1 for each q_1 point of the tile (items (q_1, k_3), k_3 fastest)
+    for (int t = tid; t < ntm * KF; t += blockDim.x) {
+        const int tm = t / KF, cf = t - tm * KF;
+        const double *nt = T0s + tm * BSP, *mt = nt + 2 * (PP + 1);
+        const int cms = (int)(v0.span[qma + tm] - kma);
+        double X[NEP];
         #pragma unroll
-        for (int vc = 0; vc < NE; ++vc) X[vc] = 0.0;
+        for (int vc = 0; vc < NEP; ++vc) X[vc] = 0.0;
         #pragma unroll
-        for (int r = 0; r <= p; ++r) {
-            const double nv = nt[2 * r], mv = r < p ? mt[r] : 0.0;
+        for (int r = 0; r <= PP; ++r) {
+            const double nv = nt[2 * r], mv = r < PP ? mt[r] : 0.0;
             #pragma unroll
             for (int vc = 0; vc < NE; ++vc) {
                 if (vc < 3) {  // derivative in direction 1: M1
-                    if (r < p) X[vc] = fma(mv, Asm[(vc * KFM + cf) * KMM + cms + 1 + r], X[vc]);
+                    if (r < PP) X[vc] = fma(mv, Asm[(vc * KFM + cf) * KMM + cms + 1 + r], X[vc]);
                 } else {
                     X[vc] = fma(nv, Asm[(vc * KFM + cf) * KMM + cms + r], X[vc]);
                 }
             }
         }
+        double2 *xr = (double2 *)(Xsm + (tm * KFM + cf) * NEP);
         #pragma unroll
-        for (int vc = 0; vc < NE; ++vc) Xr[it][vc] = X[vc];
-    }
-    __syncthreads();
-    #pragma unroll
-    for (int it = 0; it < XIT; ++it) {
-        const int t = tid + it * (int)blockDim.x;
-        if (t >= ntm * KF) break;
-        const int tm = t / KF, cf = t % KF;
-        #pragma unroll
-        for (int vc = 0; vc < NE; ++vc) Xsm[(tm * NE + vc) * KFM + cf] = Xr[it][vc];
+        for (int h = 0; h < NEP / 2; ++h) xr[h] = make_double2(X[2 * h], X[2 * h + 1]);
     }
     __syncthreads();
     // stage C: one thread per point (q_3 fastest)
     const int tf = tid % TQF, tm = tid / TQF;
     if (tf >= ntf || tm >= ntm) return;
     const int64_t q2l = qfa + tf, q0 = qma + tm;
-    const double *nt = Ntab(v2, p, cqb + q2l), *mt = Mtab(v2, p, cqb + q2l);
+    const double *nt = T2s + tf * BSP, *mt = nt + 2 * (PP + 1);
     const int cfs = (int)(v2.span[cqb + q2l] - kfa);
     double J[3][3], nu[2] = {0.0, 0.0};
     #pragma unroll
     for (int c = 0; c < 3; ++c)
         #pragma unroll
         for (int m = 0; m < 3; ++m) J[c][m] = 0.0;
-    const double *X = Xsm + (tm * NE) * KFM;
+    // rows r' = 0..p of the point's k_3 window, each read once as NEP/2 double2 (rows at an 80/96-B
+    // stride: the 4 distinct rows of a quarter-warp fall on disjoint banks): entries 0..5 and the
+    // coefficient nets with N3 (row r'), entries 6..8 with M3 (functions span+1.., row r' >= 1)
+    const double2 *X = (const double2 *)(Xsm + (tm * KFM + cfs) * NEP);
     #pragma unroll
-    for (int r = 0; r <= p; ++r) {
-        const double nv = nt[2 * r], mv = r < p ? mt[r] : 0.0;
+    for (int r = 0; r <= PP; ++r) {
+        double x[NEP];
+        #pragma unroll
+        for (int h = 0; h < NEP / 2; ++h) {
+            const double2 v = X[r * (NEP / 2) + h];
+            x[2 * h] = v.x;
+            x[2 * h + 1] = v.y;
+        }
+        const double nv = nt[2 * r];
         #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            J[c][0] = fma(nv, X[(0 * 3 + c) * KFM + cfs + r], J[c][0]);
-            J[c][1] = fma(nv, X[(1 * 3 + c) * KFM + cfs + r], J[c][1]);
-            if (r < p) J[c][2] = fma(mv, X[(2 * 3 + c) * KFM + cfs + 1 + r], J[c][2]);
+            J[c][0] = fma(nv, x[0 * 3 + c], J[c][0]);
+            J[c][1] = fma(nv, x[1 * 3 + c], J[c][1]);
+        }
+        if (r >= 1) {
+            const double mv = mt[r - 1];
+            #pragma unroll
+            for (int c = 0; c < 3; ++c) J[c][2] = fma(mv, x[2 * 3 + c], J[c][2]);
         }
         #pragma unroll
-        for (int u = 0; u < NNU; ++u) nu[u] = fma(nv, X[(9 + u) * KFM + cfs + r], nu[u]);
+        for (int u = 0; u < NNU; ++u) nu[u] = fma(nv, x[9 + u], nu[u]);
     }
     // coefficient values: kappa then gamma among the NNU nets
     const double kap = a.kappa ? nu[0] : 1.0;
@@ -596,11 +610,17 @@ wq_status launch_coef(wq_plan_s *P, const double *ctrl, const double *kappa, con
             auto runt = [&](auto PPc, auto NUc) {
                 constexpr int PP = decltype(PPc)::value, NNU = decltype(NUc)::value;
                 const size_t ne = 9 + NNU;
-                const size_t na = ne * (TQM + P->p + 1) * (TQF + P->p + 1), nx = (size_t)TQM * ne * (TQF + P->p + 1);
-                const size_t sm = (na > nx ? na : nx) * sizeof(double);
-                wq_smem_attr((const void *)k_coefz<TQM, PP, NNU>, sm);
+                const size_t kfm = TQF / 2 + 2 + PP, kmm = TQM / 2 + 2 + PP, bsp = wq_bstride(PP) + 1;
+                const size_t na = (ne * kfm * kmm + 1) & ~(size_t)1, nx = (size_t)TQM * ((ne + 1) & ~(size_t)1) * kfm;
+                const size_t sm = (na + nx + (TQF + TQM) * bsp) * sizeof(double);
                 dim3 g((unsigned)((a.nq_loc_d + TQF - 1) / TQF), (unsigned)((P->dir[0].nq + TQM - 1) / TQM), (unsigned)P->dir[1].nq);
-                k_coefz<TQM, PP, NNU><<<g, TQF * TQM, sm, s>>>(a);
+                if (getenv("WQ_COEFZ_MINB2")) {
+                    wq_smem_attr((const void *)k_coefz<TQM, PP, NNU, 2>, sm);
+                    k_coefz<TQM, PP, NNU, 2><<<g, TQF * TQM, sm, s>>>(a);
+                } else {
+                    wq_smem_attr((const void *)k_coefz<TQM, PP, NNU, 3>, sm);
+                    k_coefz<TQM, PP, NNU, 3><<<g, TQF * TQM, sm, s>>>(a);
+                }
             };
             auto runt_p = [&](auto NUc) {
                 switch (P->p) {
