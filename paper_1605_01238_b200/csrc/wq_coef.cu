@@ -227,14 +227,20 @@ __global__ void __launch_bounds__(TQF * TQM, MINB) k_coefz(CoefArgs a) {
     if (KF > KFM || KM > KMM) __trap();  // point-layout invariant
     constexpr int NEP = (NE + 1) & ~1;     // X row: the NE entries padded to whole double2 pairs
     constexpr int BS = wq_bstride(PP), BSP = BS + 1;  // table rows, padded to an odd stride in smem
-    double *Asm = sm;                                   // [NE entries][KFM][KMM]  (k_1 fastest)
-    double *Xsm = Asm + ((NE * KFM * KMM + 1) & ~1);    // [TQM][KFM][NEP]
+    // A row (one k_3): the tile's k_1 window x NE entries, padded to an odd length so that the lanes
+    // of stage B (consecutive k_3) hit distinct banks
+    constexpr int RL = (KMM * NE) | 1;
+    double *Asm = sm;                                   // [KFM][RL]: entry (k_1 - kma) * NE + e
+    double *Xsm = Asm + ((KFM * RL + 1) & ~1);          // [TQM][KFM][NEP]
     double *T2s = Xsm + TQM * KFM * NEP;                // [TQF][BSP] basis rows of the tile's q_3 points
     double *T0s = T2s + TQF * BSP;                      // [TQM][BSP] basis rows of the tile's q_1 points
     const int tid = threadIdx.x;
     const int64_t n0 = v0.n, n1 = v1.n;
-    for (int x = tid; x < ntf * BS; x += blockDim.x) T2s[(x / BS) * BSP + x % BS] = v2.B[(cqb + qfa) * BS + x];
-    for (int x = tid; x < ntm * BS; x += blockDim.x) T0s[(x / BS) * BSP + x % BS] = v0.B[qma * BS + x];
+    {
+        const double *b2 = v2.B + (cqb + qfa) * BS, *b0 = v0.B + qma * BS;
+        for (int x = tid; x < ntf * BS; x += TQF * TQM) T2s[(x / BS) * BSP + x % BS] = b2[x];
+        for (int x = tid; x < ntm * BS; x += TQF * TQM) T0s[(x / BS) * BSP + x % BS] = b0[x];
+    }
     {
         // stage A: contract k_2 with the plane's basis.  Thread = one fixed column e = (k_1 - kma)*NE +
         // entry of the tile and a row group g, looping over the rows k_3 = g, g + G, ...: for fixed
@@ -244,9 +250,11 @@ __global__ void __launch_bounds__(TQF * TQM, MINB) k_coefz(CoefArgs a) {
         // with N2; the M2 column's weight 0 is paired with the valid row span, so every lane loads)
         const double *nt = Ntab(v1, p, q1p), *mt = Mtab(v1, p, q1p);
         const int64_t e1 = v1.span[q1p];
-        const int KE = KM * NE, G = (int)blockDim.x / KE;
-        const int g = tid / KE, e = tid - g * KE;
-        if (g < G) {
+        // fixed thread -> (row group, column) map for the largest window (compile-time divisions)
+        constexpr int KEM = KMM * NE, G = TQF * TQM / KEM;
+        static_assert(G >= 1, "one row group");
+        const int g = tid / KEM, e = tid - g * KEM;
+        if (g < G && e < KM * NE) {
             const int cm = e / NE, vc = e - cm * NE;
             const bool dv = vc >= 3 && vc < 6;
             double w[PP + 1];
@@ -254,9 +262,9 @@ __global__ void __launch_bounds__(TQF * TQM, MINB) k_coefz(CoefArgs a) {
             for (int r = 0; r <= PP; ++r) w[r] = dv ? (r >= 1 ? mt[r - 1] : 0.0) : nt[2 * r];
             const int64_t rs = n0 * NE, ps = n0 * n1 * NE * G;
             const double *Qe = a.dnet + (kma + n0 * (e1 + n1 * (kfa - a.k3b + g))) * NE + e;
-            double *As = Asm + (vc * KFM + g) * KMM + cm;
+            double *As = Asm + g * RL + e;  // consecutive lanes, consecutive words
             #pragma unroll 2
-            for (int cf = g; cf < KF; cf += G, Qe += ps, As += G * KMM) {
+            for (int cf = g; cf < KF; cf += G, Qe += ps, As += G * RL) {
                 double acc = 0.0;
                 #pragma unroll
                 for (int r = 0; r <= PP; ++r) acc = fma(w[r], __ldg(Qe + r * rs), acc);
@@ -266,7 +274,7 @@ __global__ void __launch_bounds__(TQF * TQM, MINB) k_coefz(CoefArgs a) {
     }
     __syncthreads();
     // stage B: contract k_1 for each q_1 point of the tile (items (q_1, k_3), k_3 fastest)
-    for (int t = tid; t < ntm * KF; t += blockDim.x) {
+    for (int t = tid; t < ntm * KF; t += TQF * TQM) {
         const int tm = t / KF, cf = t - tm * KF;
         const double *nt = T0s + tm * BSP, *mt = nt + 2 * (PP + 1);
         const int cms = (int)(v0.span[qma + tm] - kma);
@@ -279,9 +287,9 @@ __global__ void __launch_bounds__(TQF * TQM, MINB) k_coefz(CoefArgs a) {
             #pragma unroll
             for (int vc = 0; vc < NE; ++vc) {
                 if (vc < 3) {  // derivative in direction 1: M1
-                    if (r < PP) X[vc] = fma(mv, Asm[(vc * KFM + cf) * KMM + cms + 1 + r], X[vc]);
+                    if (r < PP) X[vc] = fma(mv, Asm[cf * RL + (cms + 1 + r) * NE + vc], X[vc]);
                 } else {
-                    X[vc] = fma(nv, Asm[(vc * KFM + cf) * KMM + cms + r], X[vc]);
+                    X[vc] = fma(nv, Asm[cf * RL + (cms + r) * NE + vc], X[vc]);
                 }
             }
         }
@@ -611,7 +619,7 @@ wq_status launch_coef(wq_plan_s *P, const double *ctrl, const double *kappa, con
                 constexpr int PP = decltype(PPc)::value, NNU = decltype(NUc)::value;
                 const size_t ne = 9 + NNU;
                 const size_t kfm = TQF / 2 + 2 + PP, kmm = TQM / 2 + 2 + PP, bsp = wq_bstride(PP) + 1;
-                const size_t na = (ne * kfm * kmm + 1) & ~(size_t)1, nx = (size_t)TQM * ((ne + 1) & ~(size_t)1) * kfm;
+                const size_t na = (kfm * ((kmm * ne) | 1) + 1) & ~(size_t)1, nx = (size_t)TQM * ((ne + 1) & ~(size_t)1) * kfm;
                 const size_t sm = (na + nx + (TQF + TQM) * bsp) * sizeof(double);
                 dim3 g((unsigned)((a.nq_loc_d + TQF - 1) / TQF), (unsigned)((P->dir[0].nq + TQM - 1) / TQM), (unsigned)P->dir[1].nq);
                 if (getenv("WQ_COEFZ_MINB2")) {
