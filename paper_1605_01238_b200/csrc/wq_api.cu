@@ -440,7 +440,7 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     if (!st) {
         // measured on C4 (100^3 elements, BASELINE configs[3]): mass by ZHP for
         // 4 <= p <= 7 and the row-tile kernel otherwise, stiffness by the z-line kernel for p <= 6
-        // and ZHP above
+        // except p = 5 (ZHP 17.7 ms against 19.6: its boundary lines are faster), ZHP for p = 7..9
         const bool zhp_m = zhp_supported(P, WQ_MASS) && p >= 4 && p <= 7;
         P->kernel_auto[0] = !P->need_mass ? 0
                           : d < 3 ? WQ_KERNEL_DIRECT
@@ -467,6 +467,7 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
         // stiffness: ZHP for p = 7..9, the row-tile kernel on the standard-layout copy at p = 10
         P->kernel_auto[1] = !P->need_stiff ? 0
                           : d < 3 ? WQ_KERNEL_DIRECT
+                          : p == 5 && zhp_supported(P, WQ_STIFFNESS) ? WQ_KERNEL_ZHP
                           : P->zline_ok ? WQ_KERNEL_ZLINE
                           : zhp_supported(P, WQ_STIFFNESS) && ((p >= 7 && p <= 9) || !tile_supported(P, WQ_STIFFNESS))
                               ? WQ_KERNEL_ZHP

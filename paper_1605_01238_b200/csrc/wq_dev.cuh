@@ -103,6 +103,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
     }
 }
 
+// wait with a nanosleep back-off after each failed test: for roles that wait long (a whole pipeline
+// step), so that their re-tests do not take issue slots from the warps doing the work
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *b, unsigned parity) {
+    unsigned spins = 0;
+    while (!mbar_try(b, parity)) {
+        __nanosleep(256);
+        if (++spins > (1u << 25)) __trap();
+    }
+}
+
+// 16-B asynchronous global -> shared copy (L2 only); src_bytes < 16 zero-fills the rest
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, unsigned src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ---------------------------------------------------------------- named barrier (subset of warps)
 __device__ __forceinline__ void bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -41,6 +41,13 @@
 namespace zhp {
 using namespace wqdev;
 
+// fully unrolled interior staircases (bits: 1 stage A, 2 stage B, 4 stage C); the rolled offset-group
+// form is smaller code (instruction-cache misses are the top stall of both roles at high p)
+#ifndef WQ_ZHP_UNROLL
+#define WQ_ZHP_UNROLL 7
+#endif
+constexpr bool kIntA = (WQ_ZHP_UNROLL & 1) != 0, kIntB = (WQ_ZHP_UNROLL & 2) != 0, kIntC = (WQ_ZHP_UNROLL & 4) != 0;
+
 constexpr int NPRO = 256;             // producer threads (stages A, B)
 constexpr int NCON = 256;             // consumer threads (stage C)
 constexpr int NT = NPRO + NCON;
@@ -83,12 +90,14 @@ struct Args {
     const int32_t *lines;    // line = i0 + n0 * i1
     int64_t n_lines;
     int ns;                  // G ring slots
+    int depth;               // pipeline depth D: the producers run up to D-1 steps ahead (2..4)
     int R;                   // rows per step
     int nb;                  // box buffers
     double *val;
     int32_t *col;
     int64_t val_base;
     int cl;                  // launched as clusters of the NCH chunk CTAs of a line (lockstep per step)
+    int abl;                 // measurement switch (env WQ_ZHP_ABLATE), bits: 1 = no stage C, 2 = no stages A, B, 4 = no box loads
 };
 
 // shared-memory carve-up (byte offsets), identical on host and device
@@ -101,7 +110,7 @@ __host__ __device__ inline Layout layout(int nb, int R, int ns, int64_t n2l) {
     Layout L;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 127) & ~(size_t)127; return r; };
-    L.bar = take(8 * 12);
+    L.bar = take(8 * 16);
     L.box = take(8 * (size_t)nb * CF::BOXD);
     L.y = take(8 * (size_t)R * CF::YPAIR);
     L.ring = take(8 * (size_t)ns * CF::SLOT);
@@ -115,7 +124,7 @@ __host__ __device__ inline Layout layout(int nb, int R, int ns, int64_t n2l) {
     L.g0 = take(4 * (size_t)(CF::NP + 1));
     L.g1 = take(4 * (size_t)(CF::NP + 1));
     L.w2 = take(8 * 4 * 2 * (size_t)R * CF::QR);
-    L.g2 = take(4 * 2 * (size_t)R * (CF::NP + 1));
+    L.g2 = take(4 * (size_t)n2l * (CF::NP + 1));
     L.d2 = take(8 * (size_t)(n2l + 1) + 16 * (size_t)n2l);
     L.total = o;
     return L;
@@ -173,7 +182,7 @@ __device__ __forceinline__ void stage_a(const double *Boxes, int nb, int pp0, in
         for (int t = 0; t < T; ++t) { y0[0][t] = 0.0; y0[1][t] = 0.0; y1[0][t] = 0.0; y1[1][t] = 0.0; }
         if constexpr (MASS) {
             const double w1 = W1t[c1 * 4 + 0];
-            staircase<P, QX == 2 * P + 1>(g0, [&](int c0, auto O) {
+            staircase<P, kIntA && QX == 2 * P + 1>(g0, [&](int c0, auto O) {
                 constexpr int o = decltype(O)::value;
                 const double2 cv = *(const double2 *)(box + (c0 * QX + c1) * 2);
                 const double s = W0t[c0 * 4 + 0] * w1;
@@ -203,7 +212,7 @@ __device__ __forceinline__ void stage_a(const double *Boxes, int nb, int pp0, in
             const double2 w1p = *(const double2 *)(W1t + c1 * 4 + (m == 1 ? 2 : 0));  // (w1^(0,b1), w1^(1,b1))
             const int w0o = m == 0 ? 2 : 0;
             const bool der0 = m == 0;
-            staircase<P, QX == 2 * P + 1>(g0, [&](int c0, auto O) {
+            staircase<P, kIntA && QX == 2 * P + 1>(g0, [&](int c0, auto O) {
                 constexpr int o = decltype(O)::value;
                 const double2 w0p = *(const double2 *)(W0t + c0 * 4 + w0o);  // (w0^(0,b0), w0^(1,b0))
                 const double s1 = w0p.x * w1p.x, s2 = w0p.y * w1p.x, s3 = w0p.x * w1p.y;
@@ -247,8 +256,9 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
     const int n2l = (int)a.n2l;
     const Layout Ly = layout<P, MASS, T, QX>(NB, R, NS, a.n2l);
     uint64_t *full = (uint64_t *)(smb + Ly.bar);  // [NB] box loads
-    uint64_t *ready = full + 8;                   // [2] step planes produced (count NPRO)
-    uint64_t *freeb = full + 10;                  // [2] step consumed (count NCON)
+    uint64_t *ready = full + 8;                   // [D] step planes produced (count NPRO)
+    uint64_t *freeb = full + 12;                  // [D] step consumed (count NCON)
+    const int D = a.depth;
     double *Box = (double *)(smb + Ly.box);
     double *Y = (double *)(smb + Ly.y);
     double *Ring = (double *)(smb + Ly.ring);
@@ -258,7 +268,7 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
     int *off0 = (int *)(smb + Ly.o0), *off1 = (int *)(smb + Ly.o1);
     int *g0 = (int *)(smb + Ly.g0), *g1 = (int *)(smb + Ly.g1);
     double *W2s = (double *)(smb + Ly.w2);  // [2 parities][R][QR][4]
-    int *g2s = (int *)(smb + Ly.g2);        // [2 parities][R][NP+1]
+    int *g2s = (int *)(smb + Ly.g2);        // [n2l][NP+1] staircase groups of every row (direction 2)
     int64_t *pref2 = (int64_t *)(smb + Ly.d2);
     int *qlo2 = (int *)(pref2 + n2l + 1), *qlen2 = qlo2 + n2l, *jlo2 = qlen2 + n2l, *jlen2 = jlo2 + n2l;
 
@@ -269,9 +279,17 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
         qlo2[x] = v2.qlo[i2b + x] - cqb; qlen2[x] = v2.qlen[i2b + x]; jlo2[x] = v2.jlo[i2b + x]; jlen2[x] = v2.jlen[i2b + x];
     }
     for (int x = tid; x <= n2l; x += NT) pref2[x] = v2.pref[i2b + x] - v2.pref[a.slab_b];
+    // the rows' groups depend on i2 only: formed once per CTA for every line
+    for (int x = tid; x < n2l * (NP + 1); x += NT) {
+        const int rr = x / (NP + 1), o = x % (NP + 1);
+        const int q0 = v2.qlo[i2b + rr], n = v2.qlen[i2b + rr], j = v2.jlo[i2b + rr];
+        int c = 0;
+        while (c < n && v2.span[q0 + c] - j < o) ++c;
+        g2s[x] = o == NP ? n : c;
+    }
     if (tid == 0) {
         for (int b = 0; b < NB; ++b) mbar_init(&full[b], 1);
-        for (int b = 0; b < 2; ++b) { mbar_init(&ready[b], NPRO); mbar_init(&freeb[b], NCON); }
+        for (int b = 0; b < D; ++b) { mbar_init(&ready[b], NPRO); mbar_init(&freeb[b], NCON); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -300,9 +318,9 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
             const int ql0 = v0.qlo[i0], nq0 = v0.qlen[i0], jl0 = v0.jlo[i0];
             const int ql1 = v1.qlo[i1], nq1 = v1.qlen[i1], jl1 = v1.jlo[i1];
             // the ring restarts at plane 0: wait until the consumers have finished the previous item
-            if (gs >= 1) mbar_wait(&freeb[(gs - 1) & 1], ((gs - 1) >> 1) & 1);
+            if (gs >= 1) mbar_wait_sleep(&freeb[(gs - 1) % D], ((gs - 1) / D) & 1);
             bar_sync(1, NPRO);  // every producer is past the previous item (tables free)
-            if (ptid == 0) {
+            if (ptid == 0 && !(a.abl & 4)) {
                 for (int b = 0; b < NB && b < npairs; ++b) {
                     mbar_arrive_tx(&full[b], BOX_BYTES);
                     tma_load_4d(Box + b * CF::BOXD, &tm, &full[b], (int)a.qoff + 2 * b, ql1, ql0, 0);
@@ -330,15 +348,15 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                 const int r0 = st * R;
                 const int rl = (r0 + R <= n2l ? r0 + R : n2l) - 1;
                 const int need = (qlo2[rl] + qlen2[rl] + 1) / 2;  // pairs covering the step's last point
-                // the slots this step writes were last read two steps ago
-                if (gs >= 2) mbar_wait(&freeb[gs & 1], ((gs >> 1) - 1) & 1);
+                // the slots this step writes were last read D steps ago
+                if (gs >= D) mbar_wait_sleep(&freeb[gs % D], ((gs - D) / D) & 1);
                 while (pairs_done < need) {
                     const int nbat = need - pairs_done < R ? need - pairs_done : R;
                     for (int k = 0; k < nbat; ++k) {
                         const int b = (pairs_done + k) % NB;
-                        mbar_wait(&full[b], (use_bits >> b) & 1);
+                        if (!(a.abl & 4)) mbar_wait(&full[b], (use_bits >> b) & 1);
                     }
-                    switch (ch) {
+                    if (!(a.abl & 2)) switch (ch) {
                     case 0: stage_a<P, MASS, T, QX, 0>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
                     case 1: if constexpr (NCH > 1) stage_a<P, MASS, T, QX, 1>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
                     case 2: if constexpr (NCH > 2) stage_a<P, MASS, T, QX, 2>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
@@ -352,14 +370,14 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                     for (int k = 0; k < nbat; ++k) {
                         const int pp = pairs_done + k, b = pp % NB;
                         use_bits ^= 1u << b;
-                        if (ptid == 0 && pp + NB < npairs) {
+                        if (ptid == 0 && pp + NB < npairs && !(a.abl & 4)) {
                             if (k == 0) fence_async_smem();
                             mbar_arrive_tx(&full[b], BOX_BYTES);
                             tma_load_4d(Box + b * CF::BOXD, &tm, &full[b], (int)a.qoff + 2 * (pp + NB), ql1, ql0, 0);
                         }
                     }
                     // stage B for the batch: items (plane j, t0, family g) -> G ring, + the planes' B2 pairs
-                    const int nitem = nbat * 2 * NGF * T;
+                    const int nitem = (a.abl & 2) ? 0 : nbat * 2 * NGF * T;
                     for (int x = ptid; x < nitem; x += NPRO) {
                         const int g = x % NGF, tl = (x / NGF) % T, j = x / (NGF * T);
                         const int k = j >> 1, pt = j & 1;
@@ -369,7 +387,7 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                         #pragma unroll
                         for (int t = 0; t < K; ++t) acc[t] = 0.0;
                         if constexpr (MASS) {
-                            staircase<P, QX == 2 * P + 1>(g1, [&](int c1, auto O) {
+                            staircase<P, kIntB && QX == 2 * P + 1>(g1, [&](int c1, auto O) {
                                 constexpr int o = decltype(O)::value;
                                 const double yv = Yk[c1 * T + tl];
                                 const double2 *bp = B1t + c1 * NP;
@@ -382,7 +400,7 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                             const int a2 = g & 1, b2 = g >> 1;
                             const double *Ya = Yk + ((b2 ? 4 : 0) + a2) * QX * T;
                             const double *Yb = Yk + (2 + a2) * QX * T;
-                            staircase<P, QX == 2 * P + 1>(g1, [&](int c1, auto O) {
+                            staircase<P, kIntB && QX == 2 * P + 1>(g1, [&](int c1, auto O) {
                                 constexpr int o = decltype(O)::value;
                                 const double ya = Ya[c1 * T + tl];
                                 const double yb = b2 ? 0.0 : Yb[c1 * T + tl];
@@ -409,7 +427,7 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                     bar_sync(1, NPRO);  // Y free for the next batch
                     pairs_done += nbat;
                 }
-                mbar_arrive(&ready[gs & 1]);  // release: this step's planes are in the ring
+                mbar_arrive(&ready[gs % D]);  // release: this step's planes are in the ring
                 step_sync();
             }
         }
@@ -419,6 +437,20 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
     // ==================================================================== consumers
     const int ctid = tid - NPRO;
     int64_t gs = 0;
+    // direction-2 weights of a step's rows (they depend on i2 only), copied asynchronously one step
+    // ahead into the buffer of that step's parity: [2 parities][R][QR][4]
+    auto load_w2 = [&](int st, int par) {
+        const int r0 = st * R, nr = r0 + R <= n2l ? R : n2l - r0;
+        double *W2p = W2s + (size_t)par * R * CF::QR * 4;
+        for (int x = ctid; x < nr * CF::QR * 2; x += NCON) {  // 16-B pieces: (point, half)
+            const int rho = x / (CF::QR * 2), e = x % (CF::QR * 2);
+            const int i2 = i2b + r0 + rho;
+            const bool in = e / 2 < qlen2[r0 + rho];
+            cp_async16(W2p + (size_t)rho * CF::QR * 4 + 2 * e, in ? (const void *)(v2.W + (int64_t)i2 * v2.maxq * 4 + 2 * e) : (const void *)v2.W,
+                       in ? 16u : 0u);
+        }
+    };
+    if (a.n_lines > blockIdx.x / NCH) load_w2(0, 0);
     for (int64_t li = blockIdx.x / NCH; li < a.n_lines; li += gridDim.x / NCH) {
         const int line = a.lines[li];
         const int ch = (int)(blockIdx.x % NCH);
@@ -434,27 +466,20 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
             const int nr = r0 + R <= n2l ? R : n2l - r0;
             const int par = (int)(gs & 1);
             double *W2p = W2s + (size_t)par * R * CF::QR * 4;
-            int *g2p = g2s + par * R * (NP + 1);
-            // row tables of the step: weights of direction 2 and the staircase groups
-            for (int x = ctid; x < nr * CF::QR * 4; x += NCON) {
-                const int rho = x / (CF::QR * 4), e = x % (CF::QR * 4);
-                const int i2 = i2b + r0 + rho;
-                W2p[x] = e / 4 < qlen2[r0 + rho] ? __ldg(v2.W + (int64_t)i2 * v2.maxq * 4 + e) : 0.0;
-            }
-            if (ctid < nr * (NP + 1)) {
-                const int rho = ctid / (NP + 1), o = ctid % (NP + 1), rr = r0 + rho;
-                const int q0 = qlo2[rr], n = qlen2[rr], j = jlo2[rr];
-                int c = 0;
-                while (c < n && v2.span[cqb + q0 + c] - j < o) ++c;
-                g2p[rho * (NP + 1) + o] = o == NP ? n : c;
-            }
+            const int *g2p = g2s + r0 * (NP + 1);
             bool all_int = true;
             for (int rho = 0; rho < nr; ++rho) {
                 const int i2 = i2b + r0 + rho;
                 all_int = all_int && i2 >= P + 1 && i2 <= (int)v2.n - P - 2 && qlen2[r0 + rho] == 2 * P + 1;
             }
-            bar_sync(2, NCON);
-            mbar_wait(&ready[par], (gs >> 1) & 1);  // acquire: the step's planes
+            cp_async_wait_all();  // this thread's pieces of the step's weights
+            bar_sync(2, NCON);    // everyone's pieces; every consumer is past the previous step
+            {   // next step's weights (the next line's first step after the last one)
+                const bool last_item = li + gridDim.x / NCH >= a.n_lines;
+                if (st + 1 < nsteps) load_w2(st + 1, par ^ 1);
+                else if (!last_item) load_w2(0, par ^ 1);
+            }
+            mbar_wait_sleep(&ready[gs % D], (gs / D) & 1);  // acquire: the step's planes
             // stage C: CPT adjacent columns per thread (the row's point weights and basis pairs are
             // loaded once for them)
             auto stage_c = [&](auto IC) {
@@ -463,7 +488,7 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                 for (int x = ctid; x < nr * NCP; x += NCON) {
                     const int rho = x / NCP, cl0 = x % NCP;  // columns cl0 + j NCP (consecutive lanes, consecutive columns)
                     const int rr = r0 + rho;
-                    const int q0 = qlo2[rr];
+                    const int q0 = qlo2[rr], s0 = q0 % NS;  // ring slot of the row's first point
                     const double *Wr = W2p + rho * CF::QR * 4;
                     const int *gg = g2p + rho * (NP + 1);
                     int clc[CPT];
@@ -476,7 +501,7 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                         for (int t = 0; t < K; ++t) acc[j][t] = 0.0;
                     staircase<P, INTC>(gg, [&](int c, auto O) {
                         constexpr int o = decltype(O)::value;
-                        const int s = (q0 + c) % NS;
+                        const int s = s0 + c < NS ? s0 + c : s0 + c - NS;  // c < #Q <= NS
                         const double2 *bp = RB2 + s * NP;
                         const double *Gs = Ring + (size_t)s * CF::SLOT;
                         if constexpr (MASS) {
@@ -508,32 +533,44 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                             }
                         }
                     });
-                    const int ni2 = jlen2[rr];
+                    const int ni2 = INTC ? K : jlen2[rr];  // interior rows: 2p+1 trial indices t2
                     const int64_t row = pref2[rr] * a.L1 * a.L0 + (int64_t)ni2 * (p1L0 + p0n1) - a.val_base;
-                    const int64_t stp = (int64_t)ni0 * ni1;
+                    const int stp = ni0 * ni1;
                     #pragma unroll
                     for (int j = 0; j < CPT; ++j) {
                         const int cl = cl0 + j * NCP;
                         const int tl = cl % T, t1 = cl / T, tg = ta + tl;
                         if (cl < COLS && tl < tn && tg < ni0 && t1 < ni1) {
                             const int64_t e0 = row + tg + (int64_t)ni0 * t1;
+                            double *vp = a.val + e0;  // pointer walk: one 64-bit add per store
                             #pragma unroll
-                            for (int t = 0; t < K; ++t)
-                                if (t < ni2) a.val[e0 + stp * t] = acc[j][t];
+                            for (int t = 0; t < K; ++t) {
+                                if (INTC || t < ni2) *vp = acc[j][t];
+                                vp += stp;
+                            }
                             if (a.col) {
                                 const int jb = (jl0 + tg) + (int)a.n0 * ((jl1 + t1) + (int)a.n1 * jlo2[rr]);
                                 const int js = (int)(a.n0 * a.n1);
+                                int32_t *cp = a.col + e0;
                                 #pragma unroll
-                                for (int t = 0; t < K; ++t)
-                                    if (t < ni2) a.col[e0 + stp * t] = jb + js * t;
+                                for (int t = 0; t < K; ++t) {
+                                    if (INTC || t < ni2) *cp = jb + js * t;
+                                    cp += stp;
+                                }
                             }
                         }
                     }
                 }
             };
-            if (all_int) stage_c(std::true_type{});
+            if (a.abl & 1) {
+            } else if (kIntC && all_int) stage_c(std::true_type{});
             else stage_c(std::false_type{});
-            mbar_arrive(&freeb[par]);  // this step's ring slots may be overwritten
+            // this step's ring slots may be overwritten.  Relaxed: every value this thread read from
+            // the ring fed the accumulators of the stores it has already issued, so the reads are
+            // complete; a release arrive would also wait for those global stores to be acknowledged
+            // (ncu: 'membar' stalls of the consumers, C4 p = 8).  Bit-repeatability stress test:
+            // tests/test_gpu_parity.py::test_zline_repeatable_bit_exact (ZHP cases).
+            mbar_arrive_relaxed(&freeb[gs % D]);
             step_sync();
         }
     }
@@ -577,14 +614,21 @@ inline Plan2 plan2(const wq_plan_s *Pl, int64_t pl_lo, int64_t pl_hi) {
 // ring slots for R rows per step: the production of a step overwrites slot (q mod NS) of planes q <
 // 2 need while the step's rows read planes >= qlo(first row)
 // (the producers write the planes of step s+1 while the consumers read those of step s)
-inline int ring_slots(const Plan2 &g, int R) {
+inline int ring_slots(const Plan2 &g, int R, int D) {
     int ns = 2;
     for (int64_t r0 = 0; r0 < g.n2l; r0 += R) {
-        const int64_t r1 = std::min<int64_t>(r0 + 2 * R, g.n2l) - 1;  // last row of the next step
+        const int64_t r1 = std::min<int64_t>(r0 + (int64_t)D * R, g.n2l) - 1;  // last row D-1 steps ahead
         const int need = (g.qhi[r1] + 2) / 2;
         ns = std::max(ns, 2 * need - g.qlo[r0]);
     }
     return ns;
+}
+
+// pipeline depth (measurement switch WQ_ZHP_D, 2..4)
+inline int zhp_depth() {
+    const char *e = getenv("WQ_ZHP_D");
+    const int d = e ? atoi(e) : 2;
+    return d < 2 ? 2 : (d > 4 ? 4 : d);
 }
 
 template <int P, bool MASS, int QX>
@@ -600,7 +644,7 @@ bool choose(const Plan2 &g, int &nb, int &R, int &ns, size_t &smem, int optin) {
     for (int r = rbest; r >= 1; --r)
         for (int b = 2 * r; b >= r; --b) {
             if (b > 8 || (nb_env && b != nb_env)) continue;
-            const int n = ring_slots(g, r);
+            const int n = ring_slots(g, r, zhp_depth());
             const Layout L = layout<P, MASS, T, QX>(b, r, n, g.n2l);
             if (L.total <= (size_t)optin) {
                 nb = b;
@@ -644,6 +688,7 @@ wq_status launch_cls(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, const
     a.ns = ns;
     a.R = R;
     a.nb = nb;
+    a.depth = zhp_depth();
     a.val = val;
     a.col = col;
     a.val_base = val_base;
@@ -681,6 +726,7 @@ wq_status launch_cls(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, const
     // measured: lockstep clusters pay with two chunks (C4 p = 7 mass 42.9 -> 34.6 ms) and cost with
     // three or more (p = 8 stiffness 155 -> 298 ms)
     a.cl = NCH == 2 && !getenv("WQ_ZHP_NOCLUSTER");
+    a.abl = getenv("WQ_ZHP_ABLATE") ? atoi(getenv("WQ_ZHP_ABLATE")) : 0;
     cfg.numAttrs = a.cl ? 1 : 0;
     ce = cudaLaunchKernelEx(&cfg, k_zhp<P, MASS, T, QX>, m, a);
     wq_count_launches(1);

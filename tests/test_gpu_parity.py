@@ -409,19 +409,23 @@ def test_every_kernel_reads_every_plan():
         check_every_row(o, STIFFNESS, rp, col, val)
 
 
-@pytest.mark.parametrize("p,E", [(3, 14), (4, 18)])
-def test_zline_repeatable_bit_exact(p, E):
+@pytest.mark.parametrize("p,E,kernel,matrix", [(3, 14, "ZLINE", STIFFNESS), (4, 18, "ZLINE", STIFFNESS),
+                                               (4, 18, "ZHP", STIFFNESS), (8, 20, "ZHP", STIFFNESS),
+                                               (6, 16, "ZHP", MASS)])
+def test_zline_repeatable_bit_exact(p, E, kernel, matrix):
     """Stress check of the producer/consumer hand-offs (ADVICE: ring slots are returned with relaxed
-    mbarrier arrives): 20 back-to-back assemblies of the same plan give bit-identical values."""
+    mbarrier arrives, z-line and ZHP): 20 back-to-back assemblies of the same plan give bit-identical
+    values."""
     torch = _torch()
     ks, ctrl = make_case(3, p, E, "annulus", 0.05)
-    plan = wq.Plan(p, ks, ctrl=ctrl, need_mass=False)
+    plan = wq.Plan(p, ks, ctrl=ctrl, need_mass=matrix == MASS, need_stiffness=matrix == STIFFNESS)
+    k = getattr(wq, "WQ_KERNEL_" + kernel)
     rp, col, val = plan.alloc_csr()
-    wq.wq_assemble(plan.h, STIFFNESS, val, col)
+    wq.wq_assemble(plan.h, matrix, val, col, kernel=k)
     ref = val.clone()
     for _ in range(20):
         val.zero_()
-        wq.wq_assemble(plan.h, STIFFNESS, val, col)
+        wq.wq_assemble(plan.h, matrix, val, col, kernel=k)
         torch.cuda.synchronize()
         assert torch.equal(val, ref)
     plan.close()
