@@ -438,19 +438,20 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
     }
     // ---- which kernel WQ_KERNEL_AUTO runs
     if (!st) {
-        // measured on C4 (100^3 elements, BASELINE configs[3]): mass by ZHP for
-        // 4 <= p <= 7 and the row-tile kernel otherwise, stiffness by the z-line kernel for p <= 6
-        // except p = 5 (ZHP 17.7 ms against 19.6: its boundary lines are faster), ZHP for p = 7..9
-        const bool zhp_m = zhp_supported(P, WQ_MASS) && p >= 4 && p <= 7;
+        // measured on C4 (100^3 elements, BASELINE configs[3]): mass by ZHP for p >= 4
+        // and the row-tile kernel below, stiffness by the z-line kernel for p <= 6 except p = 5 (ZHP
+        // 17.5 ms against 19.6: its boundary lines are faster), ZHP for p >= 7
+        const bool zhp_m = zhp_supported(P, WQ_MASS) && p >= 4;
         P->kernel_auto[0] = !P->need_mass ? 0
                           : d < 3 ? WQ_KERNEL_DIRECT
                           : zhp_m ? WQ_KERNEL_ZHP
                           : tile_supported(P, WQ_MASS) ? WQ_KERNEL_TILE
                           : zhp_supported(P, WQ_MASS) ? WQ_KERNEL_ZHP : WQ_KERNEL_DIRECT;
-        if (d == 3 && P->need_stiff && !P->zline_ok && !(zhp_supported(P, WQ_STIFFNESS) && p >= 7 && p <= 9) &&
+        if (d == 3 && P->need_stiff && !P->zline_ok && !(zhp_supported(P, WQ_STIFFNESS) && p >= 7) &&
             tile_supported(P, WQ_STIFFNESS)) {
-            // the row-tile stiffness reads a standard-layout copy (made after every coefficient build;
-            // measured at C4 p = 10: 574 -> 407 ms; its mass path is faster on the z layout)
+            // the row-tile stiffness (fallback when ZHP does not fit) reads a standard-layout copy
+            // (made after every coefficient build; measured at C4 p = 10: 574 -> 407 ms; its mass
+            // path is faster on the z layout)
             const size_t sb = sizeof(double) * (size_t)P->ncomp * (size_t)cp;
             ce = cudaMalloc((void **)&P->coef_std, sb);
             if (ce != cudaSuccess) { P->coef_std = nullptr; st = fail(WQ_ENOMEM, "standard-layout coefficient copy"); }
@@ -464,12 +465,12 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
             }
         }
         if (!st) st = create_build(P);
-        // stiffness: ZHP for p = 7..9, the row-tile kernel on the standard-layout copy at p = 10
+        // stiffness: ZHP for p >= 7 (C4 p = 10: 361 ms, row-tile on the standard-layout copy 407)
         P->kernel_auto[1] = !P->need_stiff ? 0
                           : d < 3 ? WQ_KERNEL_DIRECT
                           : p == 5 && zhp_supported(P, WQ_STIFFNESS) ? WQ_KERNEL_ZHP
                           : P->zline_ok ? WQ_KERNEL_ZLINE
-                          : zhp_supported(P, WQ_STIFFNESS) && ((p >= 7 && p <= 9) || !tile_supported(P, WQ_STIFFNESS))
+                          : zhp_supported(P, WQ_STIFFNESS) && (p >= 7 || !tile_supported(P, WQ_STIFFNESS))
                               ? WQ_KERNEL_ZHP
                           : tile_supported(P, WQ_STIFFNESS) ? WQ_KERNEL_TILE : WQ_KERNEL_DIRECT;
     }

@@ -1,37 +1,39 @@
 #pragma once
 // wq_zhp.cuh -- step 7, the z-line kernel for every degree and both matrices (WQ_KERNEL_ZHP):
-// lines along direction 3 like k_zline, but with CTA-wide phases instead of warp roles, so that
-// the shared-memory pipeline stays within the SM at high p.
+// lines along direction 3 like k_zline, with a producer and a consumer thread group per CTA, built
+// so that the shared-memory pipeline fits the SM at every degree.
 //
 // Arithmetic (Eq. sumfactorization P:837 / Alg. 3; stiffness reading R8, families R3).
 // A LINE is the set of rows i = (i0, i1, i2), (i0, i1) fixed, i2 over the plan's slab; an ITEM is a
-// line and a chunk of T consecutive values of t_0 (the first trial index).  With the weights of
+// line and a chunk of T consecutive values of t_1 (the second trial index).  With the weights of
 // directions 0 and 1 pushed onto the coefficient field pointwise:
 //   stiffness (6 chains (m, a2): m = trial-derivative direction, a2 = test derivative in dir. 2)
 //     H_{m,1} = w0^(0,b0) w1^(0,b1) C_2m,  H_{m,0} = w0^(1,b0) w1^(0,b1) C_0m + w0^(0,b0) w1^(1,b1) C_1m,
 //     b_k = [m == k];
-//     stage A (contract c0):  Y_{m,a2}(c1, t0) = sum_c0 D^{b0}B0_{t0}(c0) H_{m,a2}(c0, c1)
-//     stage B (contract c1):  G[b2][a2](t0, t1) = sum_{m: [m==2]=b2} sum_c1 D^{b1}B1_{t1}(c1) Y_{m,a2}(c1, t0)
+//     stage A (contract c1):  Y_{m,a2}(c0, t1) = sum_c1 D^{b1}B1_{t1}(c1) H_{m,a2}(c0, c1)
+//     stage B (contract c0):  G[b2][a2](t0, t1) = sum_{m: [m==2]=b2} sum_c0 D^{b0}B0_{t0}(c0) Y_{m,a2}(c0, t1)
 //     stage C (contract c2, per row i2):
 //       S(i; t0, t1, t2) = sum_c2 B2_{t2}(c2) U0(c2) + B2'_{t2}(c2) U1(c2),
 //       U0 = w2^(0,0) G[0][0] + w2^(1,0) G[0][1],  U1 = w2^(0,1) G[1][0] + w2^(1,1) G[1][1];
-//   mass (one chain): H = w0^(0,0) w1^(0,0) c, Y = sum_c0 B0 H, G = sum_c1 B1 Y,
+//   mass (one chain): H = w0^(0,0) w1^(0,0) c, Y = sum_c1 B1 H, G = sum_c0 B0 Y,
 //       M(i; t) = sum_c2 w2^(0,0) B2_{t2}(c2) G(c2).
+// (H is pointwise in (c0, c1), so the order of the first two contractions is free; contracting c1
+// first lets an item own whole runs of t0, the fastest index of a CSR row segment: a chunk CTA writes
+// every 32-B sector of its runs alone instead of sharing it with the neighbouring t0 chunk, which
+// had cost a read-modify-write of most written sectors at p = 8.)
 // Staircases for every row type: the points c of a row are grouped by their staircase offset
 // o(c) = span(c) - jlo (non-decreasing in c, 0 <= o <= p for every row of every knot vector), and
 // the kernel loops over o at compile time and over the points of the group at run time, so each
 // accumulator index o + r is a compile-time register index while the group bounds come from
 // small per-row tables: one code path for interior, boundary and graded rows.
 //
-// CTA (256 threads, one or two per SM, persistent over items): per step of R rows of the line
-//   production of the G planes the step needs, pair of points by pair of points (the coefficient
-//   box of a pair, 2 x QX x QX x ncomp, is one 4D TMA tile of the z layout, double buffered):
-//     stage A (threads = fibres (m, c1, point)), barrier, next box load, stage B (threads =
-//     (point, family, t0)) into a ring of G planes (+ the planes' direction-2 basis pairs);
-//   stage C: threads = (row, column (t0, t1)), acc[t2] in registers, plain coalesced stores of
-//   values (and fused columns) straight from registers.
-// The chunks of a line are consecutive items, so they run at the same time on neighbouring CTAs
-// and their interleaved partial-sector stores merge in L2.
+// CTA (256 producer + 256 consumer threads, one per SM, persistent over items): per step of R rows
+//   producers: the G planes the step needs, pair of points by pair of points (the coefficient box of
+//     a pair, 2 x QX x QX x ncomp, is one 4D TMA tile of the z layout, several in flight):
+//     stage A (threads = fibres (m, c0) of a pair), barrier, next box loads, stage B (threads =
+//     (point, family, t1)) into a ring of G planes (+ the planes' direction-2 basis pairs);
+//   consumers (stage C): threads = (row, column (t0, t1)), acc[t2] in registers, plain coalesced
+//     stores of values (and fused columns) straight from registers.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <algorithm>
@@ -71,7 +73,7 @@ struct Cfg {
     static constexpr int NC = MASS ? 1 : 6;       // coefficient components in the box
     static constexpr int NCHAIN = MASS ? 1 : 6;   // stage-A chains
     static constexpr int NGF = MASS ? 1 : 4;      // G families per column
-    static constexpr int COLS = T * K;            // columns (t0 local, t1) of an item, t0 fastest
+    static constexpr int COLS = T * K;            // columns (t0, t1 local) of an item, t0 fastest
     static constexpr int BOXD = (NC * QX * QX * 2 + 15) / 16 * 16;  // doubles per box buffer (128-B aligned TMA dst)
     static constexpr int YPAIR = 2 * NCHAIN * QX * T;  // doubles of Y per pair [pt][chain][c1][t0]
     static constexpr int SLOT = COLS * NGF;       // doubles of a G ring slot [col][family]
@@ -97,6 +99,7 @@ struct Args {
     int32_t *col;
     int64_t val_base;
     int cl;                  // launched as clusters of the NCH chunk CTAs of a line (lockstep per step)
+    int rollc;               // stage C in the rolled sliding-window form (env WQ_ZHP_ROLLC; default p >= 8)
     int abl;                 // measurement switch (env WQ_ZHP_ABLATE), bits: 1 = no stage C, 2 = no stages A, B, 4 = no box loads
 };
 
@@ -162,32 +165,33 @@ __device__ __forceinline__ void staircase(const int *g, F &&f) {
     }
 }
 
-// stage A of the pairs pp0 .. pp0 + nbat - 1 (box of pair pp in buffer pp % nb, Y of batch pair k);
-// a thread = fibre (m, c1) of one pair, both points (the box holds the pair's points side by side, so
-// one 16-B load serves both and the tables are loaded once per two points)
+// stage A of the pairs pp0 .. pp0 + nbat - 1 (box of pair pp in buffer pp % nb, Y of batch pair k):
+// contracts c1 for the chunk's t1 range; a thread = fibre (m, c0) of one pair, both points (the box
+// holds the pair's points side by side, so one 16-B load serves both and the tables are loaded once
+// per two points)
 template <int P, bool MASS, int T, int QX, int CH>
 __device__ __forceinline__ void stage_a(const double *Boxes, int nb, int pp0, int nbat, double *Yall,
-                                        const double2 *B0t, const double *W0t, const double *W1t, const int *g0,
-                                        int nq0, int nq1, int tid) {
+                                        const double2 *B1t, const double *W0t, const double *W1t, const int *g1,
+                                        int nq0, int tid) {
     using CF = Cfg<P, MASS, T, QX>;
-    constexpr int TA = Chunks<P>::ta(CH), TN = Chunks<P>::tn(CH);  // t0 range of the chunk
-    const int nfib = (MASS ? 1 : 3) * nq1;
+    constexpr int TA = Chunks<P>::ta(CH), TN = Chunks<P>::tn(CH);  // t1 range of the chunk
+    const int nfib = (MASS ? 1 : 3) * nq0;
     for (int fx = tid; fx < nbat * nfib; fx += NPRO) {
         const int k = fx / nfib, f = fx % nfib;
         const double *box = Boxes + ((pp0 + k) % nb) * CF::BOXD;
         double *Y = Yall + k * CF::YPAIR;
-        const int c1 = f % nq1, m = f / nq1;
+        const int c0 = f % nq0, m = f / nq0;
         double y0[2][T], y1[2][T];
         #pragma unroll
         for (int t = 0; t < T; ++t) { y0[0][t] = 0.0; y0[1][t] = 0.0; y1[0][t] = 0.0; y1[1][t] = 0.0; }
         if constexpr (MASS) {
-            const double w1 = W1t[c1 * 4 + 0];
-            staircase<P, kIntA && QX == 2 * P + 1>(g0, [&](int c0, auto O) {
+            const double w0 = W0t[c0 * 4 + 0];
+            staircase<P, kIntA && QX == 2 * P + 1>(g1, [&](int c1, auto O) {
                 constexpr int o = decltype(O)::value;
                 const double2 cv = *(const double2 *)(box + (c0 * QX + c1) * 2);
-                const double s = W0t[c0 * 4 + 0] * w1;
+                const double s = W1t[c1 * 4 + 0] * w0;
                 const double ha = s * cv.x, hb = s * cv.y;
-                const double2 *bp = B0t + c0 * CF::NP;
+                const double2 *bp = B1t + c1 * CF::NP;
                 #pragma unroll
                 for (int r = 0; r <= P; ++r) {
                     const int t = o + r - TA;
@@ -200,7 +204,7 @@ __device__ __forceinline__ void stage_a(const double *Boxes, int nb, int pp0, in
             });
             #pragma unroll
             for (int pt = 0; pt < 2; ++pt) {
-                double *Yo = Y + ((pt * CF::NCHAIN + 0) * QX + c1) * T;
+                double *Yo = Y + ((pt * CF::NCHAIN + 0) * QX + c0) * T;
                 #pragma unroll
                 for (int t = 0; t < T; ++t) Yo[t] = y0[pt][t];
             }
@@ -209,24 +213,24 @@ __device__ __forceinline__ void stage_a(const double *Boxes, int nb, int pp0, in
             const int ka = m == 0 ? 2 : (m == 1 ? 4 : 5);
             const int kb = m == 0 ? 0 : (m == 1 ? 1 : 2);
             const int kc = m == 0 ? 1 : (m == 1 ? 3 : 4);
-            const double2 w1p = *(const double2 *)(W1t + c1 * 4 + (m == 1 ? 2 : 0));  // (w1^(0,b1), w1^(1,b1))
-            const int w0o = m == 0 ? 2 : 0;
-            const bool der0 = m == 0;
-            staircase<P, kIntA && QX == 2 * P + 1>(g0, [&](int c0, auto O) {
+            const double2 w0p = *(const double2 *)(W0t + c0 * 4 + (m == 0 ? 2 : 0));  // (w0^(0,b0), w0^(1,b0))
+            const int w1o = m == 1 ? 2 : 0;
+            const bool der1 = m == 1;
+            staircase<P, kIntA && QX == 2 * P + 1>(g1, [&](int c1, auto O) {
                 constexpr int o = decltype(O)::value;
-                const double2 w0p = *(const double2 *)(W0t + c0 * 4 + w0o);  // (w0^(0,b0), w0^(1,b0))
+                const double2 w1p = *(const double2 *)(W1t + c1 * 4 + w1o);  // (w1^(0,b1), w1^(1,b1))
                 const double s1 = w0p.x * w1p.x, s2 = w0p.y * w1p.x, s3 = w0p.x * w1p.y;
                 const double2 ca = *(const double2 *)(box + ((ka * QX + c0) * QX + c1) * 2);
                 const double2 cb = *(const double2 *)(box + ((kb * QX + c0) * QX + c1) * 2);
                 const double2 cc = *(const double2 *)(box + ((kc * QX + c0) * QX + c1) * 2);
                 const double h1a = s1 * ca.x, h1b = s1 * ca.y;                                // a2 = 1 (l = 2)
                 const double h0a = fma(s2, cb.x, s3 * cc.x), h0b = fma(s2, cb.y, s3 * cc.y);  // a2 = 0 (l = 0, 1)
-                const double2 *bp = B0t + c0 * CF::NP;
+                const double2 *bp = B1t + c1 * CF::NP;
                 #pragma unroll
                 for (int r = 0; r <= P; ++r) {
                     const int t = o + r - TA;
                     if (t >= 0 && t < TN) {
-                        const double bv = der0 ? bp[r].y : bp[r].x;
+                        const double bv = der1 ? bp[r].y : bp[r].x;
                         y0[0][t] = fma(bv, h0a, y0[0][t]);
                         y0[1][t] = fma(bv, h0b, y0[1][t]);
                         y1[0][t] = fma(bv, h1a, y1[0][t]);
@@ -236,8 +240,8 @@ __device__ __forceinline__ void stage_a(const double *Boxes, int nb, int pp0, in
             });
             #pragma unroll
             for (int pt = 0; pt < 2; ++pt) {
-                double *Y0 = Y + ((pt * CF::NCHAIN + m * 2 + 0) * QX + c1) * T;
-                double *Y1 = Y + ((pt * CF::NCHAIN + m * 2 + 1) * QX + c1) * T;
+                double *Y0 = Y + ((pt * CF::NCHAIN + m * 2 + 0) * QX + c0) * T;
+                double *Y1 = Y + ((pt * CF::NCHAIN + m * 2 + 1) * QX + c0) * T;
                 #pragma unroll
                 for (int t = 0; t < T; ++t) { Y0[t] = y0[pt][t]; Y1[t] = y1[pt][t]; }
             }
@@ -357,13 +361,13 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                         if (!(a.abl & 4)) mbar_wait(&full[b], (use_bits >> b) & 1);
                     }
                     if (!(a.abl & 2)) switch (ch) {
-                    case 0: stage_a<P, MASS, T, QX, 0>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
-                    case 1: if constexpr (NCH > 1) stage_a<P, MASS, T, QX, 1>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
-                    case 2: if constexpr (NCH > 2) stage_a<P, MASS, T, QX, 2>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
-                    case 3: if constexpr (NCH > 3) stage_a<P, MASS, T, QX, 3>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
-                    case 4: if constexpr (NCH > 4) stage_a<P, MASS, T, QX, 4>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
-                    case 5: if constexpr (NCH > 5) stage_a<P, MASS, T, QX, 5>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
-                    case 6: if constexpr (NCH > 6) stage_a<P, MASS, T, QX, 6>(Box, NB, pairs_done, nbat, Y, B0t, W0t, W1t, g0, nq0, nq1, ptid); break;
+                    case 0: stage_a<P, MASS, T, QX, 0>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
+                    case 1: if constexpr (NCH > 1) stage_a<P, MASS, T, QX, 1>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
+                    case 2: if constexpr (NCH > 2) stage_a<P, MASS, T, QX, 2>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
+                    case 3: if constexpr (NCH > 3) stage_a<P, MASS, T, QX, 3>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
+                    case 4: if constexpr (NCH > 4) stage_a<P, MASS, T, QX, 4>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
+                    case 5: if constexpr (NCH > 5) stage_a<P, MASS, T, QX, 5>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
+                    case 6: if constexpr (NCH > 6) stage_a<P, MASS, T, QX, 6>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
                     default: break;
                     }
                     bar_sync(1, NPRO);  // the batch's boxes consumed, Y written
@@ -376,45 +380,46 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                             tma_load_4d(Box + b * CF::BOXD, &tm, &full[b], (int)a.qoff + 2 * (pp + NB), ql1, ql0, 0);
                         }
                     }
-                    // stage B for the batch: items (plane j, t0, family g) -> G ring, + the planes' B2 pairs
+                    // stage B for the batch: items (plane j, t1 of the chunk, family g), contracting c0 for
+                    // every t0 -> G ring (column t0 + K t1l), + the planes' B2 pairs
                     const int nitem = (a.abl & 2) ? 0 : nbat * 2 * NGF * T;
                     for (int x = ptid; x < nitem; x += NPRO) {
                         const int g = x % NGF, tl = (x / NGF) % T, j = x / (NGF * T);
                         const int k = j >> 1, pt = j & 1;
                         const int q = 2 * (pairs_done + k) + pt;  // local point
                         const double *Yk = Y + k * CF::YPAIR + pt * CF::NCHAIN * QX * T;
+                        double *G = Ring + (size_t)(q % NS) * CF::SLOT;
                         double acc[K];
                         #pragma unroll
                         for (int t = 0; t < K; ++t) acc[t] = 0.0;
                         if constexpr (MASS) {
-                            staircase<P, kIntB && QX == 2 * P + 1>(g1, [&](int c1, auto O) {
+                            staircase<P, kIntB && QX == 2 * P + 1>(g0, [&](int c0, auto O) {
                                 constexpr int o = decltype(O)::value;
-                                const double yv = Yk[c1 * T + tl];
-                                const double2 *bp = B1t + c1 * NP;
+                                const double yv = Yk[c0 * T + tl];
+                                const double2 *bp = B0t + c0 * NP;
                                 #pragma unroll
                                 for (int r = 0; r <= P; ++r) acc[o + r] = fma(bp[r].x, yv, acc[o + r]);
                             });
                         } else {
-                            // g = a2 + 2 b2: b2 = 0 sums chains m = 0 (B1 values) and m = 1 (B1
-                            // derivatives), b2 = 1 is chain m = 2 (B1 values)
+                            // g = a2 + 2 b2: b2 = 0 sums chains m = 1 (B0 values) and m = 0 (B0
+                            // derivatives), b2 = 1 is chain m = 2 (B0 values)
                             const int a2 = g & 1, b2 = g >> 1;
-                            const double *Ya = Yk + ((b2 ? 4 : 0) + a2) * QX * T;
-                            const double *Yb = Yk + (2 + a2) * QX * T;
-                            staircase<P, kIntB && QX == 2 * P + 1>(g1, [&](int c1, auto O) {
+                            const double *Ya = Yk + ((b2 ? 4 : 2) + a2) * QX * T;
+                            const double *Yb = Yk + a2 * QX * T;
+                            staircase<P, kIntB && QX == 2 * P + 1>(g0, [&](int c0, auto O) {
                                 constexpr int o = decltype(O)::value;
-                                const double ya = Ya[c1 * T + tl];
-                                const double yb = b2 ? 0.0 : Yb[c1 * T + tl];
-                                const double2 *bp = B1t + c1 * NP;
+                                const double ya = Ya[c0 * T + tl];
+                                const double yb = b2 ? 0.0 : Yb[c0 * T + tl];
+                                const double2 *bp = B0t + c0 * NP;
                                 #pragma unroll
                                 for (int r = 0; r <= P; ++r) acc[o + r] = fma(bp[r].y, yb, fma(bp[r].x, ya, acc[o + r]));
                             });
                         }
-                        double *G = Ring + (size_t)(q % NS) * CF::SLOT;
                         #pragma unroll
                         for (int t = 0; t < K; ++t) {
                             // ring slot [b2][column][a2] (stage C loads (a2 = 0, 1) pairs with a 16-B
                             // lane stride: conflict-free)
-                            const int cl = tl + T * t;
+                            const int cl = t + K * tl;
                             if constexpr (MASS) G[cl] = acc[t];
                             else G[((g >> 1) * COLS + cl) * 2 + (g & 1)] = acc[t];
                         }
@@ -539,9 +544,9 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                     #pragma unroll
                     for (int j = 0; j < CPT; ++j) {
                         const int cl = cl0 + j * NCP;
-                        const int tl = cl % T, t1 = cl / T, tg = ta + tl;
-                        if (cl < COLS && tl < tn && tg < ni0 && t1 < ni1) {
-                            const int64_t e0 = row + tg + (int64_t)ni0 * t1;
+                        const int t0 = cl % K, tl = cl / K, t1 = ta + tl;  // chunks over t1: whole t0 runs
+                        if (cl < COLS && tl < tn && t0 < ni0 && t1 < ni1) {
+                            const int64_t e0 = row + t0 + (int64_t)ni0 * t1;
                             double *vp = a.val + e0;  // pointer walk: one 64-bit add per store
                             #pragma unroll
                             for (int t = 0; t < K; ++t) {
@@ -549,7 +554,7 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                                 vp += stp;
                             }
                             if (a.col) {
-                                const int jb = (jl0 + tg) + (int)a.n0 * ((jl1 + t1) + (int)a.n1 * jlo2[rr]);
+                                const int jb = (jl0 + t0) + (int)a.n0 * ((jl1 + t1) + (int)a.n1 * jlo2[rr]);
                                 const int js = (int)(a.n0 * a.n1);
                                 int32_t *cp = a.col + e0;
                                 #pragma unroll
@@ -562,8 +567,104 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                     }
                 }
             };
+            // stage C, rolled form: one loop over the staircase offsets o = 0..p with the row's
+            // accumulators as a sliding window win[r] <-> t2 = o + r (offsets are non-decreasing in c,
+            // so t2 = o is final once group o is done: stored, and the window shifts by one).  The
+            // loop body is one point: a few hundred bytes of code for every row type, instead of
+            // the fully unrolled staircases (instruction-cache misses were the top stall of both
+            // thread groups at p = 8).
+            auto stage_c_roll = [&]() {
+                constexpr int CPT = CF::CPT, NCP = (COLS + CPT - 1) / CPT;
+                const int stp = ni0 * ni1;
+                for (int x = ctid; x < nr * NCP; x += NCON) {
+                    const int rho = x / NCP, cl0 = x % NCP;  // columns cl0 + j NCP
+                    const int rr = r0 + rho;
+                    const int q0 = qlo2[rr], s0 = q0 % NS;
+                    const double *Wr = W2p + rho * CF::QR * 4;
+                    const int *gg = g2p + rho * (NP + 1);
+                    const int ni2 = jlen2[rr];
+                    const int64_t row = pref2[rr] * a.L1 * a.L0 + (int64_t)ni2 * (p1L0 + p0n1) - a.val_base;
+                    int clc[CPT];
+                    bool ok[CPT];
+                    double *vp[CPT];
+                    int32_t *cp[CPT];
+                    int jb[CPT];
+                    #pragma unroll
+                    for (int j = 0; j < CPT; ++j) {
+                        const int cl = cl0 + j * NCP;
+                        clc[j] = cl < COLS ? cl : COLS - 1;
+                        const int t0 = cl % K, tl = cl / K, t1 = ta + tl;
+                        ok[j] = cl < COLS && tl < tn && t0 < ni0 && t1 < ni1;
+                        const int64_t e0 = row + t0 + (int64_t)ni0 * t1;
+                        vp[j] = a.val + e0;
+                        cp[j] = a.col ? a.col + e0 : nullptr;
+                        jb[j] = (jl0 + t0) + (int)a.n0 * ((jl1 + t1) + (int)a.n1 * jlo2[rr]);
+                    }
+                    const int js = (int)(a.n0 * a.n1);
+                    double win[CPT][NP];
+                    #pragma unroll
+                    for (int j = 0; j < CPT; ++j)
+                        #pragma unroll
+                        for (int r = 0; r < NP; ++r) win[j][r] = 0.0;
+                    auto put = [&](int t, int j, double v) {  // value (and column) of t2 = jlo + t
+                        if (ok[j] && t < ni2) {
+                            vp[j][(int64_t)stp * t] = v;
+                            if (cp[j]) cp[j][(int64_t)stp * t] = jb[j] + js * t;
+                        }
+                    };
+                    int c = 0;
+                    for (int o = 0; o <= P; ++o) {
+                        const int ce = gg[o + 1];
+                        for (; c < ce; ++c) {
+                            const int s = s0 + c < NS ? s0 + c : s0 + c - NS;  // c < #Q <= NS
+                            const double2 *bp = RB2 + s * NP;
+                            const double *Gs = Ring + (size_t)s * CF::SLOT;
+                            if constexpr (MASS) {
+                                const double wv = Wr[c * 4];
+                                double uu[CPT];
+                                #pragma unroll
+                                for (int j = 0; j < CPT; ++j) uu[j] = wv * Gs[clc[j]];
+                                #pragma unroll
+                                for (int r = 0; r <= P; ++r) {
+                                    const double bx = bp[r].x;
+                                    #pragma unroll
+                                    for (int j = 0; j < CPT; ++j) win[j][r] = fma(bx, uu[j], win[j][r]);
+                                }
+                            } else {
+                                const double4 w = *(const double4 *)(Wr + c * 4);
+                                double u0[CPT], u1[CPT];
+                                #pragma unroll
+                                for (int j = 0; j < CPT; ++j) {
+                                    const double2 Ga = *(const double2 *)(Gs + clc[j] * 2);
+                                    const double2 Gb = *(const double2 *)(Gs + (COLS + clc[j]) * 2);
+                                    u0[j] = fma(w.x, Ga.x, w.y * Ga.y);
+                                    u1[j] = fma(w.z, Gb.x, w.w * Gb.y);
+                                }
+                                #pragma unroll
+                                for (int r = 0; r <= P; ++r) {
+                                    const double2 b2 = bp[r];
+                                    #pragma unroll
+                                    for (int j = 0; j < CPT; ++j) win[j][r] = fma(b2.y, u1[j], fma(b2.x, u0[j], win[j][r]));
+                                }
+                            }
+                        }
+                        #pragma unroll
+                        for (int j = 0; j < CPT; ++j) {
+                            put(o, j, win[j][0]);
+                            #pragma unroll
+                            for (int r = 0; r < P; ++r) win[j][r] = win[j][r + 1];
+                            win[j][P] = 0.0;
+                        }
+                    }
+                    #pragma unroll
+                    for (int r = 0; r < P; ++r)
+                        #pragma unroll
+                        for (int j = 0; j < CPT; ++j) put(P + 1 + r, j, win[j][r]);
+                }
+            };
             if (a.abl & 1) {
-            } else if (kIntC && all_int) stage_c(std::true_type{});
+            } else if (a.rollc) stage_c_roll();
+            else if (kIntC && all_int) stage_c(std::true_type{});
             else stage_c(std::false_type{});
             // this step's ring slots may be overwritten.  Relaxed: every value this thread read from
             // the ring fed the accumulators of the stores it has already issued, so the reads are
@@ -727,6 +828,9 @@ wq_status launch_cls(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, const
     // three or more (p = 8 stiffness 155 -> 298 ms)
     a.cl = NCH == 2 && !getenv("WQ_ZHP_NOCLUSTER");
     a.abl = getenv("WQ_ZHP_ABLATE") ? atoi(getenv("WQ_ZHP_ABLATE")) : 0;
+    // measured (C4): the rolled stage C pays from p = 8 on (p = 8 161 -> 132 ms, p = 9 312 -> 226 ms)
+    // and is neutral below; a rolled stage B was slower at every degree
+    a.rollc = getenv("WQ_ZHP_ROLLC") ? atoi(getenv("WQ_ZHP_ROLLC")) : (P >= 8);
     cfg.numAttrs = a.cl ? 1 : 0;
     ce = cudaLaunchKernelEx(&cfg, k_zhp<P, MASS, T, QX>, m, a);
     wq_count_launches(1);
