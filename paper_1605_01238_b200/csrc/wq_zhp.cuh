@@ -99,7 +99,7 @@ struct Args {
     int32_t *col;
     int64_t val_base;
     int cl;                  // launched as clusters of the NCH chunk CTAs of a line (lockstep per step)
-    int rollc;               // stage C in the rolled sliding-window form (env WQ_ZHP_ROLLC; default p >= 8)
+    int rollc;               // stage C in the rolled sliding-window form (env WQ_ZHP_ROLLC; default p >= 6)
     int abl;                 // measurement switch (env WQ_ZHP_ABLATE), bits: 1 = no stage C, 2 = no stages A, B, 4 = no box loads
 };
 
@@ -573,7 +573,9 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
             // loop body is one point: a few hundred bytes of code for every row type, instead of
             // the fully unrolled staircases (instruction-cache misses were the top stall of both
             // thread groups at p = 8).
-            auto stage_c_roll = [&]() {
+            auto stage_c_roll = [&](auto IC) {
+                constexpr bool INTC = decltype(IC)::value;  // every row of the step interior: groups
+                                                           // {0}, {1, 2}, .., {2p-1, 2p}
                 constexpr int CPT = CF::CPT, NCP = (COLS + CPT - 1) / CPT;
                 const int stp = ni0 * ni1;
                 for (int x = ctid; x < nr * NCP; x += NCON) {
@@ -612,10 +614,7 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                             if (cp[j]) cp[j][(int64_t)stp * t] = jb[j] + js * t;
                         }
                     };
-                    int c = 0;
-                    for (int o = 0; o <= P; ++o) {
-                        const int ce = gg[o + 1];
-                        for (; c < ce; ++c) {
+                    auto point = [&](int c) {
                             const int s = s0 + c < NS ? s0 + c : s0 + c - NS;  // c < #Q <= NS
                             const double2 *bp = RB2 + s * NP;
                             const double *Gs = Ring + (size_t)s * CF::SLOT;
@@ -647,6 +646,14 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                                     for (int j = 0; j < CPT; ++j) win[j][r] = fma(b2.y, u1[j], fma(b2.x, u0[j], win[j][r]));
                                 }
                             }
+                    };
+                    int c = 0;
+                    for (int o = 0; o <= P; ++o) {
+                        if constexpr (INTC) {
+                            if (o == 0) point(0);
+                            else { point(2 * o - 1); point(2 * o); }
+                        } else {
+                            for (const int ce = gg[o + 1]; c < ce; ++c) point(c);
                         }
                         #pragma unroll
                         for (int j = 0; j < CPT; ++j) {
@@ -663,7 +670,10 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                 }
             };
             if (a.abl & 1) {
-            } else if (a.rollc) stage_c_roll();
+            } else if (a.rollc) {
+                if (all_int) stage_c_roll(std::true_type{});
+                else stage_c_roll(std::false_type{});
+            }
             else if (kIntC && all_int) stage_c(std::true_type{});
             else stage_c(std::false_type{});
             // this step's ring slots may be overwritten.  Relaxed: every value this thread read from
@@ -828,9 +838,10 @@ wq_status launch_cls(wq_plan_s *Pl, const int32_t *lines, int64_t n_lines, const
     // three or more (p = 8 stiffness 155 -> 298 ms)
     a.cl = NCH == 2 && !getenv("WQ_ZHP_NOCLUSTER");
     a.abl = getenv("WQ_ZHP_ABLATE") ? atoi(getenv("WQ_ZHP_ABLATE")) : 0;
-    // measured (C4): the rolled stage C pays from p = 8 on (p = 8 161 -> 132 ms, p = 9 312 -> 226 ms)
-    // and is neutral below; a rolled stage B was slower at every degree
-    a.rollc = getenv("WQ_ZHP_ROLLC") ? atoi(getenv("WQ_ZHP_ROLLC")) : (P >= 8);
+    // measured (C4): the rolled stage C pays from p = 6 on (stiffness p = 7 74 -> 69 ms, p = 8 161 ->
+    // 129, p = 9 312 -> 227; mass p = 6 14.1 -> 13.2, p = 10 133 -> 121) and is neutral below; a
+    // rolled stage B was slower at every degree
+    a.rollc = getenv("WQ_ZHP_ROLLC") ? atoi(getenv("WQ_ZHP_ROLLC")) : (P >= 6);
     cfg.numAttrs = a.cl ? 1 : 0;
     ce = cudaLaunchKernelEx(&cfg, k_zhp<P, MASS, T, QX>, m, a);
     wq_count_launches(1);
