@@ -78,7 +78,13 @@ struct Cfg {
     static constexpr int YPAIR = 2 * NCHAIN * QX * T;  // doubles of Y per pair [pt][chain][c1][t0]
     static constexpr int SLOT = COLS * NGF;       // doubles of a G ring slot [col][family]
     static constexpr int QR = 3 * P + 1;          // max #Q of a row (n_EL >= p+2)
-    static constexpr int CPT = 2 * P + 1 <= 17 ? 2 : 1;  // stage-C columns per consumer thread
+#ifdef WQ_ZHP_CPT
+    static constexpr int CPT = WQ_ZHP_CPT;
+#else
+    // stage-C columns per consumer thread (measured, C4: stiffness p = 8 129 -> 112 ms with one column,
+    // mass p = 6 13.2 -> 11.5 ms with three, p = 10 121 -> 100 ms with two)
+    static constexpr int CPT = MASS ? (P == 5 || P == 6 ? 3 : 2) : (P >= 8 ? 1 : 2);
+#endif
 };
 
 struct Args {
