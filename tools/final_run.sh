@@ -10,3 +10,10 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_zl
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_zhp -c 2 -o gpurun_out/final/zhp_p8 python tools/run_step.py --p 8 --steps 1 > gpurun_out/final/ncu_zhp.log 2>&1; tail -1 gpurun_out/final/ncu_zhp.log
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_coefz|k_dnet" -c 2 -o gpurun_out/final/coef_p4 python tools/run_step.py --p 4 --steps 1 > gpurun_out/final/ncu_coef.log 2>&1; tail -1 gpurun_out/final/ncu_coef.log
 timeout 600 python studies/convergence_1d.py --out gpurun_out/final/convergence_1d.json > /dev/null 2>&1; ls -la gpurun_out/final/convergence_1d.json
+timeout 900 python tools/time_step.py --p 4 --reps 7 > gpurun_out/final/time_step_p4.json 2>&1
+timeout 1800 python tools/time_kernels.py --p 2,3,4,5,6,7,8,9,10 --kernels 0 --reps 3 > gpurun_out/final/time_kernels_stiff.jsonl 2>&1
+timeout 1800 python tools/time_kernels.py --p 2,3,4,5,6,7,8,9,10 --kernels 0 --reps 3 --matrix mass > gpurun_out/final/time_kernels_mass.jsonl 2>&1
+timeout 1800 python tools/time_slab.py --p 4 > gpurun_out/final/slab_c4p4.jsonl 2>&1
+timeout 1800 python tools/time_slab.py --p 8 --reps 2 > gpurun_out/final/slab_c4p8.jsonl 2>&1
+timeout 1800 python tools/time_slab.py --config C5 --p 4 --reps 2 > gpurun_out/final/slab_c5.jsonl 2>&1
+ls -la gpurun_out/final/
