@@ -114,8 +114,10 @@ struct ZCfg {
     static constexpr int YB = (QX * T0C * 2 + 4 + 15) / 16 * 16;
     __host__ __device__ static constexpr int yoff(int bi) { return bi * YB + (bi == 1 || bi == 3 ? 2 : (bi >= 4 ? 4 : 0)); }
     static constexpr int YTOT = 6 * YB;
-    // Y over the consumed box when stage A is one pass over interior fibres, else its own buffer
-    static constexpr bool YSEP = BND || NPASS > 1;
+    // Y in its own buffer (the box is then only read through the generic proxy and its next TMA load
+    // needs no proxy fence, and it can be issued right after stage A: C4 p = 4 5.52 -> 5.45 ms), except
+    // for the 4-point tasks of p = 2, where Y goes over the consumed box
+    static constexpr bool YSEP = BND || NPASS > 1 || P >= 3;
     static constexpr int BOXD = YSEP ? (6 * QX * QX * PTS + 15) / 16 * 16
                                      : ((6 * QX * QX * PTS > YTOT * (PTS / 2) ? 6 * QX * QX * PTS : YTOT * (PTS / 2)) + 15) / 16 * 16;
     static constexpr int YD = YSEP ? YTOT : 0;
@@ -412,6 +414,7 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             w1u0 = u.w[1][c1][m == 1 ? 2 : 0];
             w1u1 = u.w[1][c1][m == 1 ? 3 : 1];
         }
+
         int cq0 = QI, cq1 = QI, ty0 = 0, ty1 = 0, sh0 = 0, sh1 = 0;
         int use = 0;
         for (int64_t T = wp; T < n_tasks; T += NWP, ++use) {
@@ -562,8 +565,9 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             }
             __syncwarp();
             if constexpr (YSEP) {
-                // the box is consumed (Y has its own buffer): start the next task's box load now
-                fence_async_smem();
+                // the box is consumed (Y has its own buffer): start the next task's box load now.  The
+                // box was only read through the generic proxy (no cross-proxy write to order), and
+                // every lane's reads have completed (their values fed stage A) before the __syncwarp
                 if (lane == 0) issue(b);
             }
             // ---------------- stage B: lane (g, t0): acc[x][pt][t1] over the Y blocks x = 0, 1
@@ -681,7 +685,16 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
     const int mq2 = v2.maxq;
     // W2 rows of a batch are contiguous in global memory ([i][c][f]): one bulk copy per batch,
     // prefetched one batch ahead into a double buffer
+    // a batch whose rows all take the uniform rules (CU) reads no W2 rows: no copy and no wait (the
+    // issue and the wait side take the same decision per batch, so the buffer phases stay paired;
+    // C4 p = 4 5.64 -> 5.39 ms)
+    auto w2_need = [&](int r0) {
+        if (!CU) return true;
+        const int nr = n2l - r0 < NR ? n2l - r0 : NR;
+        return !(i2b + r0 >= 2 * P && i2b + r0 + nr - 1 <= (int)v2.n - 1 - 2 * P);
+    };
     auto w2_issue = [&](int r0, int buf) {
+        if (!w2_need(r0)) return;
         const int nr = n2l - r0 < NR ? n2l - r0 : NR;
         const unsigned bytes = (unsigned)(nr * mq2 * 32);
         mbar_arrive_tx(&wfull[cw * 2 + buf], bytes);
@@ -730,8 +743,10 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
             const int rl = r0 + nr - 1;
             const uint32_t t_hi = Tbase + (uint32_t)((qlo2[rl] + qlen2[rl] - 1) / PTS);
             const uint32_t t_lo = Tbase + (uint32_t)(qlo2[r0] / PTS);
-            zwait(&wfull[cw * 2 + wbuf], wuse[wbuf] & 1, wt2);
-            ++wuse[wbuf];
+            if (w2_need(r0)) {
+                zwait(&wfull[cw * 2 + wbuf], wuse[wbuf] & 1, wt2);
+                ++wuse[wbuf];
+            }
             const double2 *W2w = (const double2 *)(W2b + wbuf * CF::W2D);  // [row][c][2] double2, row stride mq2
             if (lane == 0) {
                 int nxt = r0 + NWC * NR;

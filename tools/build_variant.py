@@ -1,4 +1,4 @@
-"""Measurement builds: recompile the ZHP degree files with extra -D flags and link a variant library
+"""Measurement builds: recompile the ZHP degree files (or the files matching $WQ_VARIANT_SRC) with extra -D flags and link a variant library
 paper_1605_01238_b200/build/libwq_<name>.so (load it with WQ_LIB_DEBUG_PATH=...).  Needs a prior
 full build (the other objects are reused)."""
 import glob
@@ -17,7 +17,7 @@ objdir = os.path.join(pkg, "build")
 vdir = os.path.join(objdir, name)
 os.makedirs(vdir, exist_ok=True)
 flags = [f for f in g.NVCC_FLAGS if f != "-shared"] + ["-D" + d for d in defs]
-zsrc = sorted(glob.glob(os.path.join(pkg, "csrc", "wq_zhp_deg*.cu")))
+zsrc = sorted(glob.glob(os.path.join(pkg, "csrc", os.environ.get("WQ_VARIANT_SRC", "wq_zhp_deg*.cu"))))
 
 
 def one(src):

@@ -44,6 +44,48 @@ __global__ void k_dmma(double *out, int iters) {
     if (s == 12345.678) out[0] = s;
 }
 
+// mixed: warps 0-3 of a CTA run the DFMA loop (mode bit 1), warps 4-7 the DMMA loop (mode bit 2);
+// each SM sub-partition then holds one warp of each kind.  Comparing the time of mode 3 with
+// modes 1 and 2 tells whether DFMA and DMMA share one FP64 pipe (time adds) or not (time = max).
+__global__ void k_mixed(double *out, int iters_f, int iters_m, int mode) {
+    const int w = threadIdx.x >> 5;
+    if (w < 4) {
+        if (!(mode & 1)) return;
+        double x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+        for (int it = 0; it < iters_f; ++it) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) x[k] = fma(x[k], 0.999, 1e-9);
+        }
+        double s = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s += x[k];
+        if (s == 12345.678) out[0] = s;
+    } else {
+        if (!(mode & 2)) return;
+        double a = threadIdx.x * 1e-3, b = 0.999;
+        double c[4][2];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[k][0] = c[k][1] = 0.0;
+        for (int it = 0; it < iters_m; ++it) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                 : "+d"(c[k][0]), "+d"(c[k][1])
+                                 : "d"(a), "d"(b));
+        }
+        double s = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) s += c[k][0] + c[k][1];
+        if (s == 12345.678) out[0] = s;
+    }
+}
+
 int main() {
     double *out;
     cudaMalloc(&out, 8);
@@ -75,6 +117,21 @@ int main() {
         cudaEventElapsedTime(&ms, e0, e1);
         double fl = 2.0 * 256.0 * (blocks * threads / 32) * (double)iters * 8 * 4;  // 8x8x4 FMA per mma
         printf("{\"kernel\":\"dmma_m8n8k4\",\"ctas_per_sm\":%d,\"ms\":%.3f,\"tflops\":%.2f}\n", occ, ms, fl / ms / 1e9);
+    }
+    for (int occ : {1, 2}) {
+        const int blocks = sms * occ, threads = 256, itf = 4000, itm = 1000;
+        for (int mode : {1, 2, 3}) {
+            k_mixed<<<blocks, threads>>>(out, 50, 20, mode);
+            cudaEventRecord(e0);
+            k_mixed<<<blocks, threads>>>(out, itf, itm, mode);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            double ff = (mode & 1) ? 2.0 * blocks * 128 * (double)itf * 16 * 8 : 0.0;
+            double fm = (mode & 2) ? 2.0 * 256.0 * (blocks * 4) * (double)itm * 8 * 4 : 0.0;
+            printf("{\"kernel\":\"mixed\",\"mode\":%d,\"ctas_per_sm\":%d,\"ms\":%.3f,\"tflops\":%.2f}\n", mode, occ, ms, (ff + fm) / ms / 1e9);
+        }
     }
     cudaError_t e = cudaGetLastError();
     printf("{\"status\":\"%s\"}\n", cudaGetErrorString(e));

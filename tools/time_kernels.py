@@ -52,7 +52,7 @@ for p in [int(x) for x in a.p.split(",")]:
             ref = v
         print(json.dumps({"cfg": cfg.name, "p": p, "mat": a.matrix, "kernel": wq.KERNEL_NAMES[k] if k else "auto:" + wq.KERNEL_NAMES[plan.info["kernel"][mat]], "ms": round(ms, 3),
                           "nnz": nnz, "Gnnz_s": round(nnz / ms / 1e6, 1), "GBs": round(12 * nnz / ms / 1e6, 1),
-                          "hbm_frac": round(12 * nnz / ms / 1e6 / 6552.6, 3), "rel_diff_vs_first": diff}), flush=True)
+                          "hbm_frac": round(12 * nnz / ms / 1e6 / 6552.6, 3), "rel_diff_vs_first": diff, "csum": float(v.sum())}), flush=True)
     plan.close()
     del rp, col, val
     torch.cuda.empty_cache()
