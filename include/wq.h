@@ -91,7 +91,9 @@ typedef enum {
     WQ_KERNEL_TILE = 2,   /* sum-factorised row-tile kernel (Eq.
                              sumfactorization P:837): lines of rows along
                              direction 1 share the direction-3/2 stages        */
-    WQ_KERNEL_ZLINE = 3,  /* d = 3, 2 <= p <= 6, stiffness: lines along
+    WQ_KERNEL_ZLINE = 3,  /* d = 3, 2 <= p <= 6, stiffness, n_EL >= p+2 in
+                             every direction (the 2p+3 row staircase types it
+                             compiles in; else WQ_EINVAL): lines along
                              direction 3 (rows share the direction-1/2 mode
                              products, the direction-3 product per row),
                              warp-specialised TMA pipeline, direct coalesced
