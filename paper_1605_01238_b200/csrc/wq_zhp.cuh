@@ -78,6 +78,15 @@ struct Cfg {
     static constexpr int YPAIR = 2 * NCHAIN * QX * T;  // doubles of Y per pair [pt][chain][c1][t0]
     static constexpr int SLOT = COLS * NGF;       // doubles of a G ring slot [col][family]
     static constexpr int QR = 3 * P + 1;          // max #Q of a row (n_EL >= p+2)
+#ifdef WQ_ZHP_SPA
+    static constexpr bool SPA = WQ_ZHP_SPA;
+#else
+    // stage-A threads per pair fibre: one per point for the mass matrix at 4 <= p <= 8, where a batch
+    // has few fibres (#Q_0 per pair) for the 256 producer threads (measured, C4: p = 4 5.93 -> 5.76 ms,
+    // p = 8 37.2 -> 36.6; slower at p = 10 and for the stiffness matrix, whose three fibres per c0
+    // fill the threads better and whose 16-B loads serve both points: p = 8 113 -> 138 ms)
+    static constexpr bool SPA = MASS && P >= 4 && P <= 8;
+#endif
 #ifdef WQ_ZHP_CPT
     static constexpr int CPT = WQ_ZHP_CPT;
 #else
@@ -174,45 +183,64 @@ __device__ __forceinline__ void staircase(const int *g, F &&f) {
 // stage A of the pairs pp0 .. pp0 + nbat - 1 (box of pair pp in buffer pp % nb, Y of batch pair k):
 // contracts c1 for the chunk's t1 range; a thread = fibre (m, c0) of one pair, both points (the box
 // holds the pair's points side by side, so one 16-B load serves both and the tables are loaded once
-// per two points)
-template <int P, bool MASS, int T, int QX, int CH>
+// per two points), or with SPA one point of the pair (twice the threads, half the serial work per
+// thread: at high degree a batch has fewer fibres than producer threads)
+template <int P, bool MASS, int T, int QX, int CH, bool SPA>
 __device__ __forceinline__ void stage_a(const double *Boxes, int nb, int pp0, int nbat, double *Yall,
                                         const double2 *B1t, const double *W0t, const double *W1t, const int *g1,
                                         int nq0, int tid) {
     using CF = Cfg<P, MASS, T, QX>;
     constexpr int TA = Chunks<P>::ta(CH), TN = Chunks<P>::tn(CH);  // t1 range of the chunk
+    constexpr int NPT = SPA ? 1 : 2;                                // points per thread
     const int nfib = (MASS ? 1 : 3) * nq0;
-    for (int fx = tid; fx < nbat * nfib; fx += NPRO) {
-        const int k = fx / nfib, f = fx % nfib;
+    const int nit = nfib * (SPA ? 2 : 1);
+    for (int fx = tid; fx < nbat * nit; fx += NPRO) {
+        const int k = fx / nit, f0 = fx % nit;
+        const int pt0 = SPA ? f0 / nfib : 0, f = SPA ? f0 - pt0 * nfib : f0;
         const double *box = Boxes + ((pp0 + k) % nb) * CF::BOXD;
         double *Y = Yall + k * CF::YPAIR;
         const int c0 = f % nq0, m = f / nq0;
-        double y0[2][T], y1[2][T];
+        // the thread's points of the box entry at e (both points, or point pt0)
+        auto ld = [&](int e, double (&v)[NPT]) {
+            if constexpr (SPA) {
+                v[0] = box[e * 2 + pt0];
+            } else {
+                const double2 w = *(const double2 *)(box + e * 2);
+                v[0] = w.x;
+                v[1] = w.y;
+            }
+        };
+        double y0[NPT][T], y1[NPT][T];
         #pragma unroll
-        for (int t = 0; t < T; ++t) { y0[0][t] = 0.0; y0[1][t] = 0.0; y1[0][t] = 0.0; y1[1][t] = 0.0; }
+        for (int t = 0; t < T; ++t)
+            #pragma unroll
+            for (int h = 0; h < NPT; ++h) { y0[h][t] = 0.0; y1[h][t] = 0.0; }
         if constexpr (MASS) {
             const double w0 = W0t[c0 * 4 + 0];
             staircase<P, kIntA && QX == 2 * P + 1>(g1, [&](int c1, auto O) {
                 constexpr int o = decltype(O)::value;
-                const double2 cv = *(const double2 *)(box + (c0 * QX + c1) * 2);
+                double cv[NPT];
+                ld(c0 * QX + c1, cv);
                 const double s = W1t[c1 * 4 + 0] * w0;
-                const double ha = s * cv.x, hb = s * cv.y;
+                double ha[NPT];
+                #pragma unroll
+                for (int h = 0; h < NPT; ++h) ha[h] = s * cv[h];
                 const double2 *bp = B1t + c1 * CF::NP;
                 #pragma unroll
                 for (int r = 0; r <= P; ++r) {
                     const int t = o + r - TA;
                     if (t >= 0 && t < TN) {
                         const double bv = bp[r].x;
-                        y0[0][t] = fma(bv, ha, y0[0][t]);
-                        y0[1][t] = fma(bv, hb, y0[1][t]);
+                        #pragma unroll
+                        for (int h = 0; h < NPT; ++h) y0[h][t] = fma(bv, ha[h], y0[h][t]);
                     }
                 }
             });
             #pragma unroll
-            for (int pt = 0; pt < 2; ++pt) {
-                double *Yo = Y + ((pt * CF::NCHAIN + 0) * QX + c0) * T;
+            for (int h = 0; h < NPT; ++h) {
+                double *Yo = Y + (((pt0 + h) * CF::NCHAIN + 0) * QX + c0) * T;
                 #pragma unroll
-                for (int t = 0; t < T; ++t) Yo[t] = y0[pt][t];
+                for (int t = 0; t < T; ++t) Yo[t] = y0[h][t];
             }
         } else {
             // components C00 C01 C02 C11 C12 C22: ka = C_2m, kb = C_0m, kc = C_1m
@@ -226,30 +254,35 @@ __device__ __forceinline__ void stage_a(const double *Boxes, int nb, int pp0, in
                 constexpr int o = decltype(O)::value;
                 const double2 w1p = *(const double2 *)(W1t + c1 * 4 + w1o);  // (w1^(0,b1), w1^(1,b1))
                 const double s1 = w0p.x * w1p.x, s2 = w0p.y * w1p.x, s3 = w0p.x * w1p.y;
-                const double2 ca = *(const double2 *)(box + ((ka * QX + c0) * QX + c1) * 2);
-                const double2 cb = *(const double2 *)(box + ((kb * QX + c0) * QX + c1) * 2);
-                const double2 cc = *(const double2 *)(box + ((kc * QX + c0) * QX + c1) * 2);
-                const double h1a = s1 * ca.x, h1b = s1 * ca.y;                                // a2 = 1 (l = 2)
-                const double h0a = fma(s2, cb.x, s3 * cc.x), h0b = fma(s2, cb.y, s3 * cc.y);  // a2 = 0 (l = 0, 1)
+                double ca[NPT], cb[NPT], cc[NPT], h1[NPT], h0[NPT];
+                ld((ka * QX + c0) * QX + c1, ca);
+                ld((kb * QX + c0) * QX + c1, cb);
+                ld((kc * QX + c0) * QX + c1, cc);
+                #pragma unroll
+                for (int h = 0; h < NPT; ++h) {
+                    h1[h] = s1 * ca[h];                    // a2 = 1 (l = 2)
+                    h0[h] = fma(s2, cb[h], s3 * cc[h]);    // a2 = 0 (l = 0, 1)
+                }
                 const double2 *bp = B1t + c1 * CF::NP;
                 #pragma unroll
                 for (int r = 0; r <= P; ++r) {
                     const int t = o + r - TA;
                     if (t >= 0 && t < TN) {
                         const double bv = der1 ? bp[r].y : bp[r].x;
-                        y0[0][t] = fma(bv, h0a, y0[0][t]);
-                        y0[1][t] = fma(bv, h0b, y0[1][t]);
-                        y1[0][t] = fma(bv, h1a, y1[0][t]);
-                        y1[1][t] = fma(bv, h1b, y1[1][t]);
+                        #pragma unroll
+                        for (int h = 0; h < NPT; ++h) {
+                            y0[h][t] = fma(bv, h0[h], y0[h][t]);
+                            y1[h][t] = fma(bv, h1[h], y1[h][t]);
+                        }
                     }
                 }
             });
             #pragma unroll
-            for (int pt = 0; pt < 2; ++pt) {
-                double *Y0 = Y + ((pt * CF::NCHAIN + m * 2 + 0) * QX + c0) * T;
-                double *Y1 = Y + ((pt * CF::NCHAIN + m * 2 + 1) * QX + c0) * T;
+            for (int h = 0; h < NPT; ++h) {
+                double *Y0 = Y + (((pt0 + h) * CF::NCHAIN + m * 2 + 0) * QX + c0) * T;
+                double *Y1 = Y + (((pt0 + h) * CF::NCHAIN + m * 2 + 1) * QX + c0) * T;
                 #pragma unroll
-                for (int t = 0; t < T; ++t) { Y0[t] = y0[pt][t]; Y1[t] = y1[pt][t]; }
+                for (int t = 0; t < T; ++t) { Y0[t] = y0[h][t]; Y1[t] = y1[h][t]; }
             }
         }
     }
@@ -315,6 +348,7 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
         }
     };
     constexpr unsigned BOX_BYTES = CF::NC * QX * QX * 2 * 8;
+    constexpr bool SPA = CF::SPA;
 
     if (tid < NPRO) {
         // ================================================================ producers
@@ -367,13 +401,13 @@ __global__ void __launch_bounds__(NT, 1) k_zhp(const __grid_constant__ CUtensorM
                         if (!(a.abl & 4)) mbar_wait(&full[b], (use_bits >> b) & 1);
                     }
                     if (!(a.abl & 2)) switch (ch) {
-                    case 0: stage_a<P, MASS, T, QX, 0>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
-                    case 1: if constexpr (NCH > 1) stage_a<P, MASS, T, QX, 1>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
-                    case 2: if constexpr (NCH > 2) stage_a<P, MASS, T, QX, 2>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
-                    case 3: if constexpr (NCH > 3) stage_a<P, MASS, T, QX, 3>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
-                    case 4: if constexpr (NCH > 4) stage_a<P, MASS, T, QX, 4>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
-                    case 5: if constexpr (NCH > 5) stage_a<P, MASS, T, QX, 5>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
-                    case 6: if constexpr (NCH > 6) stage_a<P, MASS, T, QX, 6>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
+                    case 0: stage_a<P, MASS, T, QX, 0, SPA>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
+                    case 1: if constexpr (NCH > 1) stage_a<P, MASS, T, QX, 1, SPA>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
+                    case 2: if constexpr (NCH > 2) stage_a<P, MASS, T, QX, 2, SPA>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
+                    case 3: if constexpr (NCH > 3) stage_a<P, MASS, T, QX, 3, SPA>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
+                    case 4: if constexpr (NCH > 4) stage_a<P, MASS, T, QX, 4, SPA>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
+                    case 5: if constexpr (NCH > 5) stage_a<P, MASS, T, QX, 5, SPA>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
+                    case 6: if constexpr (NCH > 6) stage_a<P, MASS, T, QX, 6, SPA>(Box, NB, pairs_done, nbat, Y, B1t, W0t, W1t, g1, nq0, ptid); break;
                     default: break;
                     }
                     bar_sync(1, NPRO);  // the batch's boxes consumed, Y written
