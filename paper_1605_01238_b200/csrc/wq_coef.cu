@@ -172,28 +172,38 @@ __global__ void __launch_bounds__(NTC) k_coef(CoefArgs a) {
 // else 0, then the coefficient nets: [k][NE], NE = 9 + NNU, entries (m, c) = 3 m + c, 9 = kappa,
 // 9 or 10 = gamma; one thread per control point of the planes k_3 in [k3b, k3b + ntot / (n0 n1)).
 template <int NNU>
-__global__ void k_dnet(const double *__restrict__ P, const double *__restrict__ kap, const double *__restrict__ gam,
-                       double *__restrict__ Q, DirView v0, DirView v1, DirView v2, int p, int64_t k3b, int64_t ntot) {
+__global__ void __launch_bounds__(256) k_dnet(const double *__restrict__ P, const double *__restrict__ kap,
+                                              const double *__restrict__ gam, double *__restrict__ Q, DirView v0,
+                                              DirView v1, DirView v2, int p, int64_t k3b, int64_t ntot) {
     constexpr int NE = 9 + NNU;
-    const int64_t kl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (kl >= ntot) return;
-    const int64_t n0 = v0.n, n1 = v1.n;
-    const int64_t k0 = kl % n0, k1 = (kl / n0) % n1, k2 = k3b + kl / (n0 * n1);
-    const int64_t k = k0 + n0 * (k1 + n1 * k2);
-    const double s0 = k0 >= 1 ? dscale(v0, p, k0) : 0.0;
-    const double s1 = k1 >= 1 ? dscale(v1, p, k1) : 0.0;
-    const double s2 = k2 >= 1 ? dscale(v2, p, k2) : 0.0;
-    double *q = Q + kl * NE;
-    #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        const double cur = P[k * 3 + c];
-        q[0 + c] = k0 >= 1 ? (cur - P[(k - 1) * 3 + c]) * s0 : 0.0;
-        q[3 + c] = k1 >= 1 ? (cur - P[(k - n0) * 3 + c]) * s1 : 0.0;
-        q[6 + c] = k2 >= 1 ? (cur - P[(k - n0 * n1) * 3 + c]) * s2 : 0.0;
+    // the CTA's 256 consecutive control points are written as one contiguous run of 256 NE doubles:
+    // staged in shared memory, then stored with consecutive threads on consecutive words
+    __shared__ double st[256 * NE];
+    const int64_t kb = (int64_t)blockIdx.x * 256;
+    const int64_t kl = kb + threadIdx.x;
+    if (kl < ntot) {
+        const int64_t n0 = v0.n, n1 = v1.n;
+        const int64_t k0 = kl % n0, k1 = (kl / n0) % n1, k2 = k3b + kl / (n0 * n1);
+        const int64_t k = k0 + n0 * (k1 + n1 * k2);
+        const double s0 = k0 >= 1 ? dscale(v0, p, k0) : 0.0;
+        const double s1 = k1 >= 1 ? dscale(v1, p, k1) : 0.0;
+        const double s2 = k2 >= 1 ? dscale(v2, p, k2) : 0.0;
+        double *q = st + threadIdx.x * NE;
+        #pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double cur = P[k * 3 + c];
+            q[0 + c] = k0 >= 1 ? (cur - P[(k - 1) * 3 + c]) * s0 : 0.0;
+            q[3 + c] = k1 >= 1 ? (cur - P[(k - n0) * 3 + c]) * s1 : 0.0;
+            q[6 + c] = k2 >= 1 ? (cur - P[(k - n0 * n1) * 3 + c]) * s2 : 0.0;
+        }
+        int e = 9;
+        if (NNU > 0 && kap) q[e++] = kap[k];
+        if (NNU > 0 && gam) q[e++] = gam[k];
     }
-    int e = 9;
-    if (NNU > 0 && kap) q[e++] = kap[k];
-    if (NNU > 0 && gam) q[e++] = gam[k];
+    __syncthreads();
+    const int64_t nv = (ntot - kb < 256 ? ntot - kb : 256) * NE;
+    double *out = Q + kb * NE;
+    for (int x = threadIdx.x; x < nv; x += 256) out[x] = st[x];
 }
 // Tiled form (p <= 6): CTA = TQF points q_3 x TQM points q_1 of one q_2 plane, the three
 // contractions of the tile in one kernel:

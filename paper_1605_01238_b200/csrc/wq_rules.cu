@@ -175,7 +175,9 @@ __global__ void k_gauss(int n, double *gl) {
         double dP = n == 1 ? 1.0 : n * (x * P1 - P0) / (x * x - 1.0);
         double dx = P1 / dP;
         x -= dx;
-        if (fabs(dx) <= 1e-15 * fabs(x)) break;  // FP64 accurate; the dd Newton steps below finish
+        // FP64 accurate (absolute: the roots lie in (-1, 1), and the middle root of an odd rule is 0,
+        // where a relative test never holds); the dd Newton steps below finish
+        if (fabs(dx) <= 1e-15) break;
     }
     dd X = dd_make(x), Pn, dPn;
     for (int it = 0; it < 3; ++it) {  // dd Newton
