@@ -70,10 +70,24 @@ def test_slab_rowptr_two_ranks(ns, p):
 
 
 def test_slab_cuts_balanced():
+    from paper_1605_01238_b200.dist import plane_cost
     for n, p, w in [(104, 4, 8), (260, 4, 8), (110, 10, 4), (5, 2, 4)]:
-        cuts = slab_cuts(n, p, w)
-        assert cuts[0] == 0 and cuts[-1] == n and all(b < e for b, e in zip(cuts, cuts[1:]))
-        nnz = [slab_nnz([n, n, n], p, b, e) for b, e in zip(cuts, cuts[1:])]
-        assert sum(nnz) == slab_nnz([n, n, n], p, 0, n)
-        if n >= 8 * w:
-            assert max(nnz) / min(nnz) < 1.1
+        for balance in ("cost", "nnz"):
+            cuts = slab_cuts(n, p, w, balance)
+            assert cuts[0] == 0 and cuts[-1] == n and all(b < e for b, e in zip(cuts, cuts[1:]))
+            nnz = [slab_nnz([n, n, n], p, b, e) for b, e in zip(cuts, cuts[1:])]
+            assert sum(nnz) == slab_nnz([n, n, n], p, 0, n)
+            wts = plane_cost(n, p) if balance == "cost" else ni_1d(n, p)
+            per = [wts[b:e].sum() for b, e in zip(cuts, cuts[1:])]
+            if n >= 8 * w:
+                assert max(per) / min(per) < 1.1, (n, p, w, balance, per)
+
+
+def test_plane_cost_counts():
+    """#Q_i of reading R1 (interior 2p+1, boundary p+1+2i) against the oracle's point ranges."""
+    import oracle
+    from paper_1605_01238_b200.dist import nq_1d
+    from wqinputs import uniform_open_knots
+    for p, E in [(2, 9), (4, 12), (6, 15)]:
+        D = oracle.Oracle(p, [uniform_open_knots(p, E)]).direction(0)
+        assert np.array_equal(nq_1d(E + p, p), np.asarray(D["qlen"]))

@@ -19,6 +19,7 @@ ap.add_argument("--p", type=int, default=4)
 ap.add_argument("--config", default="C4")
 ap.add_argument("--world", default="1,2,4,8")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--balance", default="cost", help="slab cuts: cost (default, dist.plane_cost) or nnz")
 a = ap.parse_args()
 cfg = baseline_config(a.config, a.p)
 n = cfg.n_el + cfg.p
@@ -26,7 +27,7 @@ ctrl = cfg.ctrl()
 d_ctrl = torch.from_numpy(ctrl).cuda()
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 for world in [int(x) for x in a.world.split(",")]:
-    cuts = slab_cuts(n, cfg.p, world)
+    cuts = slab_cuts(n, cfg.p, world, a.balance)
     per = []
     for r in range(world):
         plan = wq.Plan(cfg.p, cfg.knots(), ctrl=ctrl, slab=(cuts[r], cuts[r + 1]), need_mass=False)
@@ -53,7 +54,7 @@ for world in [int(x) for x in a.world.split(",")]:
         torch.cuda.empty_cache()
     tmax = max(x[0] for x in per)
     nnz = sum(x[2] for x in per)
-    print(json.dumps({"config": cfg.name, "world": world, "step_ms_max": round(tmax, 3),
+    print(json.dumps({"config": cfg.name, "world": world, "balance": a.balance, "cuts": cuts, "step_ms_max": round(tmax, 3),
                       "step_ms_per_rank": [round(x[0], 3) for x in per],
                       "assemble_ms_per_rank": [round(x[1], 3) for x in per],
                       "nnz_per_s": nnz / tmax * 1e3}), flush=True)
