@@ -352,7 +352,16 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
         for (int64_t i1 = 0; i1 < n1; ++i1)
             for (int64_t i0 = 0; i0 < n0; ++i0) {
                 const int32_t line = (int32_t)(i0 + n0 * i1);
-                if (!(interz(0, i0) && interz(1, i1))) P->zlines_bnd.push_back(line);
+                if (!(interz(0, i0) && interz(1, i1))) {
+                    // measurement switch (debug only; wrong values): boundary lines of one kind only,
+                    // 0 = boundary in direction 0 only, 1 = in direction 1 only, 2 = in both
+                    static const char *flt = getenv("WQ_ZL_BND_FILTER");
+                    if (flt) {
+                        const int kind = interz(1, i1) ? 0 : (interz(0, i0) ? 1 : 2);
+                        if (kind != atoi(flt)) continue;
+                    }
+                    P->zlines_bnd.push_back(line);
+                }
                 else (uniz(0, i0) && uniz(1, i1) ? P->zlines_uni : P->zlines_int).push_back(line);
             }
         // boundary lines: greedy longest-processing-time assignment to the CTAs of one launch (cost:

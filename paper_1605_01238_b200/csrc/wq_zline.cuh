@@ -416,6 +416,13 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
         }
 
         int cq0 = QI, cq1 = QI, ty0 = 0, ty1 = 0, sh0 = 0, sh1 = 0;
+        // boundary lines with column chunks (p >= 5, no direction-0 staircase groups): stage A loops
+        // over the offset groups of the line's row type (first plane of offset o = og0[o]) instead of
+        // one fully unrolled staircase per row type (2p+3 of them: 12.8 K instructions at p = 6)
+        constexpr bool OGA = BND && !CF::ZMA && P >= 5;
+        int og0[OGA ? NP + 1 : 1];
+        #pragma unroll
+        for (int o = 0; o < (OGA ? NP + 1 : 1); ++o) og0[o] = 0;
         int use = 0;
         for (int64_t T = wp; T < n_tasks; T += NWP, ++use) {
             const int b = NB == 2 ? (use & 1) : 0;
@@ -442,6 +449,15 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                         ty1 = ZTy<P>::group(ty1);
                         cq1 += 2 * sh1;
                     }
+                }
+                if constexpr (OGA) {
+                    #pragma unroll
+                    for (int o = 0; o <= P; ++o) {
+                        int c = 0;
+                        while (c < cq0 && ZTy<P>::off(ty0, c) < o) ++c;
+                        og0[o] = c;
+                    }
+                    og0[P + 1] = cq0;
                 }
                 // tables over the box's points c (the row's points start at c = 2 sh)
                 const int64_t tq0 = I.ql0 - 2 * sh0, tq1 = I.ql1 - 2 * sh1;
@@ -532,6 +548,12 @@ __global__ void __launch_bounds__(ZCfg<P, BND>::NT, 1)
                             #pragma unroll 1
                             for (int c0 = 2 * P - 1; c0 <= 3 * P; ++c0) plane(c0, std::integral_constant<int, P>{});
                         }
+                    } else if constexpr (OGA) {
+                        unroll<NP>([&](auto O) {
+                            constexpr int o = decltype(O)::value;
+                            #pragma unroll 1
+                            for (int c0 = og0[o]; c0 < og0[o + 1]; ++c0) plane(c0, std::integral_constant<int, o>{});
+                        });
                     } else if constexpr (BND) {
                         zdispatch<P>(ty0, [&](auto TT) {
                             constexpr int t = decltype(TT)::value;
