@@ -483,6 +483,13 @@ def main():
             torch.cuda.empty_cache()
         for p in C4_DEGREES:
             add(baseline_config("C4", p), 1)
+        add(baseline_config("C1"), 1)
+        add(baseline_config("C1"), 0)
+        # d = 2 at a size that fills the GPU (the sum-factorised d <= 2 kernel, WQ_KERNEL_SF2)
+        for p in (2, 4, 6):
+            c2d = Config(f"D2p{p}", 2, p, 1000, "grid", 0.1)
+            add(c2d, 1, label=f"2D 1000^2 p={p} stiffness")
+            add(c2d, 0, label=f"2D 1000^2 p={p} mass")
         add(baseline_config("C2"), 1)
         add(baseline_config("C2"), 0)
         add(baseline_config("C3"), 1)

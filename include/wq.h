@@ -98,9 +98,14 @@ typedef enum {
                              products, the direction-3 product per row),
                              warp-specialised TMA pipeline, direct coalesced
                              stores                                           */
-    WQ_KERNEL_ZHP = 4     /* d = 3, any p, mass and stiffness: lines along
+    WQ_KERNEL_ZHP = 4,    /* d = 3, any p, mass and stiffness: lines along
                              direction 3 in t_1 column chunks, CTA-wide
                              phases (the high-degree / mass kernel)           */
+    WQ_KERNEL_SF2 = 5     /* d <= 2, any p, mass and stiffness: one warp per
+                             row, the two contractions of Eq.
+                             sumfactorization in shared memory
+                             (Alg. 3); WQ_EINVAL when d = 3 or
+                             the row tables exceed 200 KB of shared memory  */
 } wq_kernel;
 
 typedef struct wq_plan_s *wq_plan;

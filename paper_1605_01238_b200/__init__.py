@@ -20,10 +20,10 @@ LIB_PATH = os.environ.get("WQ_LIB_DEBUG_PATH") or os.path.join(_HERE, "libwq.so"
 
 WQ_OK, WQ_EINVAL, WQ_EKNOTS, WQ_ESINGULAR, WQ_EGEOMETRY, WQ_ENOMEM, WQ_ECUDA, WQ_ERANGE = range(8)
 WQ_MASS, WQ_STIFFNESS = 0, 1
-WQ_KERNEL_AUTO, WQ_KERNEL_DIRECT, WQ_KERNEL_TILE, WQ_KERNEL_ZLINE, WQ_KERNEL_ZHP = 0, 1, 2, 3, 4
+WQ_KERNEL_AUTO, WQ_KERNEL_DIRECT, WQ_KERNEL_TILE, WQ_KERNEL_ZLINE, WQ_KERNEL_ZHP, WQ_KERNEL_SF2 = 0, 1, 2, 3, 4, 5
 WQ_BPTS_INTERIOR, WQ_BPTS_ENDPOINTS = 0, 1
 WQ_MAX_DEGREE = 10
-KERNEL_NAMES = {0: "none", 1: "direct", 2: "tile", 3: "zline", 4: "zhp"}
+KERNEL_NAMES = {0: "none", 1: "direct", 2: "tile", 3: "zline", 4: "zhp", 5: "sf2"}
 
 EXPORTED = ("wq_plan_create", "wq_plan_destroy", "wq_plan_info", "wq_build_rules", "wq_build_coef",
             "wq_pattern", "wq_assemble", "wq_assemble_ex", "wq_assemble_sgq", "wq_check", "wq_form_host",

@@ -452,7 +452,7 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
         // 17.5 ms against 19.6: its boundary lines are faster), ZHP for p >= 7
         const bool zhp_m = zhp_supported(P, WQ_MASS) && p >= 4;
         P->kernel_auto[0] = !P->need_mass ? 0
-                          : d < 3 ? WQ_KERNEL_DIRECT
+                          : d < 3 ? (sf2_supported(P, WQ_MASS) ? WQ_KERNEL_SF2 : WQ_KERNEL_DIRECT)
                           : zhp_m ? WQ_KERNEL_ZHP
                           : tile_supported(P, WQ_MASS) ? WQ_KERNEL_TILE
                           : zhp_supported(P, WQ_MASS) ? WQ_KERNEL_ZHP : WQ_KERNEL_DIRECT;
@@ -476,7 +476,7 @@ wq_status wq_plan_create(const wq_plan_desc *desc, wq_plan *out) {
         if (!st) st = create_build(P);
         // stiffness: ZHP for p >= 7 (C4 p = 10: 361 ms, row-tile on the standard-layout copy 407)
         P->kernel_auto[1] = !P->need_stiff ? 0
-                          : d < 3 ? WQ_KERNEL_DIRECT
+                          : d < 3 ? (sf2_supported(P, WQ_STIFFNESS) ? WQ_KERNEL_SF2 : WQ_KERNEL_DIRECT)
                           : p == 5 && zhp_supported(P, WQ_STIFFNESS) ? WQ_KERNEL_ZHP
                           : P->zline_ok ? WQ_KERNEL_ZLINE
                           : zhp_supported(P, WQ_STIFFNESS) && (p >= 7 || !tile_supported(P, WQ_STIFFNESS))
@@ -557,6 +557,15 @@ wq_status wq_pattern(wq_plan P, int64_t nnz_base, int64_t *d_row_ptr, int32_t *d
     return launch_pattern(P, nnz_base, d_row_ptr, d_col, 0, P->n_rows_local, S(stream));
 }
 
+// z-line stiffness: boundary lines through the ZHP kernel's boundary class (the same line set:
+// a support touching a boundary span in direction 1 or 2).  Measurement switch WQ_ZL_BND=zhp|zline.
+static bool zl_bnd_zhp(const wq_plan_s *P) {
+    if (!zhp_supported(P, WQ_STIFFNESS)) return false;
+    static const char *env = getenv("WQ_ZL_BND");
+    if (env) return strcmp(env, "zhp") == 0;
+    return false;
+}
+
 static wq_status assemble_range(wq_plan_s *P, int matrix, wq_kernel kernel, double *val, int32_t *col,
                                 int64_t pl_lo, int64_t pl_hi, int64_t val_base, cudaStream_t s) {
     if (matrix == WQ_MASS && !P->need_mass) return fail(WQ_EINVAL, "plan was created without need_mass");
@@ -571,7 +580,12 @@ static wq_status assemble_range(wq_plan_s *P, int matrix, wq_kernel kernel, doub
                       nb = (int64_t)P->zlines_bnd.size();
         wq_status st = launch_assemble_zline(P, 0, P->zlines_dev, nu, pl_lo, pl_hi, val, col, val_base, s);
         if (!st) st = launch_assemble_zline(P, 1, P->zlines_dev + nu, ni, pl_lo, pl_hi, val, col, val_base, s);
-        if (!st) st = launch_assemble_zline(P, 2, P->zlines_dev + nu + ni, nb, pl_lo, pl_hi, val, col, val_base, s);
+        if (!st) {
+            // boundary lines: by the ZHP kernel's boundary class where that is measured faster
+            // (zl_bnd_zhp), else the z-line kernel's boundary launch
+            if (zl_bnd_zhp(P)) st = launch_assemble_zhp(P, matrix, pl_lo, pl_hi, val, col, val_base, s, 2);
+            else st = launch_assemble_zline(P, 2, P->zlines_dev + nu + ni, nb, pl_lo, pl_hi, val, col, val_base, s);
+        }
         return st;
     }
     case WQ_KERNEL_ZHP:
@@ -580,6 +594,9 @@ static wq_status assemble_range(wq_plan_s *P, int matrix, wq_kernel kernel, doub
     case WQ_KERNEL_TILE:
         if (!tile_supported(P, matrix)) return fail(WQ_EINVAL, "tile kernel not available for this (d, p)");
         return launch_assemble_tile(P, matrix, val, col, pl_lo, pl_hi, val_base, s);
+    case WQ_KERNEL_SF2:
+        if (!sf2_supported(P, matrix)) return fail(WQ_EINVAL, "sf2 kernel not available for this plan (d <= 2)");
+        return launch_assemble_sf2(P, matrix, val, col, pl_lo, pl_hi, val_base, s);
     case WQ_KERNEL_DIRECT:
         return launch_assemble_direct(P, matrix, val, col, pl_lo, pl_hi, val_base, s);
     default:

@@ -23,18 +23,18 @@ bool zhp_supported(const wq_plan_s *P, int matrix) {
 }
 
 wq_status launch_assemble_zhp(wq_plan_s *P, int matrix, int64_t pl_lo, int64_t pl_hi, double *val, int32_t *col,
-                              int64_t val_base, cudaStream_t s) {
+                              int64_t val_base, cudaStream_t s, int classes) {
     switch (P->p) {
-    case 1: return zhp_launch_deg_1(P, matrix, pl_lo, pl_hi, val, col, val_base, s);
-    case 2: return zhp_launch_deg_2(P, matrix, pl_lo, pl_hi, val, col, val_base, s);
-    case 3: return zhp_launch_deg_3(P, matrix, pl_lo, pl_hi, val, col, val_base, s);
-    case 4: return zhp_launch_deg_4(P, matrix, pl_lo, pl_hi, val, col, val_base, s);
-    case 5: return zhp_launch_deg_5(P, matrix, pl_lo, pl_hi, val, col, val_base, s);
-    case 6: return zhp_launch_deg_6(P, matrix, pl_lo, pl_hi, val, col, val_base, s);
-    case 7: return zhp_launch_deg_7(P, matrix, pl_lo, pl_hi, val, col, val_base, s);
-    case 8: return zhp_launch_deg_8(P, matrix, pl_lo, pl_hi, val, col, val_base, s);
-    case 9: return zhp_launch_deg_9(P, matrix, pl_lo, pl_hi, val, col, val_base, s);
-    case 10: return zhp_launch_deg_10(P, matrix, pl_lo, pl_hi, val, col, val_base, s);
+    case 1: return zhp_launch_deg_1(P, matrix, pl_lo, pl_hi, val, col, val_base, s, classes);
+    case 2: return zhp_launch_deg_2(P, matrix, pl_lo, pl_hi, val, col, val_base, s, classes);
+    case 3: return zhp_launch_deg_3(P, matrix, pl_lo, pl_hi, val, col, val_base, s, classes);
+    case 4: return zhp_launch_deg_4(P, matrix, pl_lo, pl_hi, val, col, val_base, s, classes);
+    case 5: return zhp_launch_deg_5(P, matrix, pl_lo, pl_hi, val, col, val_base, s, classes);
+    case 6: return zhp_launch_deg_6(P, matrix, pl_lo, pl_hi, val, col, val_base, s, classes);
+    case 7: return zhp_launch_deg_7(P, matrix, pl_lo, pl_hi, val, col, val_base, s, classes);
+    case 8: return zhp_launch_deg_8(P, matrix, pl_lo, pl_hi, val, col, val_base, s, classes);
+    case 9: return zhp_launch_deg_9(P, matrix, pl_lo, pl_hi, val, col, val_base, s, classes);
+    case 10: return zhp_launch_deg_10(P, matrix, pl_lo, pl_hi, val, col, val_base, s, classes);
     }
     wq_set_error("ZHP kernel: unsupported degree");
     return WQ_EINVAL;

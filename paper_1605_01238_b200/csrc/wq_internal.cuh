@@ -136,6 +136,10 @@ wq_status launch_assemble_direct(wq_plan_s *P, int matrix, double *val, int32_t 
 wq_status launch_assemble_tile(wq_plan_s *P, int matrix, double *val, int32_t *col, int64_t plane_lo,
                                int64_t plane_hi, int64_t val_base, cudaStream_t s);
 bool tile_supported(const wq_plan_s *P, int matrix);
+// d <= 2: sum-factorised rows, one warp per row
+wq_status launch_assemble_sf2(wq_plan_s *P, int matrix, double *val, int32_t *col, int64_t plane_lo,
+                              int64_t plane_hi, int64_t val_base, cudaStream_t s);
+bool sf2_supported(const wq_plan_s *P, int matrix);
 // z-line kernel (stiffness, d = 3, coefficients in the z layout) over a list of lines (i1 + n1 * i2)
 // and the planes [pl_lo, pl_hi) of the slab
 bool zline_supported_p(int d, int p, const int64_t *n, const int32_t *maxq, int64_t n2l, int64_t nq2l);
@@ -149,7 +153,7 @@ wq_status zline_prepare(wq_plan_s *P);
 // high-degree / mass line kernel (d = 3, any p)
 bool zhp_supported(const wq_plan_s *P, int matrix);
 wq_status launch_assemble_zhp(wq_plan_s *P, int matrix, int64_t pl_lo, int64_t pl_hi, double *val, int32_t *col,
-                              int64_t val_base, cudaStream_t s);
+                              int64_t val_base, cudaStream_t s, int classes = 3);
 // standard element-loop Gauss quadrature (SGQ), scatter-added into the CSR values
 wq_status launch_assemble_sgq(wq_plan_s *P, int matrix, const double *ctrl, const double *kappa, const double *gamma,
                               double *val, int32_t *col, cudaStream_t s);

@@ -905,16 +905,17 @@ bool supported_p(const wq_plan_s *Pl, int matrix) {
 
 template <int P>
 wq_status launch_p(wq_plan_s *Pl, int matrix, int64_t pl_lo, int64_t pl_hi, double *val, int32_t *col,
-                   int64_t val_base, cudaStream_t s) {
+                   int64_t val_base, cudaStream_t s, int classes) {
+    // classes: bit 0 = interior lines (boxes of 2p+1 points), bit 1 = the rest (boundary lines)
     const Plan2 g = plan2(Pl, pl_lo, pl_hi);
     const int64_t ni = (int64_t)Pl->zh_int.size(), nbd = (int64_t)Pl->zh_bnd.size();
-    wq_status st;
+    wq_status st = WQ_OK;
     if (matrix == WQ_MASS) {
-        st = launch_cls<P, true, 2 * P + 1>(Pl, Pl->zh_dev, ni, g, val, col, val_base, s);
-        if (!st) st = launch_cls<P, true, 3 * P + 1>(Pl, Pl->zh_dev + ni, nbd, g, val, col, val_base, s);
+        if (classes & 1) st = launch_cls<P, true, 2 * P + 1>(Pl, Pl->zh_dev, ni, g, val, col, val_base, s);
+        if (!st && (classes & 2)) st = launch_cls<P, true, 3 * P + 1>(Pl, Pl->zh_dev + ni, nbd, g, val, col, val_base, s);
     } else {
-        st = launch_cls<P, false, 2 * P + 1>(Pl, Pl->zh_dev, ni, g, val, col, val_base, s);
-        if (!st) st = launch_cls<P, false, 3 * P + 1>(Pl, Pl->zh_dev + ni, nbd, g, val, col, val_base, s);
+        if (classes & 1) st = launch_cls<P, false, 2 * P + 1>(Pl, Pl->zh_dev, ni, g, val, col, val_base, s);
+        if (!st && (classes & 2)) st = launch_cls<P, false, 3 * P + 1>(Pl, Pl->zh_dev + ni, nbd, g, val, col, val_base, s);
     }
     return st;
 }
@@ -924,12 +925,12 @@ wq_status launch_p(wq_plan_s *Pl, int matrix, int64_t pl_lo, int64_t pl_hi, doub
 #define WQ_ZHP_DEG_DECL(PP)                                                                                          \
     bool zhp_supported_deg_##PP(const wq_plan_s *Pl, int matrix);                                                 \
     wq_status zhp_launch_deg_##PP(wq_plan_s *Pl, int matrix, int64_t pl_lo, int64_t pl_hi, double *val, int32_t *col, \
-                                  int64_t val_base, cudaStream_t s);
+                                  int64_t val_base, cudaStream_t s, int classes);
 #define WQ_ZHP_DEG_DEF(PP)                                                                                           \
     bool zhp_supported_deg_##PP(const wq_plan_s *Pl, int matrix) { return zhp::supported_p<PP>(Pl, matrix); }      \
     wq_status zhp_launch_deg_##PP(wq_plan_s *Pl, int matrix, int64_t pl_lo, int64_t pl_hi, double *val, int32_t *col, \
-                                  int64_t val_base, cudaStream_t s) {                                               \
-        return zhp::launch_p<PP>(Pl, matrix, pl_lo, pl_hi, val, col, val_base, s);                                   \
+                                  int64_t val_base, cudaStream_t s, int classes) {                                  \
+        return zhp::launch_p<PP>(Pl, matrix, pl_lo, pl_hi, val, col, val_base, s, classes);                          \
     }
 WQ_ZHP_DEG_DECL(1) WQ_ZHP_DEG_DECL(2) WQ_ZHP_DEG_DECL(3) WQ_ZHP_DEG_DECL(4) WQ_ZHP_DEG_DECL(5)
 WQ_ZHP_DEG_DECL(6) WQ_ZHP_DEG_DECL(7) WQ_ZHP_DEG_DECL(8) WQ_ZHP_DEG_DECL(9) WQ_ZHP_DEG_DECL(10)

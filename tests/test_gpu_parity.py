@@ -11,7 +11,8 @@ from wqinputs import control_net, graded_open_knots, greville, uniform_open_knot
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [wq.WQ_KERNEL_AUTO, wq.WQ_KERNEL_DIRECT, wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_ZLINE, wq.WQ_KERNEL_ZHP]
+KERNELS = [wq.WQ_KERNEL_AUTO, wq.WQ_KERNEL_DIRECT, wq.WQ_KERNEL_TILE, wq.WQ_KERNEL_ZLINE, wq.WQ_KERNEL_ZHP,
+           wq.WQ_KERNEL_SF2]
 
 
 def _torch():
@@ -66,12 +67,14 @@ def check_every_row(o, mat, rp, col, val, key=None, strict=False):
 
 def refusal_expected(kernel, ks, p, mat):
     """The documented contract of the explicit kernels (include/wq.h wq_kernel): ZLINE serves
-    stiffness, d = 3, 2 <= p <= 6, n_EL >= p+2 in every direction; TILE and ZHP serve d = 3; none of them serves a direction with
+    stiffness, d = 3, 2 <= p <= 6, n_EL >= p+2 in every direction; TILE and ZHP serve d = 3, SF2 d <= 2; none of them serves a direction with
     one DOF row pair or a support that holds both boundary spans (#Q > 3p+1, reading R15).  AUTO and
     DIRECT serve every plan.  Used to turn a refusal into a check instead of a skip."""
     if kernel in (wq.WQ_KERNEL_AUTO, wq.WQ_KERNEL_DIRECT):
         return False
     d = len(ks)
+    if kernel == wq.WQ_KERNEL_SF2:  # d <= 2, any p (the row tables of these tests fit in shared memory)
+        return d == 3
     if d != 3:
         return True
     if kernel == wq.WQ_KERNEL_ZLINE and (mat != STIFFNESS or p < 2 or p > 6):
@@ -304,6 +307,22 @@ def test_graded_knots_every_row(p, E, kernel):
     o = Oracle(p, ks, ctrl)
     run_matrices(ks, ctrl, p, kernel, (STIFFNESS, MASS),
                  lambda mat, rp, col, val, info: check_every_row(o, mat, rp, col, val, ("graded", p, E)))
+
+
+# ------------------------------------------------- d <= 2 sum-factorised rows
+@pytest.mark.parametrize("d,p,E,knots", [(2, p, E, kn) for p, E in [(1, 9), (2, 7), (3, 11), (4, 6), (5, 8),
+                                                                   (6, 5), (7, 9), (8, 3), (9, 4), (10, 12)]
+                                         for kn in ("uniform", "graded")] + [(1, 10, 17, "graded"), (1, 4, 2, "uniform")])
+def test_sf2_every_row(d, p, E, knots):
+    """The d <= 2 product kernel (WQ_KERNEL_SF2, Eq. sumfactorization) on every row, both
+    matrices, p = 1..10, uniform and graded knots, n_EL from below p+1 to several tiles of rows
+    per CTA (8 rows per CTA: the last CTA ragged); AUTO must pick it."""
+    ks, ctrl = make_case(d, p, E, "grid", 0.08, knots=knots, seed=5 + p)
+    o = Oracle(p, ks, ctrl)
+    for mat in (MASS, STIFFNESS):
+        rp, col, val, info = run_full(ks, ctrl, p, mat, wq.WQ_KERNEL_SF2)
+        assert info["kernel"][mat] == wq.WQ_KERNEL_SF2
+        check_every_row(o, mat, rp, col, val, ("sf2", d, p, E, knots))
 
 
 # ------------------------------------------------- scalar coefficients (R17)

@@ -17,11 +17,12 @@ ap.add_argument("--matrix", default="stiffness")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--config", default="C4")
 ap.add_argument("--nel", type=int, default=0, help="override n_el (grid geometry)")
+ap.add_argument("--d", type=int, default=3, help="dimension with --nel")
 a = ap.parse_args()
 mat = wq.WQ_STIFFNESS if a.matrix == "stiffness" else wq.WQ_MASS
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 for p in [int(x) for x in a.p.split(",")]:
-    cfg = baseline_config(a.config, p) if not a.nel else Config(f"G{a.nel}p{p}", 3, p, a.nel, "grid", 0.1)
+    cfg = baseline_config(a.config, p) if not a.nel else Config(f"G{a.d}d{a.nel}p{p}", a.d, p, a.nel, "grid", 0.1)
     plan = wq.Plan(cfg.p, cfg.knots(), ctrl=cfg.ctrl(), need_mass=mat == wq.WQ_MASS,
                    need_stiffness=mat == wq.WQ_STIFFNESS)
     rp, col, val = plan.alloc_csr()
