@@ -6,8 +6,16 @@
 // with A_k^f(t, c) = w^f_{k,i_k,q} D^{b(f)} B_{j_k}(x_q) (family f = a + 2b,
 // (a,b) = (delta_kl, delta_km), reading R3; mass: the single term f = 0 and c).
 // O(#I_1 #Q_1 #Q_2 + #I_1 #I_2 #Q_2) per row, i.e. O(p) per entry instead of
-// the O(p^d) of the direct kernel.  d = 1 is the same code with a trivial
-// direction 2 (#Q_2 = #I_2 = 1, A_2 = 1).
+// the O(p^d) of the direct kernel.
+//   k_sf2l (d = 2): CTA = one i_1 and a chunk of RC consecutive rows i_2.  The
+//     rows share A_1 and, over the chunk's whole point range in q_2, stage 1
+//     (Y does not depend on i_2): it is done once per CTA, then stage 2 per
+//     row batch with that row's A_2 (stage 1 amortised over the chunk, as the
+//     line kernels of d = 3 amortise their first two contractions).
+//   k_sf2 (d = 1, and d = 2 when the chunk tables do not fit): one warp per
+//     row, both stages per row; d = 1 is the same code with a trivial
+//     direction 2 (#Q_2 = #I_2 = 1, A_2 = 1).
+#include <cstdlib>
 #include "wq_rows.cuh"
 
 namespace {
@@ -103,6 +111,169 @@ __global__ void __launch_bounds__(256) k_sf2(Sf2Args a) {
     }
 }
 
+
+struct Sf2lArgs {
+    RowGeo g;
+    DirView v[2];
+    int p, matrix;
+    CoefView cv;
+    int64_t cq_b;
+    int comp_mass;
+    double *val;
+    int32_t *col;
+    int64_t val_base;
+    int64_t i2b, i2e;        // rows i_2 of this launch (global)
+    int rc, rb;              // rows i_2 per CTA, rows per stage-2 batch
+    int km, qm, qrm;         // strides: max #I, max #Q (odd), max points of a chunk in q_2 (odd)
+};
+
+// sum_{c < N} a[c] b[c] with N a compile-time bound (rows padded with zeros beyond their #Q)
+template <int N>
+__device__ __forceinline__ double dotn(const double *x, const double *y) {
+    double s0 = 0.0, s1 = 0.0;
+    #pragma unroll
+    for (int c = 0; c + 1 < N; c += 2) {
+        s0 = fma(x[c], y[c], s0);
+        s1 = fma(x[c + 1], y[c + 1], s1);
+    }
+    if (N & 1) s0 = fma(x[N - 1], y[N - 1], s0);
+    return s0 + s1;
+}
+
+// Shared-memory layout (doubles), strides compile-time from the degree: QS = (3p+1)|1 point slots
+// per row (#Q_i <= 3p+1 when n_EL >= p+2), zero padded beyond the row's #Q:
+//   A1 [f][t_1][QS], Cs [u][r][QS] (r < QR, the chunk's points in q_2), Y [term][t_1][QY]
+//   (QY = (QR + QS) | 1, zero beyond the chunk), A2 [row of batch][f][t_2][QS], per-row scalars.
+template <int P, bool MASS>
+__global__ void __launch_bounds__(256) k_sf2l(Sf2lArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    constexpr int KM = 2 * P + 1, QX = 3 * P + 1, QS = QX | 1, BS = wq_bstride(P);
+    constexpr int NF = MASS ? 1 : 4, NT = NF, NCU = MASS ? 1 : 3;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int QR = a.qrm, QY = (QR + QS) | 1;  // odd: the lanes of stage 2 (consecutive t_1) hit distinct banks
+    const DirView &v0 = a.v[0], &v1 = a.v[1];
+    const int64_t i1 = blockIdx.y;
+    const int64_t i2a = a.i2b + (int64_t)blockIdx.x * a.rc;
+    const int64_t i2e = i2a + a.rc < a.i2e ? i2a + a.rc : a.i2e;
+    const int ni1 = v0.jlen[i1], nq1 = v0.qlen[i1];
+    const int64_t jl1 = v0.jlo[i1], ql1 = v0.qlo[i1];
+    const int64_t q2a = v1.qlo[i2a];
+    const int nr2 = (int)(v1.qlo[i2e - 1] + v1.qlen[i2e - 1] - q2a);  // points of the chunk in q_2
+    double *A1 = sm;
+    double *Cs = A1 + NF * KM * QS;
+    double *Y = Cs + NCU * QR * QS;
+    double *A2 = Y + NT * KM * QY;
+    int64_t *roff = (int64_t *)(A2 + a.rb * NF * KM * QS);  // per batch row: CSR offset
+    int *rint = (int *)(roff + a.rb);                       // per batch row: #I_2, #Q_2, r0
+    // A1: thread = point slot c of direction 1
+    for (int c = tid; c < QS; c += nth) {
+        double w[4] = {0.0, 0.0, 0.0, 0.0}, bv[2 * (P + 1)];
+        int sp = 0;
+        if (c < nq1) {
+            const int64_t q = ql1 + c;
+            sp = v0.span[q];
+            #pragma unroll
+            for (int f = 0; f < NF; ++f) w[f] = v0.W[(i1 * v0.maxq + c) * 4 + f];
+            #pragma unroll
+            for (int k = 0; k < 2 * (P + 1); ++k) bv[k] = v0.B[q * BS + k];
+        }
+        #pragma unroll
+        for (int t = 0; t < KM; ++t) {
+            const int loc = (int)(jl1 + t - sp);
+            #pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                double x = 0.0;
+                #pragma unroll
+                for (int k = 0; k <= P; ++k)
+                    if (loc == k) x = bv[2 * k + (f >> 1)];
+                A1[(f * KM + t) * QS + c] = c < nq1 && t < ni1 ? w[f] * x : 0.0;
+            }
+        }
+    }
+    // the chunk's coefficient values, zero padded beyond #Q_1
+    for (int x = tid; x < NCU * QR * QS; x += nth) {
+        const int u = x / (QR * QS), e = x - u * QR * QS, r = e / QS, c = e - r * QS;
+        double cv = 0.0;
+        if (r < nr2 && c < nq1) cv = __ldg(a.cv.ptr(MASS ? a.comp_mass : u, ql1 + c, q2a + r - a.cq_b, 0));
+        Cs[x] = cv;
+    }
+    __syncthreads();
+    // stage 1: item (term, t_1, r); term (l, m) = (term >> 1, term & 1): family of direction 1
+    // (l == 0) + 2 (m == 0), component C_{l+m} (C_01 = C_10)
+    for (int x = tid; x < KM * QY; x += nth) {
+        const int t1 = x / QY, r = x - t1 * QY;
+        #pragma unroll
+        for (int term = 0; term < NT; ++term) {
+            const int lt = term >> 1, mt = term & 1;
+            const int f1 = MASS ? 0 : (lt == 0) + 2 * (mt == 0);
+            const int u = MASS ? 0 : lt + mt;
+            double s = 0.0;
+            if (r < nr2) s = nq1 == 2 * P + 1 ? dotn<2 * P + 1>(A1 + (f1 * KM + t1) * QS, Cs + (u * QR + r) * QS)
+                                              : dotn<QX>(A1 + (f1 * KM + t1) * QS, Cs + (u * QR + r) * QS);
+            Y[(term * KM + t1) * QY + r] = s;
+        }
+    }
+    __syncthreads();
+    // stage 2 per batch of rows i_2
+    for (int64_t ib = i2a; ib < i2e; ib += a.rb) {
+        const int nb = (int)(i2e - ib < a.rb ? i2e - ib : a.rb);
+        // A2: thread = (row of batch, point slot)
+        for (int x = tid; x < nb * QS; x += nth) {
+            const int rr = x / QS, c = x - rr * QS;
+            const int64_t i2 = ib + rr;
+            const int ni2 = v1.jlen[i2], nq2 = v1.qlen[i2];
+            const int64_t jl2 = v1.jlo[i2], ql2 = v1.qlo[i2];
+            if (c == 0) {
+                roff[rr] = a.g.offset(i1, i2, 0) - a.val_base;
+                rint[3 * rr] = ni2;
+                rint[3 * rr + 1] = nq2;
+                rint[3 * rr + 2] = (int)(ql2 - q2a);
+            }
+            double w[4] = {0.0, 0.0, 0.0, 0.0}, bv[2 * (P + 1)];
+            int sp = 0;
+            if (c < nq2) {
+                const int64_t q = ql2 + c;
+                sp = v1.span[q];
+                #pragma unroll
+                for (int f = 0; f < NF; ++f) w[f] = v1.W[(i2 * v1.maxq + c) * 4 + f];
+                #pragma unroll
+                for (int k = 0; k < 2 * (P + 1); ++k) bv[k] = v1.B[q * BS + k];
+            }
+            #pragma unroll
+            for (int t = 0; t < KM; ++t) {
+                const int loc = (int)(jl2 + t - sp);
+                #pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    double y = 0.0;
+                    #pragma unroll
+                    for (int k = 0; k <= P; ++k)
+                        if (loc == k) y = bv[2 * k + (f >> 1)];
+                    A2[((rr * NF + f) * KM + t) * QS + c] = c < nq2 && t < ni2 ? w[f] * y : 0.0;
+                }
+            }
+        }
+        __syncthreads();
+        // item (row of batch, t_2, t_1): consecutive threads store consecutive columns t_1
+        for (int x = tid; x < nb * KM * KM; x += nth) {
+            const int rr = x / (KM * KM), e = x - rr * KM * KM, t2 = e / KM, t1 = e - t2 * KM;
+            const int ni2 = rint[3 * rr], nq2 = rint[3 * rr + 1], r0 = rint[3 * rr + 2];
+            if (t1 >= ni1 || t2 >= ni2) continue;
+            double s = 0.0;
+            #pragma unroll
+            for (int term = 0; term < NT; ++term) {
+                const int lt = term >> 1, mt = term & 1;
+                const int f2 = MASS ? 0 : (lt == 1) + 2 * (mt == 1);
+                const double *Ar = A2 + ((rr * NF + f2) * KM + t2) * QS, *Yr = Y + (term * KM + t1) * QY + r0;
+                s += nq2 == 2 * P + 1 ? dotn<2 * P + 1>(Ar, Yr) : dotn<QX>(Ar, Yr);
+            }
+            const int64_t o = roff[rr] + t1 + ni1 * t2;
+            a.val[o] = s;
+            if (a.col) a.col[o] = (int32_t)((jl1 + t1) + a.g.n[0] * (v1.jlo[ib + rr] + t2));
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace
 
 // doubles of shared memory per warp; 0 when d > 2
@@ -114,14 +285,113 @@ static int64_t sf2_wstride(const wq_plan_s *P, int matrix, int &km, int &qm) {
     return P->d > 2 ? 0 : ((int64_t)(2 * nf + nterm) * km * qm + 1) / 2 * 2;
 }
 
+// d = 2 chunked-line kernel: rows i_2 per CTA (rc), stage-2 batch (rb) and strides; false if it does
+// not fit in shared memory
+static bool sf2l_config(const wq_plan_s *P, int matrix, Sf2lArgs &a, size_t &smem) {
+    if (P->d != 2 || P->p < 1 || P->p > 10) return false;
+    const int p = P->p, KM = 2 * p + 1, QS = (3 * p + 1) | 1;
+    // compile-time point slots: #Q_i <= 3p+1 (not so when one support holds both boundary spans)
+    if (P->dir[0].maxq > 3 * p + 1 || P->dir[1].maxq > 3 * p + 1) return false;
+    const bool stiff = matrix != 0;
+    const int nf = stiff ? 4 : 1, nterm = stiff ? 4 : 1, ncu = stiff ? 3 : 1;
+    const int64_t E1 = P->dir[1].E;
+    // rows per stage-2 batch: the batch's KM^2 items fill whole passes of the 256 threads
+    int rb = 1;
+    double best = 0.0;
+    for (int b = 1; b <= 16; ++b) {
+        const int it = b * KM * KM;
+        const double eff = (double)it / (double)(((it + 255) / 256) * 256);
+        const size_t a2 = (size_t)b * nf * KM * QS * sizeof(double);
+        if (eff > best + 1e-9 && a2 <= 64 * 1024) { best = eff; rb = b; }
+    }
+    for (int rc = 32; rc >= 4; rc >>= 1) {
+        int64_t qr = 1;
+        // any chunk start (launches over plane sub-ranges start anywhere in the slab)
+        for (int64_t ia = P->slab_b; ia < P->slab_e; ++ia) {
+            const int64_t ie = ia + rc < P->slab_e ? ia + rc : P->slab_e;
+            const int64_t w = wq_host_qhi(ie - 1, E1, p) - wq_host_qlo(ia, E1, p) + 1;
+            qr = w > qr ? w : qr;
+        }
+        qr |= 1;
+        const int b = rb < rc ? rb : rc;
+        const size_t n = (size_t)nf * KM * QS + (size_t)ncu * qr * QS + (size_t)nterm * KM * ((qr + QS) | 1) +
+                         (size_t)b * nf * KM * QS;
+        const size_t bytes = n * sizeof(double) + (size_t)b * (sizeof(int64_t) + 3 * sizeof(int));
+        if (bytes <= 200 * 1024) {
+            a.rc = rc;
+            a.rb = b;
+            a.km = KM;
+            a.qm = QS;
+            a.qrm = (int)qr;
+            smem = (bytes + 15) & ~(size_t)15;
+            return true;
+        }
+    }
+    return false;
+}
+
+template <int PP>
+static wq_status launch_sf2l_p(const Sf2lArgs &a, size_t sm, int matrix, dim3 g, cudaStream_t s) {
+    const void *fn = matrix == 0 ? (const void *)k_sf2l<PP, true> : (const void *)k_sf2l<PP, false>;
+    cudaError_t ce = wq_smem_attr(fn, sm);
+    if (ce != cudaSuccess) return wq_cuda_status(ce, "sf2 kernel attribute");
+    if (matrix == 0) k_sf2l<PP, true><<<g, 256, sm, s>>>(a);
+    else k_sf2l<PP, false><<<g, 256, sm, s>>>(a);
+    return WQ_OK;
+}
+
 bool sf2_supported(const wq_plan_s *P, int matrix) {
+    Sf2lArgs l;
+    size_t sl;
+    if (sf2l_config(P, matrix, l, sl)) return true;
     int km, qm;
     const int64_t w = sf2_wstride(P, matrix, km, qm);
     return w > 0 && w * (int64_t)sizeof(double) <= 200 * 1024;
 }
 
+static wq_status launch_sf2l(wq_plan_s *P, Sf2lArgs &a, size_t sm, int matrix, double *val, int32_t *col,
+                             int64_t plane_lo, int64_t plane_hi, int64_t val_base, cudaStream_t s) {
+    a.g.init(P);
+    a.i2b = P->slab_b + plane_lo;
+    a.i2e = P->slab_b + plane_hi;
+    for (int l = 0; l < 2; ++l) a.v[l] = P->dir[l];
+    a.p = P->p;
+    a.matrix = matrix;
+    a.cv = P->cview;
+    a.cq_b = P->cq_b;
+    a.comp_mass = P->comp_mass;
+    a.val = val;
+    a.col = col;
+    a.val_base = val_base;
+    const int64_t nchunk = (plane_hi - plane_lo + a.rc - 1) / a.rc;
+    if (nchunk > 0) {
+        const dim3 g((unsigned)nchunk, (unsigned)P->dir[0].n);
+        wq_status st = WQ_OK;
+        switch (P->p) {
+        case 1: st = launch_sf2l_p<1>(a, sm, matrix, g, s); break;
+        case 2: st = launch_sf2l_p<2>(a, sm, matrix, g, s); break;
+        case 3: st = launch_sf2l_p<3>(a, sm, matrix, g, s); break;
+        case 4: st = launch_sf2l_p<4>(a, sm, matrix, g, s); break;
+        case 5: st = launch_sf2l_p<5>(a, sm, matrix, g, s); break;
+        case 6: st = launch_sf2l_p<6>(a, sm, matrix, g, s); break;
+        case 7: st = launch_sf2l_p<7>(a, sm, matrix, g, s); break;
+        case 8: st = launch_sf2l_p<8>(a, sm, matrix, g, s); break;
+        case 9: st = launch_sf2l_p<9>(a, sm, matrix, g, s); break;
+        case 10: st = launch_sf2l_p<10>(a, sm, matrix, g, s); break;
+        }
+        if (st) return st;
+        wq_count_launches(1);
+    }
+    return wq_cuda_status(cudaGetLastError(), "sf2 (d = 2 line) assembly kernel");
+}
 wq_status launch_assemble_sf2(wq_plan_s *P, int matrix, double *val, int32_t *col, int64_t plane_lo,
                               int64_t plane_hi, int64_t val_base, cudaStream_t s) {
+    {
+        Sf2lArgs l;
+        size_t sl;
+        if (!getenv("WQ_SF2_ROWS") && sf2l_config(P, matrix, l, sl))
+            return launch_sf2l(P, l, sl, matrix, val, col, plane_lo, plane_hi, val_base, s);
+    }
     Sf2Args a;
     const int64_t ws = sf2_wstride(P, matrix, a.km, a.qm);
     int64_t rpp = 1;

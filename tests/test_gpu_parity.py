@@ -325,6 +325,40 @@ def test_sf2_every_row(d, p, E, knots):
         check_every_row(o, mat, rp, col, val, ("sf2", d, p, E, knots))
 
 
+@pytest.mark.parametrize("p,E,knots", [(2, 7, "graded"), (4, 6, "uniform"), (9, 4, "graded")])
+def test_sf2_row_variant_every_row(p, E, knots, monkeypatch):
+    """The warp-per-row form of WQ_KERNEL_SF2 (d = 1, and d = 2 when the chunk tables do not fit),
+    forced on d = 2 by the measurement switch WQ_SF2_ROWS: every row against the oracle."""
+    monkeypatch.setenv("WQ_SF2_ROWS", "1")
+    ks, ctrl = make_case(2, p, E, "grid", 0.08, knots=knots, seed=3)
+    o = Oracle(p, ks, ctrl)
+    for mat in (MASS, STIFFNESS):
+        rp, col, val, info = run_full(ks, ctrl, p, mat, wq.WQ_KERNEL_SF2)
+        check_every_row(o, mat, rp, col, val, ("sf2r", p, E, knots))
+
+
+@pytest.mark.parametrize("p,E,chunk", [(3, 40, 20000), (5, 37, 9000)])
+def test_sf2_plane_ranges_form_host(p, E, chunk, monkeypatch):
+    """d = 2 through wq_form_host in plane chunks (the line kernel's launches then start inside the
+    slab, at chunk boundaries that are not multiples of its rows per CTA) == one device call."""
+    torch = _torch()
+    ks, ctrl = make_case(2, p, E)
+    for mat in (MASS, STIFFNESS):
+        rp0, col0, val0, info = run_full(ks, ctrl, p, mat, wq.WQ_KERNEL_SF2)
+        monkeypatch.setenv("WQ_FORM_CHUNK_NNZ", str(chunk))
+        plan = wq.Plan(p, ks)
+        n, nnz = plan.info["n_rows_local"], plan.info["nnz_local"]
+        hrp = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+        hcol = torch.empty(nnz, dtype=torch.int32).pin_memory()
+        hval = torch.empty(nnz, dtype=torch.float64).pin_memory()
+        wq.wq_form_host(plan.h, mat, torch.from_numpy(ctrl).pin_memory(), 0, hrp, hcol, hval)
+        plan.close()
+        monkeypatch.delenv("WQ_FORM_CHUNK_NNZ")
+        assert np.array_equal(hrp.numpy(), rp0.cpu().numpy())
+        assert np.array_equal(hcol.numpy(), col0.cpu().numpy())
+        assert np.array_equal(hval.numpy(), val0.cpu().numpy())
+
+
 # ------------------------------------------------- scalar coefficients (R17)
 @pytest.mark.parametrize("d,p,E", [(1, 3, 9), (2, 3, 6), (3, 2, 6), (3, 4, 5), (3, 7, 2)])
 @pytest.mark.parametrize("kernel", KERNELS)
