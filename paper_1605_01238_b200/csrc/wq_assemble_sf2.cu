@@ -123,7 +123,7 @@ struct Sf2lArgs {
     int32_t *col;
     int64_t val_base;
     int64_t i2b, i2e;        // rows i_2 of this launch (global)
-    int rc, rb;              // rows i_2 per CTA, rows per stage-2 batch
+    int rc, rb;              // rows i_2 per CTA, stage-2 warps
     int km, qm, qrm;         // strides: max #I, max #Q (odd), max points of a chunk in q_2 (odd)
 };
 
@@ -162,9 +162,7 @@ __global__ void __launch_bounds__(256) k_sf2l(Sf2lArgs a) {
     double *A1 = sm;
     double *Cs = A1 + NF * KM * QS;
     double *Y = Cs + NCU * QR * QS;
-    double *A2 = Y + NT * KM * QY;
-    int64_t *roff = (int64_t *)(A2 + a.rb * NF * KM * QS);  // per batch row: CSR offset
-    int *rint = (int *)(roff + a.rb);                       // per batch row: #I_2, #Q_2, r0
+    double *A2 = Y + NT * KM * QY;        // per stage-2 warp: [f][t_2][QS]
     // A1: thread = point slot c of direction 1
     for (int c = tid; c < QS; c += nth) {
         double w[4] = {0.0, 0.0, 0.0, 0.0}, bv[2 * (P + 1)];
@@ -214,63 +212,57 @@ __global__ void __launch_bounds__(256) k_sf2l(Sf2lArgs a) {
         }
     }
     __syncthreads();
-    // stage 2 per batch of rows i_2
-    for (int64_t ib = i2a; ib < i2e; ib += a.rb) {
-        const int nb = (int)(i2e - ib < a.rb ? i2e - ib : a.rb);
-        // A2: thread = (row of batch, point slot)
-        for (int x = tid; x < nb * QS; x += nth) {
-            const int rr = x / QS, c = x - rr * QS;
-            const int64_t i2 = ib + rr;
-            const int ni2 = v1.jlen[i2], nq2 = v1.qlen[i2];
-            const int64_t jl2 = v1.jlo[i2], ql2 = v1.qlo[i2];
-            if (c == 0) {
-                roff[rr] = a.g.offset(i1, i2, 0) - a.val_base;
-                rint[3 * rr] = ni2;
-                rint[3 * rr + 1] = nq2;
-                rint[3 * rr + 2] = (int)(ql2 - q2a);
-            }
-            double w[4] = {0.0, 0.0, 0.0, 0.0}, bv[2 * (P + 1)];
-            int sp = 0;
-            if (c < nq2) {
-                const int64_t q = ql2 + c;
-                sp = v1.span[q];
-                #pragma unroll
-                for (int f = 0; f < NF; ++f) w[f] = v1.W[(i2 * v1.maxq + c) * 4 + f];
-                #pragma unroll
-                for (int k = 0; k < 2 * (P + 1); ++k) bv[k] = v1.B[q * BS + k];
-            }
+    // stage 2: warp w < a.rb takes the rows i2a + w, i2a + w + rb, ...: its own A2 (no CTA barrier)
+    const int warp = tid >> 5, lane = tid & 31;
+    if (warp >= a.rb) return;
+    double *A2w = A2 + warp * (NF * KM * QS);
+    for (int64_t i2 = i2a + warp; i2 < i2e; i2 += a.rb) {
+        const int ni2 = v1.jlen[i2], nq2 = v1.qlen[i2];
+        const int64_t jl2 = v1.jlo[i2], ql2 = v1.qlo[i2];
+        const int r0 = (int)(ql2 - q2a);
+        // A2 column of point slot c = lane: zeros, then the p+1 nonzero functions t_2 = span - jlo + k
+        if (lane < QS) {
             #pragma unroll
-            for (int t = 0; t < KM; ++t) {
-                const int loc = (int)(jl2 + t - sp);
+            for (int f = 0; f < NF; ++f)
                 #pragma unroll
-                for (int f = 0; f < NF; ++f) {
-                    double y = 0.0;
-                    #pragma unroll
-                    for (int k = 0; k <= P; ++k)
-                        if (loc == k) y = bv[2 * k + (f >> 1)];
-                    A2[((rr * NF + f) * KM + t) * QS + c] = c < nq2 && t < ni2 ? w[f] * y : 0.0;
+                for (int t = 0; t < KM; ++t) A2w[(f * KM + t) * QS + lane] = 0.0;
+            if (lane < nq2) {
+                const int64_t q = ql2 + lane;
+                const int t0 = (int)(v1.span[q] - jl2);
+                double w[4];
+                #pragma unroll
+                for (int f = 0; f < NF; ++f) w[f] = v1.W[(i2 * v1.maxq + lane) * 4 + f];
+                #pragma unroll
+                for (int k = 0; k <= P; ++k) {
+                    const int t = t0 + k;
+                    if (t >= 0 && t < ni2) {
+                        const double b0 = v1.B[q * BS + 2 * k], b1 = v1.B[q * BS + 2 * k + 1];
+                        #pragma unroll
+                        for (int f = 0; f < NF; ++f) A2w[(f * KM + t) * QS + lane] = w[f] * ((f >> 1) ? b1 : b0);
+                    }
                 }
             }
         }
-        __syncthreads();
-        // item (row of batch, t_2, t_1): consecutive threads store consecutive columns t_1
-        for (int x = tid; x < nb * KM * KM; x += nth) {
-            const int rr = x / (KM * KM), e = x - rr * KM * KM, t2 = e / KM, t1 = e - t2 * KM;
-            const int ni2 = rint[3 * rr], nq2 = rint[3 * rr + 1], r0 = rint[3 * rr + 2];
+        __syncwarp();
+        const int64_t off = a.g.offset(i1, i2, 0) - a.val_base;
+        // item (t_2, t_1): consecutive lanes store consecutive columns t_1 (two items per lane and
+        // iteration measured no faster: stage 2 is bound by its two shared loads per FMA)
+        for (int e = lane; e < KM * KM; e += 32) {
+            const int t2 = e / KM, t1 = e - t2 * KM;
             if (t1 >= ni1 || t2 >= ni2) continue;
             double s = 0.0;
             #pragma unroll
             for (int term = 0; term < NT; ++term) {
                 const int lt = term >> 1, mt = term & 1;
                 const int f2 = MASS ? 0 : (lt == 1) + 2 * (mt == 1);
-                const double *Ar = A2 + ((rr * NF + f2) * KM + t2) * QS, *Yr = Y + (term * KM + t1) * QY + r0;
+                const double *Ar = A2w + (f2 * KM + t2) * QS, *Yr = Y + (term * KM + t1) * QY + r0;
                 s += nq2 == 2 * P + 1 ? dotn<2 * P + 1>(Ar, Yr) : dotn<QX>(Ar, Yr);
             }
-            const int64_t o = roff[rr] + t1 + ni1 * t2;
+            const int64_t o = off + t1 + ni1 * t2;
             a.val[o] = s;
-            if (a.col) a.col[o] = (int32_t)((jl1 + t1) + a.g.n[0] * (v1.jlo[ib + rr] + t2));
+            if (a.col) a.col[o] = (int32_t)((jl1 + t1) + a.g.n[0] * (jl2 + t2));
         }
-        __syncthreads();
+        __syncwarp();
     }
 }
 
@@ -295,16 +287,12 @@ static bool sf2l_config(const wq_plan_s *P, int matrix, Sf2lArgs &a, size_t &sme
     const bool stiff = matrix != 0;
     const int nf = stiff ? 4 : 1, nterm = stiff ? 4 : 1, ncu = stiff ? 3 : 1;
     const int64_t E1 = P->dir[1].E;
-    // rows per stage-2 batch: the batch's KM^2 items fill whole passes of the 256 threads
-    int rb = 1;
-    double best = 0.0;
-    for (int b = 1; b <= 16; ++b) {
-        const int it = b * KM * KM;
-        const double eff = (double)it / (double)(((it + 255) / 256) * 256);
-        const size_t a2 = (size_t)b * nf * KM * QS * sizeof(double);
-        if (eff > best + 1e-9 && a2 <= 64 * 1024) { best = eff; rb = b; }
-    }
-    for (int rc = 32; rc >= 4; rc >>= 1) {
+    // rc rows i_2 per CTA and rb stage-2 warps (each with its own A2): 8 warps and the largest
+    // rc >= 8 that leave 3 CTAs per SM, else 2, else 1 (fewer warps before fewer rows)
+    const size_t a2 = (size_t)nf * KM * QS;
+    int64_t qrs[4];  // rc = 32, 16, 8, 4: max points in q_2 of a chunk, odd
+    for (int k = 0; k < 4; ++k) {
+        const int rc = 32 >> k;
         int64_t qr = 1;
         // any chunk start (launches over plane sub-ranges start anywhere in the slab)
         for (int64_t ia = P->slab_b; ia < P->slab_e; ++ia) {
@@ -312,21 +300,27 @@ static bool sf2l_config(const wq_plan_s *P, int matrix, Sf2lArgs &a, size_t &sme
             const int64_t w = wq_host_qhi(ie - 1, E1, p) - wq_host_qlo(ia, E1, p) + 1;
             qr = w > qr ? w : qr;
         }
-        qr |= 1;
-        const int b = rb < rc ? rb : rc;
-        const size_t n = (size_t)nf * KM * QS + (size_t)ncu * qr * QS + (size_t)nterm * KM * ((qr + QS) | 1) +
-                         (size_t)b * nf * KM * QS;
-        const size_t bytes = n * sizeof(double) + (size_t)b * (sizeof(int64_t) + 3 * sizeof(int));
-        if (bytes <= 200 * 1024) {
-            a.rc = rc;
-            a.rb = b;
-            a.km = KM;
-            a.qm = QS;
-            a.qrm = (int)qr;
-            smem = (bytes + 15) & ~(size_t)15;
-            return true;
-        }
+        qrs[k] = qr | 1;
     }
+    for (size_t budget : {(size_t)72 * 1024, (size_t)110 * 1024, (size_t)200 * 1024})
+        for (int rb = 8; rb >= 1; rb >>= 1)
+            for (int k = 0; k < 4; ++k) {
+                const int rc = 32 >> k;
+                if (budget < 200 * 1024 && (rc < 8 || rb < 8)) break;
+                const int64_t qr = qrs[k];
+                const size_t n = (size_t)nf * KM * QS + (size_t)ncu * qr * QS + (size_t)nterm * KM * ((qr + QS) | 1) +
+                                 (size_t)rb * a2;
+                const size_t bytes = n * sizeof(double);
+                if (bytes <= budget) {
+                    a.rc = rc;
+                    a.rb = rb;
+                    a.km = KM;
+                    a.qm = QS;
+                    a.qrm = (int)qr;
+                    smem = bytes;
+                    return true;
+                }
+            }
     return false;
 }
 
