@@ -140,6 +140,31 @@ __device__ __forceinline__ double dotn(const double *x, const double *y) {
     return s0 + s1;
 }
 
+
+// Stage 2 of one row for lane (g, t_1): acc[k] += sum_{c < N} A2[f][g + G k][c] y[c] with the lane's
+// Y row y (registers) reused across its KT/G trial rows t_2; A2 rows are read as 16-B pairs
+// (the same address for the lanes of a group: broadcasts)
+template <int N, int G, int NT2, int QA>
+__device__ __forceinline__ void sf2_rows(const double *__restrict__ A2f, const double *__restrict__ Yr, int g,
+                                         double (&acc)[NT2]) {
+    double y[N];
+    #pragma unroll
+    for (int c = 0; c < N; ++c) y[c] = Yr[c];
+    #pragma unroll
+    for (int k = 0; k < NT2; ++k) {
+        const double2 *ar = (const double2 *)(A2f + (g + G * k) * QA);
+        double s0 = 0.0, s1 = 0.0;
+        #pragma unroll
+        for (int c = 0; c + 1 < N; c += 2) {
+            const double2 v = ar[c / 2];
+            s0 = fma(v.x, y[c], s0);
+            s1 = fma(v.y, y[c + 1], s1);
+        }
+        if (N & 1) s0 = fma(A2f[(g + G * k) * QA + N - 1], y[N - 1], s0);
+        acc[k] += s0 + s1;
+    }
+}
+
 // Shared-memory layout (doubles), strides compile-time from the degree: QS = (3p+1)|1 point slots
 // per row (#Q_i <= 3p+1 when n_EL >= p+2), zero padded beyond the row's #Q:
 //   A1 [f][t_1][QS], Cs [u][r][QS] (r < QR, the chunk's points in q_2), Y [term][t_1][QY]
@@ -149,6 +174,9 @@ __global__ void __launch_bounds__(256) k_sf2l(Sf2lArgs a) {
     extern __shared__ __align__(16) double sm[];
     constexpr int KM = 2 * P + 1, QX = 3 * P + 1, QS = QX | 1, BS = wq_bstride(P);
     constexpr int NF = MASS ? 1 : 4, NT = NF, NCU = MASS ? 1 : 3;
+    // stage-2 lane map (g, t_1): G groups of KM lanes, each group NT2 trial rows t_2 = g + G k
+    // (rows KM .. KT-1 of A2 are zero); A2 rows padded to an even length QA (16-B pairs)
+    constexpr int G = 32 / KM, NT2 = (KM + G - 1) / G, KT = G * NT2, QA = QS + 1;
     const int tid = threadIdx.x, nth = blockDim.x;
     const int QR = a.qrm, QY = (QR + QS) | 1;  // odd: the lanes of stage 2 (consecutive t_1) hit distinct banks
     const DirView &v0 = a.v[0], &v1 = a.v[1];
@@ -162,7 +190,8 @@ __global__ void __launch_bounds__(256) k_sf2l(Sf2lArgs a) {
     double *A1 = sm;
     double *Cs = A1 + NF * KM * QS;
     double *Y = Cs + NCU * QR * QS;
-    double *A2 = Y + NT * KM * QY;        // per stage-2 warp: [f][t_2][QS]
+    // per stage-2 warp: [f][t_2 < KT][QA], 16-B aligned
+    double *A2 = sm + ((NF * KM * QS + NCU * QR * QS + NT * KM * QY + 1) & ~1);
     // A1: thread = point slot c of direction 1
     for (int c = tid; c < QS; c += nth) {
         double w[4] = {0.0, 0.0, 0.0, 0.0}, bv[2 * (P + 1)];
@@ -215,7 +244,7 @@ __global__ void __launch_bounds__(256) k_sf2l(Sf2lArgs a) {
     // stage 2: warp w < a.rb takes the rows i2a + w, i2a + w + rb, ...: its own A2 (no CTA barrier)
     const int warp = tid >> 5, lane = tid & 31;
     if (warp >= a.rb) return;
-    double *A2w = A2 + warp * (NF * KM * QS);
+    double *A2w = A2 + warp * (NF * KT * QA);
     for (int64_t i2 = i2a + warp; i2 < i2e; i2 += a.rb) {
         const int ni2 = v1.jlen[i2], nq2 = v1.qlen[i2];
         const int64_t jl2 = v1.jlo[i2], ql2 = v1.qlo[i2];
@@ -225,7 +254,7 @@ __global__ void __launch_bounds__(256) k_sf2l(Sf2lArgs a) {
             #pragma unroll
             for (int f = 0; f < NF; ++f)
                 #pragma unroll
-                for (int t = 0; t < KM; ++t) A2w[(f * KM + t) * QS + lane] = 0.0;
+                for (int t = 0; t < KT; ++t) A2w[(f * KT + t) * QA + lane] = 0.0;
             if (lane < nq2) {
                 const int64_t q = ql2 + lane;
                 const int t0 = (int)(v1.span[q] - jl2);
@@ -238,29 +267,58 @@ __global__ void __launch_bounds__(256) k_sf2l(Sf2lArgs a) {
                     if (t >= 0 && t < ni2) {
                         const double b0 = v1.B[q * BS + 2 * k], b1 = v1.B[q * BS + 2 * k + 1];
                         #pragma unroll
-                        for (int f = 0; f < NF; ++f) A2w[(f * KM + t) * QS + lane] = w[f] * ((f >> 1) ? b1 : b0);
+                        for (int f = 0; f < NF; ++f) A2w[(f * KT + t) * QA + lane] = w[f] * ((f >> 1) ? b1 : b0);
                     }
                 }
             }
         }
         __syncwarp();
         const int64_t off = a.g.offset(i1, i2, 0) - a.val_base;
-        // item (t_2, t_1): consecutive lanes store consecutive columns t_1 (two items per lane and
-        // iteration measured no faster: stage 2 is bound by its two shared loads per FMA)
-        for (int e = lane; e < KM * KM; e += 32) {
-            const int t2 = e / KM, t1 = e - t2 * KM;
-            if (t1 >= ni1 || t2 >= ni2) continue;
-            double s = 0.0;
-            #pragma unroll
-            for (int term = 0; term < NT; ++term) {
-                const int lt = term >> 1, mt = term & 1;
-                const int f2 = MASS ? 0 : (lt == 1) + 2 * (mt == 1);
-                const double *Ar = A2w + (f2 * KM + t2) * QS, *Yr = Y + (term * KM + t1) * QY + r0;
-                s += nq2 == 2 * P + 1 ? dotn<2 * P + 1>(Ar, Yr) : dotn<QX>(Ar, Yr);
+        if constexpr (P <= 8) {
+            // lane (g, t_1) forms the entries (t_1, g + G k): its Y row stays in registers across them
+            const int g = lane / KM, t1 = lane - g * KM;
+            if (g < G) {
+                double acc[NT2];
+                #pragma unroll
+                for (int k = 0; k < NT2; ++k) acc[k] = 0.0;
+                #pragma unroll
+                for (int term = 0; term < NT; ++term) {
+                    const int lt = term >> 1, mt = term & 1;
+                    const int f2 = MASS ? 0 : (lt == 1) + 2 * (mt == 1);
+                    const double *A2f = A2w + f2 * KT * QA, *Yr = Y + (term * KM + t1) * QY + r0;
+                    if (nq2 == 2 * P + 1) sf2_rows<2 * P + 1, G, NT2, QA>(A2f, Yr, g, acc);
+                    else sf2_rows<QX, G, NT2, QA>(A2f, Yr, g, acc);
+                }
+                if (t1 < ni1) {
+                    #pragma unroll
+                    for (int k = 0; k < NT2; ++k) {
+                        const int t2 = g + G * k;
+                        if (t2 < ni2) {
+                            const int64_t o = off + t1 + ni1 * t2;
+                            a.val[o] = acc[k];
+                            if (a.col) a.col[o] = (int32_t)((jl1 + t1) + a.g.n[0] * (jl2 + t2));
+                        }
+                    }
+                }
             }
-            const int64_t o = off + t1 + ni1 * t2;
-            a.val[o] = s;
-            if (a.col) a.col[o] = (int32_t)((jl1 + t1) + a.g.n[0] * (jl2 + t2));
+        } else {
+            // p >= 9: one entry per lane and pass (the register-blocked form spills here: measured
+            // 2D 1000^2 p = 10 mass 7.6 ms against 13.2)
+            for (int e = lane; e < KM * KM; e += 32) {
+                const int t2 = e / KM, t1 = e - t2 * KM;
+                if (t1 >= ni1 || t2 >= ni2) continue;
+                double s = 0.0;
+                #pragma unroll
+                for (int term = 0; term < NT; ++term) {
+                    const int lt = term >> 1, mt = term & 1;
+                    const int f2 = MASS ? 0 : (lt == 1) + 2 * (mt == 1);
+                    const double *Ar = A2w + (f2 * KT + t2) * QA, *Yr = Y + (term * KM + t1) * QY + r0;
+                    s += nq2 == 2 * P + 1 ? dotn<2 * P + 1>(Ar, Yr) : dotn<QX>(Ar, Yr);
+                }
+                const int64_t o = off + t1 + ni1 * t2;
+                a.val[o] = s;
+                if (a.col) a.col[o] = (int32_t)((jl1 + t1) + a.g.n[0] * (jl2 + t2));
+            }
         }
         __syncwarp();
     }
@@ -289,7 +347,8 @@ static bool sf2l_config(const wq_plan_s *P, int matrix, Sf2lArgs &a, size_t &sme
     const int64_t E1 = P->dir[1].E;
     // rc rows i_2 per CTA and rb stage-2 warps (each with its own A2): 8 warps and the largest
     // rc >= 8 that leave 3 CTAs per SM, else 2, else 1 (fewer warps before fewer rows)
-    const size_t a2 = (size_t)nf * KM * QS;
+    const int G = 32 / KM, KT = G * ((KM + G - 1) / G);
+    const size_t a2 = (size_t)nf * KT * (QS + 1);
     int64_t qrs[4];  // rc = 32, 16, 8, 4: max points in q_2 of a chunk, odd
     for (int k = 0; k < 4; ++k) {
         const int rc = 32 >> k;
@@ -308,8 +367,8 @@ static bool sf2l_config(const wq_plan_s *P, int matrix, Sf2lArgs &a, size_t &sme
                 const int rc = 32 >> k;
                 if (budget < 200 * 1024 && (rc < 8 || rb < 8)) break;
                 const int64_t qr = qrs[k];
-                const size_t n = (size_t)nf * KM * QS + (size_t)ncu * qr * QS + (size_t)nterm * KM * ((qr + QS) | 1) +
-                                 (size_t)rb * a2;
+                const size_t n = (((size_t)nf * KM * QS + (size_t)ncu * qr * QS + (size_t)nterm * KM * ((qr + QS) | 1) + 1) &
+                                  ~(size_t)1) + (size_t)rb * a2;
                 const size_t bytes = n * sizeof(double);
                 if (bytes <= budget) {
                     a.rc = rc;
