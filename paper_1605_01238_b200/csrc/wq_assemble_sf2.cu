@@ -192,6 +192,21 @@ __global__ void __launch_bounds__(256) k_sf2l(Sf2lArgs a) {
     double *Y = Cs + NCU * QR * QS;
     // per stage-2 warp: [f][t_2 < KT][QA], 16-B aligned
     double *A2 = sm + ((NF * KM * QS + NCU * QR * QS + NT * KM * QY + 1) & ~1);
+    // the chunk's coefficient values, zero padded beyond #Q_1: asynchronous 8-B copies (cp.async),
+    // in flight while the A1 table is built
+    #pragma unroll
+    for (int u = 0; u < NCU; ++u)
+        for (int x = tid; x < QR * QS; x += nth) {
+            const int r = x / QS, c = x - r * QS;
+            double *dst = Cs + u * QR * QS + x;
+            if (r < nr2 && c < nq1)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                             "l"(a.cv.ptr(MASS ? a.comp_mass : u, ql1 + c, q2a + r - a.cq_b, 0))
+                             : "memory");
+            else
+                *dst = 0.0;
+        }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     // A1: thread = point slot c of direction 1
     for (int c = tid; c < QS; c += nth) {
         double w[4] = {0.0, 0.0, 0.0, 0.0}, bv[2 * (P + 1)];
@@ -217,13 +232,7 @@ __global__ void __launch_bounds__(256) k_sf2l(Sf2lArgs a) {
             }
         }
     }
-    // the chunk's coefficient values, zero padded beyond #Q_1
-    for (int x = tid; x < NCU * QR * QS; x += nth) {
-        const int u = x / (QR * QS), e = x - u * QR * QS, r = e / QS, c = e - r * QS;
-        double cv = 0.0;
-        if (r < nr2 && c < nq1) cv = __ldg(a.cv.ptr(MASS ? a.comp_mass : u, ql1 + c, q2a + r - a.cq_b, 0));
-        Cs[x] = cv;
-    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     // stage 1: item (term, t_1, r); term (l, m) = (term >> 1, term & 1): family of direction 1
     // (l == 0) + 2 (m == 0), component C_{l+m} (C_01 = C_10)
