@@ -508,6 +508,10 @@ wq_status wq_plan_destroy(wq_plan P) {
     if (P->dnet) cudaFree(P->dnet);
     if (P->x2) cudaFree(P->x2);
     if (P->stage_val) cudaFree(P->stage_val);
+    for (cudaStream_t z : P->zfork)
+        if (z) cudaStreamDestroy(z);
+    for (cudaEvent_t e : P->zev)
+        if (e) cudaEventDestroy(e);
     delete P;
     return WQ_OK;
 }
@@ -578,13 +582,42 @@ static wq_status assemble_range(wq_plan_s *P, int matrix, wq_kernel kernel, doub
             return fail(WQ_EINVAL, "z-line kernel not available for this plan (stiffness, d = 3, 2 <= p <= 6)");
         const int64_t nu = (int64_t)P->zlines_uni.size(), ni = (int64_t)P->zlines_int.size(),
                       nb = (int64_t)P->zlines_bnd.size();
-        wq_status st = launch_assemble_zline(P, 0, P->zlines_dev, nu, pl_lo, pl_hi, val, col, val_base, s);
-        if (!st) st = launch_assemble_zline(P, 1, P->zlines_dev + nu, ni, pl_lo, pl_hi, val, col, val_base, s);
-        if (!st) {
+        // the three launches write disjoint rows: they run on forked streams so that the SMs a
+        // launch drains are refilled by the next one (C4 p = 4: 5.37 -> 5.26 ms, DESIGN.md §6;
+        // measurement switch WQ_ZL_FORK = 0 serial, 1 default, 2 boundary launch issued first)
+        static const char *fk = getenv("WQ_ZL_FORK");
+        const int fork = fk ? atoi(fk) : 1;
+        cudaStream_t s1 = s, s2 = s;
+        if (fork) {
+            cudaError_t ce = cudaSuccess;
+            for (int k = 0; k < 2 && ce == cudaSuccess; ++k)
+                if (!P->zfork[k]) ce = cudaStreamCreateWithFlags(&P->zfork[k], cudaStreamNonBlocking);
+            for (int k = 0; k < 3 && ce == cudaSuccess; ++k)
+                if (!P->zev[k]) ce = cudaEventCreateWithFlags(&P->zev[k], cudaEventDisableTiming);
+            if (ce == cudaSuccess) ce = cudaEventRecord(P->zev[0], s);
+            for (int k = 0; k < 2 && ce == cudaSuccess; ++k) ce = cudaStreamWaitEvent(P->zfork[k], P->zev[0], 0);
+            if (ce != cudaSuccess) return wq_cuda_status(ce, "z-line stream fork");
+            s1 = P->zfork[0];
+            s2 = P->zfork[1];
+        }
+        // order of issue: fork = 1 uniform, interior, boundary; fork = 2 boundary first
+        wq_status st = WQ_OK;
+        auto bnd = [&]() {
             // boundary lines: by the ZHP kernel's boundary class where that is measured faster
             // (zl_bnd_zhp), else the z-line kernel's boundary launch
-            if (zl_bnd_zhp(P)) st = launch_assemble_zhp(P, matrix, pl_lo, pl_hi, val, col, val_base, s, 2);
-            else st = launch_assemble_zline(P, 2, P->zlines_dev + nu + ni, nb, pl_lo, pl_hi, val, col, val_base, s);
+            if (zl_bnd_zhp(P)) return launch_assemble_zhp(P, matrix, pl_lo, pl_hi, val, col, val_base, s2, 2);
+            return launch_assemble_zline(P, 2, P->zlines_dev + nu + ni, nb, pl_lo, pl_hi, val, col, val_base, s2);
+        };
+        if (fork == 2) st = bnd();
+        if (!st) st = launch_assemble_zline(P, 0, P->zlines_dev, nu, pl_lo, pl_hi, val, col, val_base, s);
+        if (!st) st = launch_assemble_zline(P, 1, P->zlines_dev + nu, ni, pl_lo, pl_hi, val, col, val_base, s1);
+        if (!st && fork != 2) st = bnd();
+        if (fork) {
+            cudaError_t ce = cudaEventRecord(P->zev[1], s1);
+            if (ce == cudaSuccess) ce = cudaEventRecord(P->zev[2], s2);
+            if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s, P->zev[1], 0);
+            if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s, P->zev[2], 0);
+            if (!st && ce != cudaSuccess) st = wq_cuda_status(ce, "z-line stream join");
         }
         return st;
     }

@@ -103,6 +103,10 @@ struct wq_plan_s {
     // 1 usable (zuni_buf holds them), -1 not uniform
     int zuni_state;
     double zuni_buf[3 * 21 * 4 + 3 * 2 * 11 * 2];
+    // z-line: the interior and boundary launches run on two forked streams beside the uniform one
+    // (event fork / join on the caller's stream; created on first use)
+    cudaStream_t zfork[2] = {nullptr, nullptr};
+    cudaEvent_t zev[3] = {nullptr, nullptr, nullptr};
     int kernel_auto[2];            // wq_kernel AUTO runs for [mass, stiffness]
     // z-line (ZHP) kernel lines (i1 + n1 * i2): interior in directions 1 and 2 first (#Q = 2p+1),
     // then the rest; device copy zh_dev
