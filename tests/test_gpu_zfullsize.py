@@ -4,6 +4,8 @@ after the other on one GPU):
   - index arrays (row_ptr, col) compared IN FULL, streamed in plane chunks
     against the oracle's pattern generator (orc_pattern_rows, by definition of
     I_i, P:537-548), bit-exact;
+  - stiffness values on EVERY row through the zero-row-sum invariant of the WQ
+    stiffness matrix (pin P5; a property that holds at any size);
   - values on sampled rows (every boundary situation + seeded random rows; for
     C5 the corner blocks and rows on both sides of every slab seam) against the
     oracle's direct sums, per-row tolerance of reading R6.
@@ -49,6 +51,40 @@ def check_pattern_in_full(o, rp_dev, col_dev, row_begin, n_rows):
     return checked
 
 
+def stiffness_row_sums_every_row(rp_dev, val_dev, factor):
+    """Invariant of the WQ stiffness matrix that holds at any size and for any geometry (pin P5,
+    tests/test_oracle_pins.py::test_stiffness_row_sums_zero): sum_{j in I_i} D^b B_j = [b = 0] at
+    every point of Q_i, so every row of S~ sums to zero up to rounding.  Checked on EVERY row of the
+    device CSR: |sum_j s_ij| <= factor * #I_i * max_j |s_ij| (each entry carries at most the parity
+    tolerance of reading R6 relative to the row's largest entry; the callers pass 2e-14 for p <= 6
+    and 1e-12 for p >= 8, 35-75x above the worst ratios measured on the BASELINE configs:
+    3e-17 .. 3e-16 for p <= 6, 1.9e-15 at p = 8, 1.3e-14 at p = 10, profiles/r02_rowsum_every_row.log).
+    Returns the worst ratio |sum| / (#I_i max|s_ij|)."""
+    torch = _torch()
+    n_rows = rp_dev.numel() - 1
+    rp = rp_dev - rp_dev[0]
+    worst, r = 0.0, 0
+    budget = 1 << 27
+    rp_h = rp.cpu().numpy()
+    while r < n_rows:
+        r_hi = int(np.searchsorted(rp_h, rp_h[r] + budget, side="right")) - 1
+        r_hi = min(max(r_hi, r + 1), n_rows)
+        lens = rp[r + 1:r_hi + 1] - rp[r:r_hi]
+        idx = torch.repeat_interleave(torch.arange(r_hi - r, device=val_dev.device), lens)
+        v = val_dev[int(rp_h[r]):int(rp_h[r_hi])]
+        ssum = torch.zeros(r_hi - r, dtype=torch.float64, device=v.device).index_add_(0, idx, v)
+        smax = torch.zeros(r_hi - r, dtype=torch.float64, device=v.device).scatter_reduce_(0, idx, v.abs(), "amax")
+        assert bool((smax > 0).all()), "a row of zeros"
+        ratio = ssum.abs() / (lens.double() * smax)
+        w = float(ratio.max())
+        bad = int((ratio > factor).sum())
+        assert bad == 0, f"{bad} rows in [{r}, {r_hi}) break the zero row sum (worst ratio {w:.3e}, row {r + int(ratio.argmax())})"
+        worst = max(worst, w)
+        del idx, v, ssum, smax, ratio
+        r = r_hi
+    return worst
+
+
 @pytest.mark.parametrize("name,p,k_random", [("C2", None, 96), ("C3", None, 24), ("C4", 2, 48), ("C4", 3, 48),
                                              ("C4", 4, 32), ("C4", 6, 12), ("C4", 8, 4), ("C4", 10, 2)])
 def test_baseline_full_size(name, p, k_random):
@@ -75,6 +111,8 @@ def test_baseline_full_size(name, p, k_random):
         assert int(rp[-1]) == cfg.exact_nnz()
         if mat == STIFFNESS:
             assert check_pattern_in_full(o, rp, col, 0, info["n_rows_local"]) == cfg.exact_nnz()
+            print(name, p, "worst |row sum| / (#I max|s|) over every row:",
+                  stiffness_row_sums_every_row(rp, val, 2e-14 if cfg.p <= 6 else 1e-12))
         ptr, oc, ov, kappa, scale = o.rows(mat, rows)
         gptr, gc, gv = gather_rows_device(rp, col, val, rows)
         st = compare_rows(rows, gptr, gc, gv, ptr, oc, ov, kappa, scale, strict=cfg.p <= 6)
@@ -116,6 +154,7 @@ def test_C5_slabs():
         torch.cuda.synchronize()
         r0, nr = info["row_begin"], info["n_rows_local"]
         total_checked += check_pattern_in_full(o, rp, col, r0, nr)
+        print("C5 slab", s, "worst |row sum| / (#I max|s|) over every row:", stiffness_row_sums_every_row(rp, val, 2e-14))
         mine = want[(want >= r0) & (want < r0 + nr)]
         ptr, oc, ov, kappa, scale = o.rows(STIFFNESS, mine)
         gptr, gc, gv = gather_rows_device(rp - base, col, val, mine - r0)
