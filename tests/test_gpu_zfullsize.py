@@ -166,3 +166,74 @@ def test_C5_slabs():
         del rp, col, val
         torch.cuda.empty_cache()
     assert base == cfg.exact_nnz() == total_checked
+
+
+def mass_row_sums_oracle(o):
+    """sum_{j in I_i} m~_ij for every row i from the oracle's own tables, by the partition of unity
+    on Q_i (sum_{j in I_i} B_j = 1 at every point of Q_i; Eq. massquadrature):
+    sum_q w^(0,0)_{1,i1,q1} w^(0,0)_{2,i2,q2} w^(0,0)_{3,i3,q3} c(x_q), in long double.
+    Returns [n_3][n_2][n_1] flattened (row index i_1 fastest)."""
+    Wd = []
+    for l in range(3):
+        D = o.direction(l)
+        W = np.zeros((o.n[l], o.nq[l]), dtype=np.longdouble)
+        for i in range(o.n[l]):
+            lo, ln = int(D["qlo"][i]), int(D["qlen"][i])
+            W[i, lo:lo + ln] = D["w"][i, 0, :ln]
+        Wd.append(W)
+    ref, det, st = o.coef_box([0, 0, 0], list(o.nq))
+    assert st == 0
+    c = ref[:, 0].reshape(o.nq[2], o.nq[1], o.nq[0]).astype(np.longdouble)   # [q3][q2][q1]
+    t = np.einsum("ia,cba->cbi", Wd[0], c)
+    t = np.einsum("jb,cbi->cji", Wd[1], t)
+    t = np.einsum("kc,cji->kji", Wd[2], t)
+    return t.reshape(-1)
+
+
+@pytest.mark.parametrize("n_el,p", [(20, p) for p in range(1, 11)] + [(40, 3), (40, 6), (40, 10)])
+def test_mass_shapes_every_row(n_el, p):
+    """the paper's timing shapes (3D mass, 20^3 and 40^3 elements, Fig. 3),
+    AUTO kernel (tile for p <= 3, ZHP above): index arrays in full against the oracle pattern;
+    values of sampled rows against the oracle's direct sums; and the values of EVERY row through
+    their row sum against the oracle's weights and coefficient field (mass_row_sums_oracle)."""
+    torch = _torch()
+    from wqinputs import Config
+    cfg = Config(f"M{n_el}p{p}", 3, p, n_el, "grid", 0.1, ("mass",))
+    ks, ctrl = cfg.knots(), cfg.ctrl()
+    o = Oracle(p, ks, ctrl)
+    plan = wq.Plan(p, ks, ctrl=ctrl, need_mass=True, need_stiffness=False)
+    info = plan.info
+    rp, col, val = plan.alloc_csr()
+    wq.wq_pattern(plan.h, 0, rp)
+    wq.wq_assemble(plan.h, MASS, val, col)
+    wq.wq_check(plan.h)
+    torch.cuda.synchronize()
+    assert int(rp[-1]) == cfg.exact_nnz()
+    assert check_pattern_in_full(o, rp, col, 0, info["n_rows_local"]) == cfg.exact_nnz()
+    # every row: row sums
+    n_rows = info["n_rows_local"]
+    lens = rp[1:] - rp[:-1]
+    idx = torch.repeat_interleave(torch.arange(n_rows, device=val.device), lens)
+    ssum = torch.zeros(n_rows, dtype=torch.float64, device=val.device).index_add_(0, idx, val)
+    smax = torch.zeros(n_rows, dtype=torch.float64, device=val.device).scatter_reduce_(0, idx, val.abs(), "amax")
+    del idx
+    want = mass_row_sums_oracle(o)
+    got = ssum.cpu().numpy().astype(np.longdouble)
+    ratio = np.abs(got - want) / (lens.cpu().numpy() * smax.cpu().numpy())
+    # measured worst ratios (profiles/r02_mass_shapes.log): <= 1.9e-14 for p <= 6; 1.3e-13, 2.9e-13, 2.2e-12,
+    # 1.4e-11 at p = 7..10 (boundary rows, kappa_i up to 3e7: the weights alternate in sign)
+    factor = 2e-13 if p <= 6 else 2e-10
+    print(f"mass {n_el}^3 p={p}", wq.KERNEL_NAMES[info["kernel"][0]], "worst |row sum - oracle| / (#I max|m|):",
+          float(ratio.max()), "row", int(ratio.argmax()))
+    assert float(ratio.max()) <= factor
+    # sampled rows, entry by entry
+    n = n_el + p
+    rows = sample_rows(n, 3, p, k_random=8, seed=2)
+    if p >= 5:
+        rows = rows[:: max(1, len(rows) // (40 if p <= 7 else 16))]
+    ptr, oc, ov, kappa, scale = o.rows(MASS, rows)
+    gptr, gc, gv = gather_rows_device(rp, col, val, rows)
+    # these small shapes reach kappa_i ~ 1e4 on corner rows at p = 6 (DESIGN.md R6): strict regime for p <= 5
+    st = compare_rows(rows, gptr, gc, gv, ptr, oc, ov, kappa, scale, strict=p <= 5)
+    print(f"mass {n_el}^3 p={p}", st)
+    plan.close()

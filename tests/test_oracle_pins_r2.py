@@ -242,3 +242,18 @@ def test_kappa_recomputed_from_tables(mat):
         kap = abs_sum.max() / np.abs(vals).max()
         assert abs(kappa[k] - kap) <= 1e-10 * kap, (r, kappa[k], kap)
         assert abs(scale[k] - abs_sum.max()) <= 1e-12 * abs_sum.max()
+
+
+@pytest.mark.parametrize("p,E", [(2, 4), (3, 3)])
+def test_mass_row_sum_identity_used_by_gpu_tests(p, E):
+    """The every-row mass check of tests/test_gpu_zfullsize.py compares device row sums with
+    sum_q w1 w2 w3 c(x_q) built from the oracle's weights and coefficient field (partition of unity
+    on Q_i, Eq. massquadrature).  Here that helper is checked against the row sums of the
+    oracle's dense mass matrix on a perturbed 3D geometry (index order, family, point ranges)."""
+    from test_gpu_zfullsize import mass_row_sums_oracle
+    ks = [uniform_open_knots(p, E)] * 3
+    ctrl = control_net("grid", p, ks, 0.1, seed=0)
+    o = Oracle(p, ks, ctrl)
+    M = o.dense(MASS)
+    w = mass_row_sums_oracle(o).astype(np.float64)
+    assert np.abs(M.sum(axis=1) - w).max() <= 1e-13 * np.abs(M).max()
