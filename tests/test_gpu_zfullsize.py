@@ -237,3 +237,54 @@ def test_mass_shapes_every_row(n_el, p):
     st = compare_rows(rows, gptr, gc, gv, ptr, oc, ov, kappa, scale, strict=p <= 5)
     print(f"mass {n_el}^3 p={p}", st)
     plan.close()
+
+
+@pytest.mark.parametrize("p", [2, 4, 6])
+def test_2d_1000_every_row(p):
+    """The d = 2 entries of the bench sweep (1000^2 elements, k_sf2l), both matrices: indices in
+    full; stiffness of EVERY row through the zero row sum; mass of EVERY row through its row sum
+    against the oracle's weights and coefficient field; sampled rows entry by entry."""
+    torch = _torch()
+    from wqinputs import Config
+    cfg = Config(f"2D1000p{p}", 2, p, 1000, "grid", 0.1, ("stiffness", "mass"))
+    ks, ctrl = cfg.knots(), cfg.ctrl()
+    o = Oracle(p, ks, ctrl)
+    plan = wq.Plan(p, ks, ctrl=ctrl, need_mass=True, need_stiffness=True)
+    info = plan.info
+    rp, col, val = plan.alloc_csr()
+    wq.wq_pattern(plan.h, 0, rp)
+    n = cfg.n_el + p
+    rows = sample_rows(n, 2, p, k_random=64, seed=3)
+    for mat in (STIFFNESS, MASS):
+        wq.wq_assemble(plan.h, mat, val, col)
+        wq.wq_check(plan.h)
+        torch.cuda.synchronize()
+        assert int(rp[-1]) == cfg.exact_nnz()
+        if mat == STIFFNESS:
+            assert check_pattern_in_full(o, rp, col, 0, info["n_rows_local"]) == cfg.exact_nnz()
+            print("2D 1000^2 p =", p, "stiffness worst |row sum| / (#I max|s|):", stiffness_row_sums_every_row(rp, val, 2e-14))
+        else:
+            Wd = []
+            for l in range(2):
+                D = o.direction(l)
+                W = np.zeros((o.n[l], o.nq[l]))
+                for i in range(o.n[l]):
+                    lo, ln = int(D["qlo"][i]), int(D["qlen"][i])
+                    W[i, lo:lo + ln] = D["w"][i, 0, :ln]
+                Wd.append(W)
+            ref, det, st = o.coef_box([0, 0], list(o.nq))
+            assert st == 0
+            c = ref[:, 0].reshape(o.nq[1], o.nq[0])          # [q2][q1]
+            want = (Wd[1] @ c @ Wd[0].T).reshape(-1)          # [i2][i1]
+            lens = rp[1:] - rp[:-1]
+            idx = torch.repeat_interleave(torch.arange(lens.numel(), device=val.device), lens)
+            ssum = torch.zeros(lens.numel(), dtype=torch.float64, device=val.device).index_add_(0, idx, val)
+            smax = torch.zeros(lens.numel(), dtype=torch.float64, device=val.device).scatter_reduce_(0, idx, val.abs(), "amax")
+            ratio = np.abs(ssum.cpu().numpy() - want) / (lens.cpu().numpy() * smax.cpu().numpy())
+            print("2D 1000^2 p =", p, "mass worst |row sum - oracle| / (#I max|m|):", float(ratio.max()))
+            assert float(ratio.max()) <= 2e-13
+        ptr, oc, ov, kappa, scale = o.rows(mat, rows)
+        gptr, gc, gv = gather_rows_device(rp, col, val, rows)
+        st = compare_rows(rows, gptr, gc, gv, ptr, oc, ov, kappa, scale, strict=p <= 5)
+        print("2D 1000^2 p =", p, mat, wq.KERNEL_NAMES[info["kernel"][mat]], st)
+    plan.close()
