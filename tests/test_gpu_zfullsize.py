@@ -113,6 +113,17 @@ def test_baseline_full_size(name, p, k_random):
             assert check_pattern_in_full(o, rp, col, 0, info["n_rows_local"]) == cfg.exact_nnz()
             print(name, p, "worst |row sum| / (#I max|s|) over every row:",
                   stiffness_row_sums_every_row(rp, val, 2e-14 if cfg.p <= 6 else 1e-12))
+        if mat == MASS and cfg.d == 3 and info["nnz_local"] <= (1 << 28):
+            # every row of the mass matrix through its row sum against the oracle's tables
+            lens = rp[1:] - rp[:-1]
+            idx = torch.repeat_interleave(torch.arange(lens.numel(), device=val.device), lens)
+            ssum = torch.zeros(lens.numel(), dtype=torch.float64, device=val.device).index_add_(0, idx, val)
+            smax = torch.zeros(lens.numel(), dtype=torch.float64, device=val.device).scatter_reduce_(0, idx, val.abs(), "amax")
+            want = mass_row_sums_oracle(o).astype(np.float64)
+            ratio = np.abs(ssum.cpu().numpy() - want) / (lens.cpu().numpy() * smax.cpu().numpy())
+            print(name, p, "mass worst |row sum - oracle| / (#I max|m|) over every row:", float(ratio.max()))
+            assert float(ratio.max()) <= 2e-13
+            del idx
         ptr, oc, ov, kappa, scale = o.rows(mat, rows)
         gptr, gc, gv = gather_rows_device(rp, col, val, rows)
         st = compare_rows(rows, gptr, gc, gv, ptr, oc, ov, kappa, scale, strict=cfg.p <= 6)
